@@ -1,0 +1,470 @@
+#!/usr/bin/env python
+"""TETRIS hot-path benchmark on B200: select (prefix product + global top-C) -> verify (rejection sampling + residual /
+bonus resample) -> compact, one "step" = one verification step of a batch of requests.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl tetris|reference]
+
+Default workload: BASELINE.json configs[2] ("cfg3": B=1024 requests, k=16, C=8192, V=128256, stochastic), the
+configuration the north-star target is quoted on, per GPU; with N GPUs requests are sharded (B=1024 per rank, global
+capacity 8192*N enforced by an NCCL all-gather of the candidate scores) -> weak scaling.  Inputs are synthetic
+(paper_2502_15197_b200/synthetic.py), resident in HBM before the timed region, and larger than L2 (17.3 GB per set,
+two sets rotated).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "cfg1": dict(B=16, k=5, C=48, V=32000, mode="greedy"),
+    "cfg2": dict(B=256, k=8, C=1024, V=32000, mode="stochastic"),
+    "cfg3": dict(B=1024, k=16, C=8192, V=128256, mode="stochastic"),
+    # cfg5: B=16384 requests sharded over the GPUs (strong scaling), C assumed B*8
+    "cfg5": dict(B=16384, k=16, C=131072, V=128256, mode="stochastic", strong=True),
+}
+METRIC = "verified tokens/sec"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peak_hbm():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is under load."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        load = [x for x in sm if x > 500] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------------------------------
+def _setup_dist(n_gpus: int):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if n_gpus > 1 and world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch with torchrun --nproc-per-node {n_gpus}")
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local, group
+
+
+def _barrier(group):
+    if group is not None:
+        import torch.distributed as dist
+
+        dist.barrier(group=group)
+
+
+def _max_over_ranks(x: float, group) -> float:
+    if group is None:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def _sum_over_ranks(x: float, group) -> float:
+    if group is None:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item())
+
+
+def _verify_bytes(cfg, windows, accepted):
+    """Algorithmic bytes of one stochastic verify launch: one fp32 vocabulary row per request
+    (bonus) or two (residual after a rejection), plus per selected position the two gathered probabilities (8 B),
+    the draft token (4 B) and its uniform (8 B), plus per request window, u_res, accepted, token (24 B)."""
+    V = cfg["V"]
+    if cfg["mode"] == "greedy":
+        return int((windows.sum() + len(windows)) * V * 4 + 20 * windows.sum() + 24 * len(windows))
+    rej = (accepted < windows).sum()
+    return int(len(windows) * V * 4 + rej * V * 4 + 20 * windows.sum() + 24 * len(windows))
+
+
+def _load_traffic(config_name: str):
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(f.read_text())
+        return d.get(config_name)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------------------------------------
+def run_tetris(args):
+    import numpy as np
+    import torch
+
+    from paper_2502_15197_b200 import ops
+    from paper_2502_15197_b200.synthetic import make_batch
+
+    world, rank, local, group = _setup_dist(args.gpus)
+    cfg = dict(CONFIGS[args.config])
+    if cfg.get("strong"):
+        B_local = cfg["B"] // world
+        C = cfg["C"]
+    else:
+        B_local = cfg["B"]
+        C = cfg["C"] * world
+    k, V, mode = cfg["k"], cfg["V"], cfg["mode"]
+    dev = torch.device("cuda", local)
+    nsets = args.sets
+    sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
+            for s in range(nsets)]
+    step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None)
+
+    def run(i, events=None):
+        bt = sets[i % nsets]
+        step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, events=events)
+
+    # per-set verified tokens / bytes (the step is deterministic for a given input set)
+    tokens_per_set, bytes_per_set = [], []
+    for s in range(nsets):
+        run(s)
+        torch.cuda.synchronize()
+        ops.raise_for_status(step.status, "bench")
+        tokens_per_set.append(int(step.offsets[-1].item()))
+        w = step.windows.cpu().numpy().astype(np.int64)
+        a = step.accepted.cpu().numpy().astype(np.int64)
+        bytes_per_set.append(_verify_bytes(cfg, w, a))
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for i in range(args.warmup):
+        run(i)
+    torch.cuda.synchronize()
+    _barrier(group)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(args.steps):
+        run(i, ev[i])
+    t1.record()
+    torch.cuda.synchronize()
+    _barrier(group)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    elapsed_ms = t0.elapsed_time(t1)
+    sel_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    ver_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    cmp_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    local_tokens = sum(tokens_per_set[i % nsets] for i in range(args.steps))
+    alg_bytes = sum(bytes_per_set[i % nsets] for i in range(args.steps))
+    max_ms = _max_over_ranks(elapsed_ms, group)
+    total_tokens = _sum_over_ranks(float(local_tokens), group)
+    verify_avg_s = sum(ver_ms) / len(ver_ms) / 1e3
+    achieved = alg_bytes / args.steps / verify_avg_s / 1e9
+    peak, peak_kind = _peak_hbm()
+    # sanity: the results did not change over the timed steps
+    assert int(step.offsets[-1].item()) == tokens_per_set[(args.steps - 1) % nsets]
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(args, cfg, step, sets[0], B_local, k, V, C, mode, group, world, dev)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline(cfg, sets[0], step, B_local, C, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": total_tokens / (max_ms / 1e3),
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong" if cfg.get("strong") else "weak",
+            "vs_baseline": None,
+            "dtype": "f32 probabilities, f64 accumulation",
+            "data": "synthetic (seeded spiked-softmax draft/target distributions, paper_2502_15197_b200/synthetic.py)",
+            "config": {"workload": f"{args.config}: B={B_local * world} k={k} C={C} V={V} {mode}",
+                       "B_per_gpu": B_local, "k": k, "C": C, "V": V, "verify": mode, "input_sets": nsets,
+                       "l2": "inputs larger than L2 (%.1f GB per set), %d sets rotated" % (
+                           (B_local * ((k + 1) + k) * V * 4) / 1e9, nsets),
+                       "parallelism": f"request-sharded dp{world}" + (" + NCCL all-gather select" if world > 1 else "")},
+            "stage_us": {"select": 1e3 * statistics.median(sel_ms), "verify": 1e3 * statistics.median(ver_ms),
+                         "compact": 1e3 * statistics.median(cmp_ms)},
+            "select_verify_latency_us": 1e3 * statistics.median([a + b for a, b in zip(sel_ms, ver_ms)]),
+            "tokens_per_step": total_tokens / args.steps,
+            "roofline": {"bound": "hbm", "kernel": "sample_kernel<float,VEC,FUSED> (tetris_verify_stochastic_f32)"
+                         if mode == "stochastic" else "greedy_kernel", "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "alg_bytes_per_launch": alg_bytes / args.steps,
+                         "traffic": _load_traffic(args.config)},
+            "clocks": clk,
+            "gpu_launches": ops.TetrisStep.launches_per_step * args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def _e2e(args, cfg, step_dev, bt, B, k, V, C, mode, group, world, dev):
+    """Same metric through the host-buffer API: inputs in pinned host memory, small per-request inputs copied H2D,
+    p/q rows read zero-copy by the streaming kernel, the compacted token stream copied D2H, every step."""
+    import torch
+
+    from paper_2502_15197_b200 import ops
+
+    try:
+        p_h = torch.empty(bt.p.shape, dtype=bt.p.dtype, pin_memory=True)
+        p_h.copy_(bt.p)
+        q_h = torch.empty(bt.q.shape, dtype=bt.q.dtype, pin_memory=True)
+        q_h.copy_(bt.q)
+        small = [t.cpu().pin_memory() for t in (bt.conf, bt.lengths, bt.d, bt.u_acc, bt.u_res)]
+    except RuntimeError as e:
+        return {"value": None, "unit": "tokens/s", "error": f"pinned host allocation failed: {e}"[:200]}
+    hs = ops.HostTetrisStep(B, k, V, C, p_h, q_h, mode=mode, device=dev)
+    if world > 1:
+        hs.step = ops.TetrisStep(B, k, V, C, mode=mode, device=dev, group=group)
+    steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        hs.run(*small)
+    torch.cuda.synchronize()
+    ref_tokens = int(hs.offsets_host[-1])
+    _barrier(group)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        hs.run(*small)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(t0.elapsed_time(t1), group)
+    toks = _sum_over_ranks(float(int(hs.offsets_host[-1]) * steps), group)
+    assert int(hs.offsets_host[-1]) == ref_tokens
+    w = hs.step.windows.cpu().numpy()
+    a = hs.accepted_host.numpy()
+    zero_copy = _verify_bytes(cfg, w.astype("int64"), a.astype("int64"))
+    del p_h, q_h
+    return {"value": toks / (ms / 1e3), "unit": "tokens/s", "steps": steps, "ms_per_step": ms / steps,
+            "h2d_bytes_per_step": hs.h2d_bytes() + zero_copy, "d2h_bytes_per_step": hs.d2h_bytes(),
+            "h2d_mode": "explicit copies of conf/lengths/draft tokens/uniforms (%d B) + zero-copy kernel reads of the "
+                        "needed p/q rows from pinned host memory (%d B)" % (hs.h2d_bytes(), zero_copy)}
+
+
+def _cpu_baseline(cfg, bt, step, B, C, args):
+    """The reference algorithm (oracle/reference_port.py: heapq select + numpy verify/residual/choice) on the host
+    cores, on a bounded sample: the full selection plus verification of the first `n` requests, scaled to the
+    whole batch (requests are independent).  Also reports how many sampled requests emit the same token as the GPU."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    n = min(B, args.cpu_sample)
+    h = _reference_step_inputs(bt, n)
+    threads = os.cpu_count() or 1
+    t_sel, t_ver, toks, out = _time_reference(h, C, n, cfg["mode"], threads)
+    scale = B / n
+    step_s = t_sel + t_ver * scale
+    agree = None
+    if args.sets >= 1:
+        # step currently holds the results of the last timed step; recompute set 0 for the comparison
+        step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+        acc = step.accepted.cpu().numpy()[:n]
+        tok = step.out_tok.cpu().numpy()[:n]
+        agree = int(sum(1 for b, (a, x) in enumerate(out) if a == acc[b] and x == tok[b]))
+    return {"value": toks * scale / step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"full selection over B={B} + verification of {n}/{B} requests, scaled x{scale:.1f} "
+                      f"(select {t_sel * 1e3:.1f} ms, verify {t_ver * 1e3:.1f} ms for the sample)",
+            "cpu_model": _cpu_model(), "gpu_agreement": f"{agree}/{n} requests identical (accepted, token)"}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _reference_step_inputs(bt, n):
+    """Host numpy copies of one input set (the CPU arm reads from host RAM like a CPU server would); the vocabulary
+    rows only for the first n requests (the bounded sample), the per-request scalars for all."""
+    return {"p": bt.p[:n].cpu().numpy(), "q": bt.q[:n].cpu().numpy(), "d": bt.d.cpu().numpy(),
+            "conf": bt.conf.cpu().numpy(), "lengths": bt.lengths.cpu().numpy(), "u_acc": bt.u_acc.cpu().numpy(),
+            "u_res": bt.u_res.cpu().numpy()}
+
+
+def _time_reference(h, C, n, mode, threads):
+    """One reference step: select_tetris(cumulative_products(conf)) then verify requests [0, n) on `threads`
+    threads.  Returns (select seconds, verify seconds, emitted tokens in the sample, None)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import reference_port as RP
+
+    rows = [list(map(float, h["conf"][b, : h["lengths"][b]])) for b in range(h["conf"].shape[0])]
+    t0 = time.perf_counter()
+    windows, _ = RP.select_tetris(RP.cumulative_products(rows), C)
+    t1 = time.perf_counter()
+
+    def one(b):
+        if mode == "greedy":
+            return RP.verify_request_greedy(h["p"][b], h["d"][b], windows[b])
+        return RP.verify_request(h["p"][b], h["q"][b], h["d"][b], windows[b], h["u_acc"][b], h["u_res"][b])
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        out = list(ex.map(one, range(n)))
+    t2 = time.perf_counter()
+    toks = sum(a + 1 for a, _ in out)
+    return t1 - t0, t2 - t1, toks, out
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port) timed on the host cores, same metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    from paper_2502_15197_b200.synthetic import make_batch
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    cfg = dict(CONFIGS[args.config])
+    world = args.gpus
+    B = cfg["B"] // world if cfg.get("strong") else cfg["B"]
+    C = cfg["C"] if cfg.get("strong") else cfg["C"] * world
+    Bg = B * world
+    k, V, mode = cfg["k"], cfg["V"], cfg["mode"]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    # inputs: the same seeded synthetic batches as the GPU arm's input set 0 of every rank (torch generator only;
+    # none of this repo's kernels run here), moved to host RAM: per-request scalars for all Bg requests, the
+    # vocabulary rows for the first n requests (the bounded verification sample)
+    import numpy as np
+
+    n = min(B, args.cpu_sample)
+    parts = []
+    for r in range(world):
+        bt = make_batch(B, k, V, mode=mode, seed=args.seed + 7919 * r, device=dev)
+        parts.append(_reference_step_inputs(bt, n if r == 0 else 0))
+        del bt
+    h = dict(parts[0])
+    for key in ("d", "conf", "lengths", "u_acc", "u_res"):
+        h[key] = np.concatenate([pt[key] for pt in parts])
+    threads = os.cpu_count() or 1
+    for _ in range(max(0, min(args.warmup, 1))):
+        _time_reference(h, C, n, mode, threads)
+    sel, ver, toks = 0.0, 0.0, 0
+    for _ in range(args.steps):
+        a, b, t, _ = _time_reference(h, C, n, mode, threads)
+        sel, ver, toks = sel + a, ver + b, toks + t
+    scale = Bg / n
+    step_s = (sel + ver * scale) / args.steps
+    value = (toks / args.steps) * scale / step_s
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None, "impl": "reference",
+            "dtype": "f32 probabilities, f64 accumulation (numpy)", "data": "synthetic",
+            "config": {"workload": f"{args.config}: B={Bg} k={k} C={C} V={V} {mode}", "B_per_gpu": B, "k": k,
+                       "C": C, "V": V, "verify": mode},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                             "sample": f"per step: full selection over B={Bg} + verification of {n} requests "
+                                       f"(scaled x{scale:.1f})", "cpu_model": _cpu_model()},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="tetris", choices=["tetris", "reference"])
+    ap.add_argument("--sets", type=int, default=2, help="input sets rotated between steps")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=256, help="requests verified by the CPU baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)  # timing rule: at least 3 untimed warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_tetris(args)
+
+
+if __name__ == "__main__":
+    main()

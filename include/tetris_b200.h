@@ -1,0 +1,157 @@
+/*
+ * tetris_b200.h — C ABI of the B200-native TETRIS batch speculative-decoding hot path.
+ *
+ * The reference (arXiv 2502.15197, package `tetris_sched` 0.1.0 under /root/reference/pkg) exposes this path as
+ * plain Python module functions; there is no FFI of its own.  Each entry point below names the reference function
+ * whose semantics it implements (file:line, paths relative to /root/reference/pkg/src/tetris_sched/).  The Python
+ * drop-in adapters in paper_2502_15197_b200/{selector,accept_model,sim_engine}.py bind these symbols through ctypes
+ * and keep the reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers (or host pointers registered/mapped for device access) owned by the caller;
+ *     the library allocates nothing persistent.  Scratch space comes from a caller-provided workspace that must be
+ *     zeroed once with tetris_workspace_init() (kernels leave their arrival counters at zero after every call).
+ *   - Everything is stream-ordered on the caller's `stream`; no entry point synchronises the host.  The ABI is
+ *     reentrant: no mutable globals besides the thread-local last-error string.
+ *   - Host-checkable argument errors return TETRIS_INVALID_ARGUMENT immediately.  Data-dependent errors found on the
+ *     device are OR-ed into the caller's device word `status` (TETRIS_ST_* bits); the host adapter reads it when it
+ *     materialises results and raises the reference's exception.
+ *   - Layouts are row-major and dense: conf/cum/alpha [B][k] f64, lengths [B] i32, draft tokens d [B][k] i32,
+ *     target probabilities p [B][k+1][V] (the extra position is the bonus row), draft probabilities q [B][k][V].
+ */
+#ifndef TETRIS_B200_H_
+#define TETRIS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tetris_stream_t; /* == cudaStream_t */
+
+/* ---- return codes (host) ---------------------------------------------------------------------------------- */
+#define TETRIS_OK 0
+#define TETRIS_INVALID_ARGUMENT 1   /* -> ValueError (selector.py:145-146, accept_model.py:284-288, :304-308) */
+#define TETRIS_DEGENERATE_RESIDUAL 2 /* -> DegenerateResidualError (accept_model.py:28-29, :323-326)           */
+#define TETRIS_CUDA_ERROR 3
+
+/* ---- device status bits (OR-ed into *status by kernels) ----------------------------------------------------- */
+#define TETRIS_ST_BAD_VALUE 1u     /* alpha / cum NaN or (conf mode) outside [0,1]  (accept_model.py:55-59)       */
+#define TETRIS_ST_DEGENERATE 2u    /* residual / bonus row with zero mass           (accept_model.py:323-326)     */
+#define TETRIS_ST_BAD_TOKEN 4u     /* draft token outside [0,V)                     (accept_model.py:305-306)     */
+#define TETRIS_ST_BAD_UNIFORM 8u   /* uniform outside [0,1)                         (accept_model.py:307-308)     */
+#define TETRIS_ST_BAD_WINDOW 16u   /* window deeper than the row                    (sim_engine.py:389-392)       */
+
+/* ---- the sampling contract ---------------------------------------------------------------------------------
+ * Inverse-CDF sampling of a weight row w[0..V) with a uniform u (accept_model.py:364,368 use numpy's
+ * Generator.choice = searchsorted(cumsum(p)/cumsum[-1], u, 'right')).  The GPU and the CPU oracle
+ * (oracle/tetris_oracle.c) both follow ONE fixed fp64 summation hierarchy, every node a contiguous index range:
+ *   lane  = TETRIS_LANE_ELEMS consecutive elements, summed left to right;
+ *   seg   = 32 lanes, balanced binary tree (xor-butterfly order);
+ *   warp  = TETRIS_WARP_SEGS consecutive segs, summed left to right;
+ *   chunk = TETRIS_CHUNK_WARPS consecutive warps, summed left to right;
+ *   row   = ceil(V / TETRIS_CHUNK_ELEMS) chunks, summed left to right -> mass.
+ * T = u*mass; descend: at a left-to-right node take the first child whose running prefix exceeds T (T -= prefix
+ * before it); at a binary node go left iff left > T or right == 0 (else T -= left).  When no child qualifies the
+ * descent takes the last child with positive mass and continues with T = +inf (i.e. last positive leaf). */
+#define TETRIS_LANE_ELEMS 8
+#define TETRIS_SEG_ELEMS (32 * TETRIS_LANE_ELEMS)                   /* 256  */
+#define TETRIS_WARP_SEGS 4
+#define TETRIS_CHUNK_WARPS 8
+#define TETRIS_CHUNK_ELEMS (TETRIS_SEG_ELEMS * TETRIS_WARP_SEGS * TETRIS_CHUNK_WARPS) /* 8192 */
+
+#define TETRIS_MAX_K 255        /* depth fits the 8-bit tie-break field of the selection key                  */
+#define TETRIS_MAX_SELECT_ROWS 65535
+
+/* ---- workspace ------------------------------------------------------------------------------------------- */
+#define TETRIS_OP_SELECT 1
+#define TETRIS_OP_VERIFY 2   /* verify_stochastic / verify_greedy / sample_rows / residual                      */
+#define TETRIS_OP_ALL 3
+size_t tetris_workspace_bytes(int op, int32_t B, int32_t k, int32_t V);
+int tetris_workspace_init(void* ws, size_t ws_bytes, tetris_stream_t stream);
+
+const char* tetris_last_error(void);
+
+/* Zero-copy access to host-resident inputs: returns in *dev_ptr the device address of pinned host memory
+ * [host_ptr, host_ptr+bytes) (registering it as mapped/portable when it is not pinned yet), so the streaming kernels
+ * can read p/q rows straight from host RAM over PCIe/C2C and only the touched rows cross the link. */
+int tetris_map_host(void* host_ptr, size_t bytes, void** dev_ptr);
+int tetris_abi_version(void);
+
+/* Stages (1)+(2): prefix products and capacity-constrained greedy selection.
+ * Replaces cumulative_products (selector.py:95-110) + select_tetris (selector.py:133-176).
+ * vals_are_cum = 0: vals are acceptance rates alpha (AcceptanceMatrix rows, accept_model.py:37-70) and
+ *   cum[b][j] = ((alpha[b][0]*alpha[b][1])*...)*alpha[b][j] left to right in fp64 (selector.py:104-108).
+ * vals_are_cum = 1: vals are given Candidate.cum scores (selector.py:32-39), used as-is.
+ * The selection is the global top-C under key (cum desc, row asc, depth asc) (_HeapItem, selector.py:113-130)
+ * over each row's prefix-min envelope, which equals the heap merge exactly.  len may be NULL (all rows = k).
+ * Outputs: windows[B]; optional win_offsets[B+1] (exclusive scan of windows), cum_out[B][k] (raw cum; cells
+ * past len untouched), stats4 = {extracts, inserts, peak_queue, -1} (PolicyStats, selector.py:85-92; the heapq
+ * comparison count is produced only by tetris_heap_stats_f64). */
+int tetris_select_f64(const double* vals, const int32_t* len, int32_t B, int32_t k, int64_t C,
+                      int32_t vals_are_cum, int32_t* windows, int32_t* win_offsets, double* cum_out,
+                      int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+
+/* Exact replay of select_tetris's heapq schedule (selector.py:151-170) to produce PolicyStats including
+ * `comparisons` (every _HeapItem.__lt__ call, selector.py:128-130).  Single-thread device kernel; accounting
+ * only — not on the hot path.  cum[B][k] raw Candidate.cum values. */
+int tetris_heap_stats_f64(const double* cum, const int32_t* len, int32_t B, int32_t k, int64_t C,
+                          int64_t* stats4, void* ws, size_t ws_bytes, tetris_stream_t stream);
+
+/* expected_accepted (selector.py:286-306): one fp64 running sum over the selected cells in row order. */
+int tetris_expected_accepted_f64(const double* alpha, const int32_t* len, const int32_t* windows, int32_t B,
+                                 int32_t k, double* out, uint32_t* status, tetris_stream_t stream);
+
+/* Matrix-level cascade verification, apply_verification (sim_engine.py:374-404).  Row b consumes the uniforms
+ * u[win_offsets[b] .. win_offsets[b]+windows[b]) (== numpy rng.random(w_b) per row in row order); accepted[b] is
+ * the count before the first u >= alpha. */
+int tetris_verify_matrix_f64(const double* alpha, const int32_t* len, const int32_t* windows,
+                             const int32_t* win_offsets, const double* u, int32_t B, int32_t k,
+                             int32_t* accepted, uint32_t* status, tetris_stream_t stream);
+
+/* Stage (3) stochastic: per request b, positions j < windows[b] are tested with verify_token's rule
+ * (accept_model.py:309-313): s=(double)q[b][j][d], m=(double)p[b][j][d]; accept iff s<=m or u<m/s.
+ * accepted[b] = first rejection (or windows[b]).  On rejection the emitted token is sampled (sampling contract
+ * above, uniform u_res[b]) from max(0, p[b][a]-q[b][a]) (residual_distribution, accept_model.py:316-327);
+ * if every selected token is accepted it is sampled from p[b][windows[b]] (bonus; sim_engine.py:407-409).
+ * u_acc layout: win_offsets == NULL -> dense u_acc[b*k + j]; else packed u_acc[win_offsets[b] + j].
+ * mass_out[b] (nullable) receives the row mass.  out_tok[b] = -1 with TETRIS_ST_DEGENERATE on zero mass. */
+int tetris_verify_stochastic_f32(const float* p, const float* q, const int32_t* d, const int32_t* windows,
+                                 const int32_t* win_offsets, const double* u_acc, const double* u_res,
+                                 int32_t B, int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
+                                 double* mass_out, uint32_t* status, void* ws, size_t ws_bytes,
+                                 tetris_stream_t stream);
+
+/* Stage (3) greedy: verify_token on one-hot distributions (accept_model.py:309-313): position j is accepted iff
+ * d[b][j] == argmax_v p[b][j][v] (first maximal index, NaN ranks highest as in numpy.argmax); the emitted token is
+ * the argmax at the first mismatch, or at windows[b] (bonus). */
+int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B, int32_t k,
+                             int32_t V, int32_t* accepted, int32_t* out_tok, uint32_t* status, void* ws,
+                             size_t ws_bytes, tetris_stream_t stream);
+
+/* Row sampler (the building block of the above, exposed for the token-level adapters):
+ * for r < R: weights = max(0, p[p_row[r]] - q[q_row[r]]) if q != NULL and q_row[r] >= 0, else max(0, p[p_row[r]]);
+ * out_idx[r] = sample(weights, u[r]); mass_out[r] = row mass.  Rows are V elements, row index in units of V. */
+int tetris_sample_rows_f64(const double* p, const double* q, const int64_t* p_row, const int64_t* q_row,
+                           const double* u, int32_t R, int32_t V, int32_t* out_idx, double* mass_out,
+                           uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+int tetris_sample_rows_f32(const float* p, const float* q, const int64_t* p_row, const int64_t* q_row,
+                           const double* u, int32_t R, int32_t V, int32_t* out_idx, double* mass_out,
+                           uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+
+/* residual_distribution (accept_model.py:316-327) for R row pairs: out[r][v] = max(0, pt[r][v]-ps[r][v]) / mass[r]
+ * with mass from the contract hierarchy; rows with zero mass set TETRIS_ST_DEGENERATE and are left untouched. */
+int tetris_residual_f64(const double* p_draft, const double* p_target, int32_t R, int32_t V, double* out,
+                        double* mass_out, uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+
+/* Stage (4) compaction (sim_engine.py:467-471): n_b = accepted[b]+1, capped by cap[b] when cap != NULL;
+ * offsets[B+1] = exclusive scan of n_b; tokens[offsets[b] + i] = (d[b][0..accepted[b]) ++ [out_tok[b]])[i]. */
+int tetris_compact(const int32_t* accepted, const int32_t* out_tok, const int32_t* d, const int32_t* cap,
+                   int32_t B, int32_t k, int32_t* offsets, int32_t* tokens, tetris_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TETRIS_B200_H_ */

@@ -1,0 +1,74 @@
+// Host-side helpers shared by the C-ABI wrappers: thread-local last error, launch checks, workspace layout.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "tetris_b200.h"
+
+namespace tetris {
+namespace abi {
+
+char* err_buf();  // thread-local, defined in abi.cu
+
+inline int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(err_buf(), 512, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+inline int cuda_fail(cudaError_t e) { return fail(TETRIS_CUDA_ERROR, "CUDA error: %s", cudaGetErrorString(e)); }
+
+inline int launch_check() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  return TETRIS_OK;
+}
+
+template <typename K>
+inline cudaError_t ensure_smem(K kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+enum Region { WS_KEYS, WS_COUNTERS, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_END };
+
+inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Workspace layout.  The arrival counters sit in a fixed-size region at offset 0 (one slot per possible request),
+// so a workspace reused across calls of different shapes never finds stale sums where counters must be zero.
+constexpr size_t kCounterSlots = 65536;
+
+inline size_t region_offset(int op, int B, int k, int V, Region which) {
+  const size_t nch = (size_t)((V + TETRIS_CHUNK_ELEMS - 1) / TETRIS_CHUNK_ELEMS);
+  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0};
+  sizes[WS_COUNTERS] = kCounterSlots * 4;
+  if (op & TETRIS_OP_SELECT) {
+    const size_t keys = (size_t)B * k * 8, heap = (size_t)B * 16;  // radix keys / heap-replay items
+    sizes[WS_KEYS] = keys > heap ? keys : heap;
+  }
+  if (op & TETRIS_OP_VERIFY) {
+    // rows processed by one verify call: B requests (stochastic/greedy) or R sampled rows (sample_rows)
+    sizes[WS_CHUNK_SUMS] = (size_t)B * nch * 8;
+    sizes[WS_WARP_SUMS] = (size_t)B * nch * TETRIS_CHUNK_WARPS * 8;
+    sizes[WS_ARG_VAL] = (size_t)B * (k + 1) * nch * 4;
+    sizes[WS_ARG_IDX] = (size_t)B * (k + 1) * nch * 4;
+    sizes[WS_SCRATCH] = align_up((size_t)B * 8) * 3 + align_up((size_t)B * 4);  // residual: rows, u, idx
+  }
+  const Region order[WS_END] = {WS_COUNTERS, WS_KEYS, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH};
+  size_t off = 0;
+  for (int i = 0; i < WS_END; ++i) {
+    if (order[i] == which) return off;
+    off += align_up(sizes[order[i]]);
+  }
+  return off;  // WS_END -> total
+}
+
+inline void* ws_region(void* ws, int op, int B, int k, int V, Region which) {
+  return (char*)ws + region_offset(op, B, k, V, which);
+}
+
+}  // namespace abi
+}  // namespace tetris

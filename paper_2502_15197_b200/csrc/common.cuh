@@ -1,0 +1,144 @@
+// Shared device helpers for the TETRIS B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tetris_b200.h"
+
+namespace tetris {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kLaneElems = TETRIS_LANE_ELEMS;
+constexpr int kSegElems = TETRIS_SEG_ELEMS;
+constexpr int kWarpSegs = TETRIS_WARP_SEGS;
+constexpr int kChunkWarps = TETRIS_CHUNK_WARPS;
+constexpr int kChunkElems = TETRIS_CHUNK_ELEMS;
+constexpr int kWarpElems = kSegElems * kWarpSegs;  // 1024
+constexpr int kStreamThreads = kChunkWarps * 32;   // 256
+
+static_assert(kLaneElems == 8, "lane = one 256-bit fp32 load");
+
+__host__ __device__ inline int n_chunks(int V) { return (V + kChunkElems - 1) / kChunkElems; }
+
+// ---- selection key --------------------------------------------------------------------------------------------
+// Ascending uint64 order == (cum descending); -0.0 is canonicalised to +0.0 so it ties with +0.0 exactly as the
+// reference's float comparison does (selector.py:123 compares -cum).
+__device__ __forceinline__ uint64_t desc_key(double v) {
+  if (v == 0.0) v = 0.0;
+  uint64_t b = (uint64_t)__double_as_longlong(v);
+  uint64_t o = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending in v
+  return ~o;                                                    // descending in v
+}
+
+// ---- 256-bit streaming loads (LDG.E.256 on sm_100a) --------------------------------------------------------------
+__device__ __forceinline__ void ldg8(const float* p, float (&v)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void ldg8(const double* p, double (&v)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+      : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+      : "l"(p + 4));
+}
+
+// Load the 8 elements of one lane starting at row element e (e is a multiple of 8).  VEC requires V % 8 == 0 (fp32)
+// or V % 4 == 0 (fp64) and a 32-byte aligned row base, so a lane is either fully inside the row or fully outside.
+template <typename T, bool VEC>
+__device__ __forceinline__ void load_lane(const T* __restrict__ row, int64_t e, int V, T (&v)[8]) {
+  if (VEC) {
+    if (e < V) {
+      ldg8(row + e, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = T(0);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (e + i < V) ? __ldg(row + e + i) : T(0);
+  }
+}
+
+// ---- element weights (sampling contract, tetris_b200.h) --------------------------------------------------------
+// residual: max(0, (double)p - (double)q)  (accept_model.py:321 clip(pM - pS, 0))
+// plain:    max(0, (double)p)
+__device__ __forceinline__ double w_res(double p, double q) {
+  double x = p - q;
+  return x > 0.0 ? x : 0.0;
+}
+__device__ __forceinline__ double w_plain(double p) { return p > 0.0 ? p : 0.0; }
+
+// Left-to-right fold over the 8 lane elements.
+__device__ __forceinline__ double fold8(const double (&w)[8]) {
+  double o = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o = o + w[i];
+  return o;
+}
+
+// Segment = balanced binary tree over the 32 lane sums (xor butterfly; every node a contiguous lane range).
+__device__ __forceinline__ double seg_sum(double x) {
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) x = x + __shfl_xor_sync(kFull, x, m);
+  return x;
+}
+
+// Left-to-right node search: first child whose running prefix exceeds T; T becomes T - prefix_before.
+// No qualifying child -> last child with positive mass and T = +inf (last-positive-leaf mode).  Returns -1 only
+// when every child is zero.
+__device__ __forceinline__ int seq_find(const double* v, int n, double& T) {
+  double P = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double Pn = P + v[i];
+    if (Pn > T) {
+      T = T - P;
+      return i;
+    }
+    P = Pn;
+  }
+  int last = -1;
+  for (int i = 0; i < n; ++i)
+    if (v[i] > 0.0) last = i;
+  T = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  return last;
+}
+
+__device__ __forceinline__ void set_status(uint32_t* status, uint32_t bits) {
+  if (status && bits) atomicOr(status, bits);
+}
+
+// ---- block-wide helpers for 1024-thread single-CTA kernels ------------------------------------------------------
+template <typename U>
+__device__ __forceinline__ U warp_incl_scan(U x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    U y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// Exclusive scan across the block (blockDim.x == 1024); also returns the block total.  `tmp` >= 33 elements.
+template <typename U>
+__device__ U block_excl_scan(U x, U* tmp, U& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  U incl = warp_incl_scan(x, lane);
+  if (lane == 31) tmp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    U t = lane < nw ? tmp[lane] : U(0);
+    U ti = warp_incl_scan(t, lane);
+    tmp[lane] = ti - t;
+    if (lane == 31) tmp[32] = ti;
+  }
+  __syncthreads();
+  U r = tmp[warp] + incl - x;
+  total = tmp[32];
+  __syncthreads();
+  return r;
+}
+
+}  // namespace tetris

@@ -1,0 +1,482 @@
+// Stage (3): batched verification + residual / bonus resampling, and the row sampler it is built on (sm_100a).
+//
+// The HBM-bound part of the path.  For every request exactly one vocabulary row (bonus: p[b][w]) or row pair
+// (residual after a rejection: p[b][a], q[b][a]) is streamed, once, with 256-bit loads (LDG.E.256).  Grid =
+// (chunks of 8192 elements) x (requests); a CTA of 8 warps owns one chunk, a warp 4 consecutive 256-element
+// segments, a lane 8 consecutive elements — exactly the nodes of the sampling contract in tetris_b200.h, so pass 1
+// produces the chunk's warp and chunk sums with no extra traffic.  The last CTA of a request to arrive (arrival
+// counter in the workspace) folds the chunk sums into the mass, draws T = u*mass and descends the hierarchy;
+// only the one 1024-element warp run that holds the sample is re-read (L2-hot).  No second launch, no host sync.
+//
+// Reference semantics: verify_token (accept_model.py:291-313), residual_distribution (accept_model.py:316-327),
+// Generator.choice inverse CDF (accept_model.py:364,368), apply_verification's first-rejection cascade
+// (sim_engine.py:388-403), bonus token (sim_engine.py:407-409).
+#include <climits>
+
+#include "common.cuh"
+
+namespace tetris {
+
+constexpr int kMaxChunks = 64;  // V <= 524288
+
+// ---- pass 1: the 4 segment sums of one warp run and its left-to-right total ---------------------------------------
+template <typename T, bool VEC, bool RES>
+__device__ __forceinline__ double warp_run_sum(const T* __restrict__ P, const T* __restrict__ Q, int64_t e0, int V,
+                                               int lane, double (&G)[kWarpSegs]) {
+  constexpr int kBatch = sizeof(T) == 4 ? kWarpSegs : 1;  // fp32: all 8 (or 4) 256-bit loads in flight per thread
+#pragma unroll
+  for (int s0 = 0; s0 < kWarpSegs; s0 += kBatch) {
+    T pv[kBatch][8], qv[kBatch][8];
+#pragma unroll
+    for (int s = 0; s < kBatch; ++s) {
+      const int64_t e = e0 + (int64_t)(s0 + s) * kSegElems + lane * kLaneElems;
+      load_lane<T, VEC>(P, e, V, pv[s]);
+      if (RES) load_lane<T, VEC>(Q, e, V, qv[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < kBatch; ++s) {
+      double w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = RES ? w_res((double)pv[s][i], (double)qv[s][i]) : w_plain((double)pv[s][i]);
+      G[s0 + s] = seg_sum(fold8(w));
+    }
+  }
+  double W = 0.0;
+#pragma unroll
+  for (int s = 0; s < kWarpSegs; ++s) W = W + G[s];
+  return W;
+}
+
+// ---- the descent below the warp level (all lanes, uniform T) -------------------------------------------------------
+template <typename T, bool VEC, bool RES>
+__device__ int warp_descend(const T* __restrict__ P, const T* __restrict__ Q, int64_t e0, int V, int lane, double T_) {
+  double G[kWarpSegs];
+  warp_run_sum<T, VEC, RES>(P, Q, e0, V, lane, G);
+  double Tv = T_;
+  const int s = seq_find(G, kWarpSegs, Tv);
+  if (s < 0) return -1;
+  const int64_t eb = e0 + (int64_t)s * kSegElems;
+  T pv[8], qv[8];
+  load_lane<T, VEC>(P, eb + lane * kLaneElems, V, pv);
+  if (RES) load_lane<T, VEC>(Q, eb + lane * kLaneElems, V, qv);
+  double w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = RES ? w_res((double)pv[i], (double)qv[i]) : w_plain((double)pv[i]);
+  double lv[5];
+  lv[0] = fold8(w);
+  double x = lv[0];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    x = x + __shfl_xor_sync(kFull, x, 1 << t);
+    lv[t + 1] = x;
+  }
+  int g = 0;
+#pragma unroll
+  for (int t = 4; t >= 0; --t) {
+    const double L = __shfl_sync(kFull, lv[t], g);
+    const double R = __shfl_sync(kFull, lv[t], g + (1 << t));
+    if (!(L > Tv || R == 0.0)) {
+      Tv = Tv - L;
+      g += 1 << t;
+    }
+  }
+  double Tl = Tv;
+  const int li_own = seq_find(w, 8, Tl);
+  const int li = __shfl_sync(kFull, li_own, g);
+  if (li < 0) return -1;
+  return (int)(eb + g * kLaneElems + li);
+}
+
+// ---- stochastic verify (FUSED) / explicit-row sampler ------------------------------------------------------------
+template <typename T, bool VEC, bool FUSED>
+__global__ void __launch_bounds__(kStreamThreads)
+    sample_kernel(const T* __restrict__ p, const T* __restrict__ q, const int32_t* __restrict__ d,
+                  const int32_t* __restrict__ windows, const int32_t* __restrict__ win_off,
+                  const double* __restrict__ u_acc, int k, int32_t* __restrict__ accepted,
+                  const int64_t* __restrict__ p_row, const int64_t* __restrict__ q_row,
+                  const double* __restrict__ u_res, int V, int32_t* __restrict__ out_idx,
+                  double* __restrict__ mass_out, uint32_t* status, int* __restrict__ counters,
+                  double* __restrict__ chunk_sums, double* __restrict__ warp_sums) {
+  const int c = blockIdx.x, b = blockIdx.y, nch = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ long long s_prow, s_qrow;
+  __shared__ int s_acc, s_last;
+  __shared__ double s_w[kChunkWarps];
+  __shared__ double s_S[kMaxChunks];
+
+  if (FUSED) {
+    if (warp == 0) {
+      // verify_token over the selected window, all positions in parallel; first rejection via ballot
+      uint32_t bad = 0;
+      int w = windows[b];
+      if (w < 0 || w > k) {
+        bad |= TETRIS_ST_BAD_WINDOW;
+        w = w < 0 ? 0 : k;
+      }
+      int a = w;
+      const int64_t uoff = win_off ? (int64_t)win_off[b] : (int64_t)b * k;
+      for (int j0 = 0; j0 < w; j0 += 32) {
+        const int j = j0 + lane;
+        bool rej = false;
+        if (j < w) {
+          const int t = d[(int64_t)b * k + j];
+          const double u = u_acc[uoff + j];
+          if (!(u >= 0.0 && u < 1.0)) bad |= TETRIS_ST_BAD_UNIFORM;
+          if (t < 0 || t >= V) {
+            bad |= TETRIS_ST_BAD_TOKEN;
+            rej = true;
+          } else {
+            const double s = (double)q[((int64_t)b * k + j) * V + t];
+            const double m = (double)p[((int64_t)b * (k + 1) + j) * V + t];
+            rej = !(s <= m) && !(u < m / s);  // accept_model.py:311-313
+          }
+        }
+        const unsigned mask = __ballot_sync(kFull, rej);
+        if (mask) {
+          a = j0 + __ffs(mask) - 1;
+          break;
+        }
+      }
+      bad = __reduce_or_sync(kFull, bad);
+      if (lane == 0) {
+        s_acc = a;
+        if (a < w) {  // rejected at depth a: residual of (p, q) at that position
+          s_prow = (long long)b * (k + 1) + a;
+          s_qrow = (long long)b * k + a;
+        } else {      // everything accepted: bonus token from the target at position w
+          s_prow = (long long)b * (k + 1) + w;
+          s_qrow = -1;
+        }
+        if (c == 0) set_status(status, bad);  // every chunk CTA derives the same verdict; report once
+      }
+    }
+  } else if (tid == 0) {
+    s_prow = p_row[b];
+    s_qrow = (q != nullptr && q_row != nullptr) ? q_row[b] : -1;
+  }
+  __syncthreads();
+
+  const T* P = p + s_prow * (int64_t)V;
+  const bool res = s_qrow >= 0;
+  const T* Q = res ? q + s_qrow * (int64_t)V : nullptr;
+  const int64_t e0 = (int64_t)c * kChunkElems + warp * kWarpElems;
+  double G[kWarpSegs];
+  const double W = res ? warp_run_sum<T, VEC, true>(P, Q, e0, V, lane, G)
+                       : warp_run_sum<T, VEC, false>(P, Q, e0, V, lane, G);
+  if (lane == 0) s_w[warp] = W;
+  __syncthreads();
+  if (tid == 0) {
+    double S = 0.0;
+#pragma unroll
+    for (int w = 0; w < kChunkWarps; ++w) S = S + s_w[w];
+    const int64_t slot = (int64_t)b * nch + c;
+    __stcg(&chunk_sums[slot], S);
+#pragma unroll
+    for (int w = 0; w < kChunkWarps; ++w) __stcg(&warp_sums[slot * kChunkWarps + w], s_w[w]);
+    __threadfence();
+    const int prev = atomicAdd(&counters[b], 1);
+    s_last = (prev == nch - 1);
+  }
+  __syncthreads();
+  if (!s_last || warp != 0) return;
+  __threadfence();
+
+  // ---- last CTA of request b: mass, T = u*mass, descent ------------------------------------------------------
+  for (int i = lane; i < nch; i += 32) s_S[i] = __ldcg(&chunk_sums[(int64_t)b * nch + i]);
+  __syncwarp();
+  double mass = 0.0;
+  for (int i = 0; i < nch; ++i) mass = mass + s_S[i];
+  int tok = -1;
+  uint32_t bad = 0;
+  const double u = u_res[b];
+  if (!(u >= 0.0 && u < 1.0)) bad |= TETRIS_ST_BAD_UNIFORM;
+  if (mass > 0.0) {
+    double Tv = u * mass;
+    const int cc = seq_find(s_S, nch, Tv);
+    double Wc[kChunkWarps];
+#pragma unroll
+    for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __ldcg(&warp_sums[((int64_t)b * nch + cc) * kChunkWarps + w]);
+    const int ww = seq_find(Wc, kChunkWarps, Tv);
+    const int64_t e0s = (int64_t)cc * kChunkElems + ww * kWarpElems;
+    tok = res ? warp_descend<T, VEC, true>(P, Q, e0s, V, lane, Tv) : warp_descend<T, VEC, false>(P, Q, e0s, V, lane, Tv);
+  }
+  if (tok < 0) bad |= TETRIS_ST_DEGENERATE;
+  if (lane == 0) {
+    counters[b] = 0;
+    out_idx[b] = tok;
+    if (mass_out) mass_out[b] = mass;
+    if (FUSED) accepted[b] = s_acc;
+    set_status(status, bad);
+  }
+}
+
+// ---- greedy verify ----------------------------------------------------------------------------------------------
+// numpy.argmax order: NaN ranks above every number (first NaN wins), otherwise larger value, ties -> lower index.
+__device__ __forceinline__ bool arg_better(float av, int ai, float bv, int bi) {
+  if (ai == INT_MAX) return false;
+  if (bi == INT_MAX) return true;
+  const bool an = isnan(av), bn = isnan(bv);
+  if (an != bn) return an;
+  if (!an && av != bv) return av > bv;
+  return ai < bi;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kStreamThreads)
+    greedy_kernel(const float* __restrict__ p, const int32_t* __restrict__ d, const int32_t* __restrict__ windows,
+                  int k, int V, int32_t* __restrict__ accepted, int32_t* __restrict__ out_tok, uint32_t* status,
+                  int* __restrict__ counters, float* __restrict__ arg_val, int32_t* __restrict__ arg_idx) {
+  const int c = blockIdx.x, j = blockIdx.y, b = blockIdx.z, nch = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float s_v[kChunkWarps];
+  __shared__ int s_i[kChunkWarps];
+  __shared__ int s_last;
+  __shared__ int s_am[TETRIS_MAX_K + 1];
+  int w = windows[b];
+  const bool bad_w = (w < 0 || w > k);
+  w = w < 0 ? 0 : (w > k ? k : w);
+  if (j > w) return;
+
+  const float* row = p + ((int64_t)b * (k + 1) + j) * V;
+  const int64_t e0 = (int64_t)c * kChunkElems + warp * kWarpElems;
+  float v[kWarpSegs][8];
+#pragma unroll
+  for (int s = 0; s < kWarpSegs; ++s) load_lane<float, VEC>(row, e0 + s * kSegElems + lane * kLaneElems, V, v[s]);
+  float bv = 0.f;
+  int bi = INT_MAX;
+#pragma unroll
+  for (int s = 0; s < kWarpSegs; ++s) {
+    const int64_t e = e0 + s * kSegElems + lane * kLaneElems;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (e + i < V && arg_better(v[s][i], (int)(e + i), bv, bi)) {
+        bv = v[s][i];
+        bi = (int)(e + i);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    const float ov = __shfl_xor_sync(kFull, bv, m);
+    const int oi = __shfl_xor_sync(kFull, bi, m);
+    if (arg_better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_v[warp] = bv;
+    s_i[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float cv = s_v[0];
+    int ci = s_i[0];
+    for (int x = 1; x < kChunkWarps; ++x)
+      if (arg_better(s_v[x], s_i[x], cv, ci)) {
+        cv = s_v[x];
+        ci = s_i[x];
+      }
+    const int64_t slot = ((int64_t)b * (k + 1) + j) * nch + c;
+    __stcg(&arg_val[slot], cv);
+    __stcg(&arg_idx[slot], ci);
+    __threadfence();
+    const int prev = atomicAdd(&counters[b], 1);
+    s_last = (prev == (w + 1) * nch - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int jj = tid; jj <= w; jj += blockDim.x) {
+    const int64_t base = ((int64_t)b * (k + 1) + jj) * nch;
+    float cv = __ldcg(&arg_val[base]);
+    int ci = __ldcg(&arg_idx[base]);
+    for (int x = 1; x < nch; ++x) {
+      const float ov = __ldcg(&arg_val[base + x]);
+      const int oi = __ldcg(&arg_idx[base + x]);
+      if (arg_better(ov, oi, cv, ci)) {
+        cv = ov;
+        ci = oi;
+      }
+    }
+    s_am[jj] = ci;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t bad = bad_w ? TETRIS_ST_BAD_WINDOW : 0u;
+    int a = w;
+    for (int jj = 0; jj < w; ++jj) {
+      const int t = d[(int64_t)b * k + jj];
+      if (t < 0 || t >= V) bad |= TETRIS_ST_BAD_TOKEN;
+      if (t != s_am[jj]) {
+        a = jj;
+        break;
+      }
+    }
+    accepted[b] = a;
+    out_tok[b] = s_am[a];
+    counters[b] = 0;
+    set_status(status, bad);
+  }
+}
+
+// ---- residual normalisation (residual_distribution's diff / mass, accept_model.py:321-327) ------------------------
+__global__ void residual_norm_kernel(const double* __restrict__ ps, const double* __restrict__ pt, int V,
+                                     const double* __restrict__ mass, double* __restrict__ out) {
+  const int r = blockIdx.y;
+  const double m = mass[r];
+  if (!(m > 0.0)) return;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)r * V + v;
+    out[o] = w_res(pt[o], ps[o]) / m;
+  }
+}
+
+__global__ void identity_rows_kernel(int64_t* a, int64_t* b, double* u, int R) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < R) {
+    a[i] = i;
+    b[i] = i;
+    u[i] = 0.0;
+  }
+}
+
+}  // namespace tetris
+
+// ---- C ABI ---------------------------------------------------------------------------------------------------------
+#include "abi_util.h"
+
+namespace {
+using namespace tetris;
+
+inline bool aligned32(const void* ptr) { return ((uintptr_t)ptr & 31u) == 0; }
+
+int check_verify_ws(int B, int k, int V, void* ws, size_t ws_bytes) {
+  size_t need = tetris_workspace_bytes(TETRIS_OP_VERIFY, B, k, V);
+  if (!ws || ws_bytes < need)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "workspace too small: %zu < %zu", ws_bytes, need);
+  return TETRIS_OK;
+}
+
+int check_shape(int B, int k, int V) {
+  if (B < 0 || B > 65535) return abi::fail(TETRIS_INVALID_ARGUMENT, "B=%d outside [0, 65535]", B);
+  if (k < 0 || k > TETRIS_MAX_K) return abi::fail(TETRIS_INVALID_ARGUMENT, "k=%d outside [0, 255]", k);
+  if (V < 1 || V > kMaxChunks * kChunkElems)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "V=%d outside [1, %d]", V, kMaxChunks * kChunkElems);
+  return TETRIS_OK;
+}
+
+template <typename T>
+int sample_rows_impl(const T* p, const T* q, const int64_t* p_row, const int64_t* q_row, const double* u, int R,
+                     int V, int32_t* out_idx, double* mass_out, uint32_t* status, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  int rc = check_shape(R, 0, V);
+  if (rc) return rc;
+  if (R == 0) return TETRIS_OK;
+  if (!p || !p_row || !u || !out_idx) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(R, 0, V, ws, ws_bytes))) return rc;
+  const bool vec = (V % (32 / sizeof(T)) == 0) && aligned32(p) && (!q || aligned32(q));
+  dim3 grid(n_chunks(V), R);
+  int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_COUNTERS);
+  double* cs = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_CHUNK_SUMS);
+  double* wsum = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_WARP_SUMS);
+  if (vec)
+    sample_kernel<T, true, false><<<grid, kStreamThreads, 0, st>>>(p, q, nullptr, nullptr, nullptr, nullptr, 0,
+                                                                   nullptr, p_row, q_row, u, V, out_idx, mass_out,
+                                                                   status, cnt, cs, wsum);
+  else
+    sample_kernel<T, false, false><<<grid, kStreamThreads, 0, st>>>(p, q, nullptr, nullptr, nullptr, nullptr, 0,
+                                                                    nullptr, p_row, q_row, u, V, out_idx, mass_out,
+                                                                    status, cnt, cs, wsum);
+  return abi::launch_check();
+}
+}  // namespace
+
+extern "C" int tetris_verify_stochastic_f32(const float* p, const float* q, const int32_t* d, const int32_t* windows,
+                                            const int32_t* win_offsets, const double* u_acc, const double* u_res,
+                                            int32_t B, int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
+                                            double* mass_out, uint32_t* status, void* ws, size_t ws_bytes,
+                                            tetris_stream_t stream) {
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (B == 0) return TETRIS_OK;
+  if (!p || !q || !d || !windows || !u_acc || !u_res || !accepted || !out_tok)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
+  const bool vec = (V % 8 == 0) && aligned32(p) && aligned32(q);
+  dim3 grid(n_chunks(V), B);
+  int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
+  double* cs = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
+  double* wsum = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (vec)
+    sample_kernel<float, true, true><<<grid, kStreamThreads, 0, st>>>(p, q, d, windows, win_offsets, u_acc, k,
+                                                                      accepted, nullptr, nullptr, u_res, V, out_tok,
+                                                                      mass_out, status, cnt, cs, wsum);
+  else
+    sample_kernel<float, false, true><<<grid, kStreamThreads, 0, st>>>(p, q, d, windows, win_offsets, u_acc, k,
+                                                                       accepted, nullptr, nullptr, u_res, V,
+                                                                       out_tok, mass_out, status, cnt, cs, wsum);
+  return abi::launch_check();
+}
+
+extern "C" int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B,
+                                        int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
+                                        uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (B == 0) return TETRIS_OK;
+  if (!p || !d || !windows || !accepted || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
+  const bool vec = (V % 8 == 0) && aligned32(p);
+  dim3 grid(n_chunks(V), k + 1, B);
+  int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
+  float* av = (float*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_VAL);
+  int32_t* ai = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_IDX);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (vec)
+    greedy_kernel<true><<<grid, kStreamThreads, 0, st>>>(p, d, windows, k, V, accepted, out_tok, status, cnt, av, ai);
+  else
+    greedy_kernel<false><<<grid, kStreamThreads, 0, st>>>(p, d, windows, k, V, accepted, out_tok, status, cnt, av,
+                                                          ai);
+  return abi::launch_check();
+}
+
+extern "C" int tetris_sample_rows_f64(const double* p, const double* q, const int64_t* p_row, const int64_t* q_row,
+                                      const double* u, int32_t R, int32_t V, int32_t* out_idx, double* mass_out,
+                                      uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  return sample_rows_impl<double>(p, q, p_row, q_row, u, R, V, out_idx, mass_out, status, ws, ws_bytes,
+                                  (cudaStream_t)stream);
+}
+
+extern "C" int tetris_sample_rows_f32(const float* p, const float* q, const int64_t* p_row, const int64_t* q_row,
+                                      const double* u, int32_t R, int32_t V, int32_t* out_idx, double* mass_out,
+                                      uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  return sample_rows_impl<float>(p, q, p_row, q_row, u, R, V, out_idx, mass_out, status, ws, ws_bytes,
+                                 (cudaStream_t)stream);
+}
+
+extern "C" int tetris_residual_f64(const double* p_draft, const double* p_target, int32_t R, int32_t V, double* out,
+                                   double* mass_out, uint32_t* status, void* ws, size_t ws_bytes,
+                                   tetris_stream_t stream) {
+  // mass via the sampler (u = 0 -> first positive element, discarded), then out = max(0, pt - ps) / mass.
+  int rc = check_shape(R, 0, V);
+  if (rc) return rc;
+  if (R == 0) return TETRIS_OK;
+  if (!p_draft || !p_target || !out || !mass_out) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(R, 0, V, ws, ws_bytes))) return rc;
+  char* x = (char*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_SCRATCH);
+  int64_t* prow = (int64_t*)x;
+  int64_t* qrow = (int64_t*)(x + abi::align_up((size_t)R * 8));
+  double* u = (double*)(x + 2 * abi::align_up((size_t)R * 8));
+  int32_t* idx = (int32_t*)(x + 3 * abi::align_up((size_t)R * 8));
+  cudaStream_t st = (cudaStream_t)stream;
+  // rows r -> r for both operands; uniforms 0
+  identity_rows_kernel<<<(R + 255) / 256, 256, 0, st>>>(prow, qrow, u, R);
+  // weights = max(0, p - q) with p = p_target, q = p_draft
+  rc = sample_rows_impl<double>(p_target, p_draft, prow, qrow, u, R, V, idx, mass_out, status, ws, ws_bytes, st);
+  if (rc) return rc;
+  dim3 grid((V + 255) / 256 < 1024 ? (V + 255) / 256 : 1024, R);
+  residual_norm_kernel<<<grid, 256, 0, st>>>(p_draft, p_target, V, mass_out, out);
+  return abi::launch_check();
+}

@@ -1,0 +1,445 @@
+"""Batched tensor API of the TETRIS hot path (CUDA tensors in, CUDA tensors out, stream-ordered, no host sync).
+
+Every function launches the sm_100a kernels of libtetris_b200.so through the C ABI on the current torch stream.
+Inputs must already be CUDA tensors; there is no CPU path.  Data-dependent errors are accumulated in a device status
+word; call `raise_for_status(status)` (one host sync) where the reference would have raised.
+
+Shapes (dense, row-major): conf/alpha/cum [B, k] f64, lengths [B] i32, p [B, k+1, V] f32 (target incl. the bonus
+position), q [B, k, V] f32 (draft), d [B, k] i32 (draft tokens), u_acc [B, k] (dense) or [sum(windows)] (packed)
+f64, u_res [B] f64.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _native as N
+from .errors import DegenerateResidualError
+
+_I32 = torch.int32
+_I64 = torch.int64
+_F64 = torch.float64
+_F32 = torch.float32
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream] = None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _need_cuda(name: str, t: Optional[torch.Tensor], dtype, ndim: Optional[int] = None, optional=False):
+    if t is None:
+        if optional:
+            return None
+        raise ValueError(f"{name} is required")
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must be {ndim}-d, got shape {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+class Workspace:
+    """Caller-owned scratch for the kernels (zeroed once; kernels leave the arrival counters at zero).
+
+    One workspace must not be used by two streams concurrently."""
+
+    def __init__(self, device, op: int, B: int, k: int, V: int):
+        self.nbytes = max(N.workspace_bytes(op, B, k, V), 256)
+        self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+        self.key = (op, B, k, V)
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+
+_ws_cache: dict = {}
+
+
+def workspace(device, op: int, B: int, k: int, V: int, stream: Optional[torch.cuda.Stream] = None) -> Workspace:
+    dev = torch.device(device)
+    sh = _stream_handle(stream) if dev.type == "cuda" else 0
+    key = (dev, sh, op)
+    ws = _ws_cache.get(key)
+    need = N.workspace_bytes(op, B, k, V)
+    if ws is None or ws.nbytes < need:
+        ws = Workspace(dev, op, B, k, V)
+        _ws_cache[key] = ws
+    return ws
+
+
+def new_status(device) -> torch.Tensor:
+    return torch.zeros(1, dtype=_I32, device=device)
+
+
+def raise_for_status(status: torch.Tensor, context: str = "") -> None:
+    """Host sync: map device status bits to the reference's exceptions."""
+    s = int(status.item()) & 0xFFFFFFFF
+    if not s:
+        return
+    where = f" ({context})" if context else ""
+    if s & N.ST_BAD_TOKEN:
+        raise ValueError(f"draft token outside the vocabulary{where}")
+    if s & N.ST_BAD_UNIFORM:
+        raise ValueError(f"uniform draw outside [0, 1){where}")
+    if s & N.ST_BAD_WINDOW:
+        raise ValueError(f"selection window deeper than the drafted row{where}")
+    if s & N.ST_BAD_VALUE:
+        raise ValueError(f"acceptance value outside [0, 1] or NaN{where}")
+    if s & N.ST_DEGENERATE:
+        raise DegenerateResidualError(f"target never rejects the draft; there is no residual to sample{where}")
+    raise RuntimeError(f"unknown status bits {s:#x}{where}")
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# stages (1)+(2): selection
+# ---------------------------------------------------------------------------------------------------------------
+@dataclass
+class SelectResult:
+    windows: torch.Tensor            # [B] i32
+    win_offsets: torch.Tensor        # [B+1] i32, exclusive scan of windows
+    stats: torch.Tensor              # [4] i64: extracts, inserts, peak_queue, comparisons (-1 unless exact)
+    status: torch.Tensor             # [1] i32 device status bits
+    cum: Optional[torch.Tensor] = None  # [B, k] f64 (when requested)
+
+
+def select(vals: torch.Tensor, capacity: int, lengths: Optional[torch.Tensor] = None, *, vals_are_cum: bool = False,
+           want_cum: bool = False, out: Optional[SelectResult] = None,
+           stream: Optional[torch.cuda.Stream] = None) -> SelectResult:
+    """cumulative_products + select_tetris (selector.py:95-176) on the GPU."""
+    vals = _need_cuda("vals", vals, _F64, 2)
+    B, k = vals.shape
+    lengths = _need_cuda("lengths", lengths, _I32, 1, optional=True)
+    if capacity < 0:
+        raise ValueError(f"capacity must be >= 0, got {capacity}")
+    dev = vals.device
+    if out is None:
+        out = SelectResult(
+            windows=torch.empty(B, dtype=_I32, device=dev),
+            win_offsets=torch.empty(B + 1, dtype=_I32, device=dev),
+            stats=torch.empty(4, dtype=_I64, device=dev),
+            status=new_status(dev),
+            cum=torch.zeros(B, k, dtype=_F64, device=dev) if want_cum else None,
+        )
+    ws = workspace(dev, N.OP_ALL, B, k, 1, stream)
+    N.call("tetris_select_f64", _ptr(vals), _ptr(lengths), B, k, int(capacity), int(bool(vals_are_cum)),
+           _ptr(out.windows), _ptr(out.win_offsets), _ptr(out.cum), _ptr(out.stats), _ptr(out.status),
+           ws.ptr, ws.nbytes, _stream_handle(stream))
+    return out
+
+
+def heap_stats(cum: torch.Tensor, capacity: int, lengths: Optional[torch.Tensor] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Exact PolicyStats incl. heapq comparisons (selector.py:151-176); single-thread accounting kernel."""
+    cum = _need_cuda("cum", cum, _F64, 2)
+    B, k = cum.shape
+    lengths = _need_cuda("lengths", lengths, _I32, 1, optional=True)
+    stats = torch.empty(4, dtype=_I64, device=cum.device)
+    ws = workspace(cum.device, N.OP_ALL, B, k, 1, stream)
+    N.call("tetris_heap_stats_f64", _ptr(cum), _ptr(lengths), B, k, int(capacity), _ptr(stats), ws.ptr, ws.nbytes,
+           _stream_handle(stream))
+    return stats
+
+
+def expected_accepted(alpha: torch.Tensor, windows: torch.Tensor, lengths: Optional[torch.Tensor] = None,
+                      status: Optional[torch.Tensor] = None) -> torch.Tensor:
+    alpha = _need_cuda("alpha", alpha, _F64, 2)
+    B, k = alpha.shape
+    windows = _need_cuda("windows", windows, _I32, 1)
+    out = torch.empty((), dtype=_F64, device=alpha.device)
+    st = status if status is not None else new_status(alpha.device)
+    N.call("tetris_expected_accepted_f64", _ptr(alpha), _ptr(lengths), _ptr(windows), B, k, _ptr(out), _ptr(st),
+           _stream_handle())
+    if status is None:
+        raise_for_status(st, "expected_accepted")
+    return out
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# stage (3): verification
+# ---------------------------------------------------------------------------------------------------------------
+def verify_matrix(alpha: torch.Tensor, windows: torch.Tensor, win_offsets: torch.Tensor, u: torch.Tensor,
+                  lengths: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """apply_verification (sim_engine.py:374-404) with the flat uniform stream u[win_offsets[b] + j]."""
+    alpha = _need_cuda("alpha", alpha, _F64, 2)
+    B, k = alpha.shape
+    windows = _need_cuda("windows", windows, _I32, 1)
+    win_offsets = _need_cuda("win_offsets", win_offsets, _I32, 1)
+    u = _need_cuda("u", u, _F64, 1)
+    lengths = _need_cuda("lengths", lengths, _I32, 1, optional=True)
+    acc = torch.empty(B, dtype=_I32, device=alpha.device)
+    st = status if status is not None else new_status(alpha.device)
+    N.call("tetris_verify_matrix_f64", _ptr(alpha), _ptr(lengths), _ptr(windows), _ptr(win_offsets), _ptr(u), B, k,
+           _ptr(acc), _ptr(st), _stream_handle())
+    if status is None:
+        raise_for_status(st, "apply_verification")
+    return acc
+
+
+@dataclass
+class VerifyResult:
+    accepted: torch.Tensor  # [B] i32
+    out_tok: torch.Tensor   # [B] i32 (correction or bonus token)
+    status: torch.Tensor    # [1] i32
+    mass: Optional[torch.Tensor] = None  # [B] f64 (stochastic, when requested)
+
+
+def verify_stochastic(p: torch.Tensor, q: torch.Tensor, d: torch.Tensor, windows: torch.Tensor,
+                      u_acc: torch.Tensor, u_res: torch.Tensor, win_offsets: Optional[torch.Tensor] = None, *,
+                      want_mass: bool = False, out: Optional[VerifyResult] = None,
+                      stream: Optional[torch.cuda.Stream] = None) -> VerifyResult:
+    p = _need_cuda("p", p, _F32, 3)
+    q = _need_cuda("q", q, _F32, 3)
+    B, k1, V = p.shape
+    k = k1 - 1
+    if tuple(q.shape) != (B, k, V):
+        raise ValueError(f"q must be [B, k, V] = {(B, k, V)}, got {tuple(q.shape)}")
+    d = _need_cuda("d", d, _I32, 2)
+    windows = _need_cuda("windows", windows, _I32, 1)
+    u_acc = _need_cuda("u_acc", u_acc, _F64)
+    u_res = _need_cuda("u_res", u_res, _F64, 1)
+    win_offsets = _need_cuda("win_offsets", win_offsets, _I32, 1, optional=True)
+    dev = p.device
+    if out is None:
+        out = VerifyResult(torch.empty(B, dtype=_I32, device=dev), torch.empty(B, dtype=_I32, device=dev),
+                           new_status(dev), torch.empty(B, dtype=_F64, device=dev) if want_mass else None)
+    ws = workspace(dev, N.OP_VERIFY, B, k, V, stream)
+    N.call("tetris_verify_stochastic_f32", _ptr(p), _ptr(q), _ptr(d), _ptr(windows), _ptr(win_offsets),
+           _ptr(u_acc), _ptr(u_res), B, k, V, _ptr(out.accepted), _ptr(out.out_tok), _ptr(out.mass),
+           _ptr(out.status), ws.ptr, ws.nbytes, _stream_handle(stream))
+    return out
+
+
+def verify_greedy(p: torch.Tensor, d: torch.Tensor, windows: torch.Tensor, *, out: Optional[VerifyResult] = None,
+                  stream: Optional[torch.cuda.Stream] = None) -> VerifyResult:
+    p = _need_cuda("p", p, _F32, 3)
+    B, k1, V = p.shape
+    k = k1 - 1
+    d = _need_cuda("d", d, _I32, 2)
+    windows = _need_cuda("windows", windows, _I32, 1)
+    dev = p.device
+    if out is None:
+        out = VerifyResult(torch.empty(B, dtype=_I32, device=dev), torch.empty(B, dtype=_I32, device=dev),
+                           new_status(dev))
+    ws = workspace(dev, N.OP_VERIFY, B, k, V, stream)
+    N.call("tetris_verify_greedy_f32", _ptr(p), _ptr(d), _ptr(windows), B, k, V, _ptr(out.accepted),
+           _ptr(out.out_tok), _ptr(out.status), ws.ptr, ws.nbytes, _stream_handle(stream))
+    return out
+
+
+def sample_rows(p: torch.Tensor, p_row: torch.Tensor, u: torch.Tensor, q: Optional[torch.Tensor] = None,
+                q_row: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None):
+    """Sample one index per (p row[, q row]) pair under the sampling contract; p/q are [rows, V] f32 or f64."""
+    if p.dtype not in (_F32, _F64):
+        raise ValueError("p must be float32 or float64")
+    p = _need_cuda("p", p, p.dtype, 2)
+    V = p.shape[1]
+    q = _need_cuda("q", q, p.dtype, 2, optional=True)
+    p_row = _need_cuda("p_row", p_row, _I64, 1)
+    R = p_row.shape[0]
+    q_row = _need_cuda("q_row", q_row, _I64, 1, optional=True)
+    u = _need_cuda("u", u, _F64, 1)
+    dev = p.device
+    idx = torch.empty(R, dtype=_I32, device=dev)
+    mass = torch.empty(R, dtype=_F64, device=dev)
+    st = status if status is not None else new_status(dev)
+    ws = workspace(dev, N.OP_VERIFY, R, 0, V)
+    fn = "tetris_sample_rows_f64" if p.dtype == _F64 else "tetris_sample_rows_f32"
+    N.call(fn, _ptr(p), _ptr(q), _ptr(p_row), _ptr(q_row), _ptr(u), R, V, _ptr(idx), _ptr(mass), _ptr(st), ws.ptr,
+           ws.nbytes, _stream_handle())
+    return idx, mass, st
+
+
+def residual(p_draft: torch.Tensor, p_target: torch.Tensor, status: Optional[torch.Tensor] = None):
+    """residual_distribution (accept_model.py:316-327) for R row pairs [R, V] f64 -> ([R, V] f64, mass [R])."""
+    p_draft = _need_cuda("p_draft", p_draft, _F64, 2)
+    p_target = _need_cuda("p_target", p_target, _F64, 2)
+    if p_draft.shape != p_target.shape:
+        raise ValueError(f"vocabulary mismatch: draft {tuple(p_draft.shape)} vs target {tuple(p_target.shape)}")
+    R, V = p_draft.shape
+    dev = p_draft.device
+    out = torch.empty(R, V, dtype=_F64, device=dev)
+    mass = torch.empty(R, dtype=_F64, device=dev)
+    st = status if status is not None else new_status(dev)
+    ws = workspace(dev, N.OP_VERIFY, R, 0, V)
+    N.call("tetris_residual_f64", _ptr(p_draft), _ptr(p_target), R, V, _ptr(out), _ptr(mass), _ptr(st), ws.ptr,
+           ws.nbytes, _stream_handle())
+    return out, mass, st
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# stage (4): compaction
+# ---------------------------------------------------------------------------------------------------------------
+def compact(accepted: torch.Tensor, out_tok: torch.Tensor, d: torch.Tensor, cap: Optional[torch.Tensor] = None, *,
+            offsets: Optional[torch.Tensor] = None, tokens: Optional[torch.Tensor] = None,
+            stream: Optional[torch.cuda.Stream] = None):
+    """Emitted tokens d[b,:a_b] ++ [x_b] (capped by cap[b]) packed back to back; returns (offsets[B+1], tokens)."""
+    accepted = _need_cuda("accepted", accepted, _I32, 1)
+    out_tok = _need_cuda("out_tok", out_tok, _I32, 1)
+    d = _need_cuda("d", d, _I32, 2)
+    cap = _need_cuda("cap", cap, _I32, 1, optional=True)
+    B, k = d.shape
+    dev = d.device
+    if offsets is None:
+        offsets = torch.empty(B + 1, dtype=_I32, device=dev)
+    if tokens is None:
+        tokens = torch.empty(B * (k + 1), dtype=_I32, device=dev)
+    N.call("tetris_compact", _ptr(accepted), _ptr(out_tok), _ptr(d), _ptr(cap), B, k, _ptr(offsets), _ptr(tokens),
+           _stream_handle(stream))
+    return offsets, tokens
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# one full verification step with preallocated buffers (CUDA-graph capturable)
+# ---------------------------------------------------------------------------------------------------------------
+class TetrisStep:
+    """select -> verify (stochastic or greedy) -> compact for fixed shapes; every launch goes on the current stream,
+    all buffers are preallocated, nothing synchronises the host, so `run` can be captured in a CUDA graph."""
+
+    def __init__(self, B: int, k: int, V: int, capacity: int, mode: str = "stochastic", device="cuda",
+                 u_layout: str = "dense", group=None):
+        if mode not in ("stochastic", "greedy"):
+            raise ValueError(f"mode must be 'stochastic' or 'greedy', got {mode!r}")
+        self.B, self.k, self.V, self.C, self.mode = B, k, V, int(capacity), mode
+        self.u_layout = u_layout
+        dev = torch.device(device)
+        self.device = dev
+        # request-sharded selection: gather every shard's scores, select globally, keep the local slice (dist.py)
+        self.group = group
+        self.world, self.rank = 1, 0
+        if group is not None:
+            import torch.distributed as dist
+
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        Bg = B * self.world
+        self.Bg = Bg
+        if self.world > 1:
+            if u_layout != "dense":
+                raise ValueError("sharded steps use the dense uniform layout")
+            self.conf_all = torch.zeros(Bg, k, dtype=_F64, device=dev)
+            self.len_all = torch.zeros(Bg, dtype=_I32, device=dev)
+        self.windows_all = torch.zeros(Bg, dtype=_I32, device=dev)
+        self.windows = self.windows_all[self.rank * B:(self.rank + 1) * B]
+        self.win_offsets = torch.zeros(Bg + 1, dtype=_I32, device=dev)
+        self.stats = torch.zeros(4, dtype=_I64, device=dev)
+        self.status = new_status(dev)
+        self.accepted = torch.zeros(B, dtype=_I32, device=dev)
+        self.out_tok = torch.zeros(B, dtype=_I32, device=dev)
+        self.mass = torch.zeros(B, dtype=_F64, device=dev)
+        self.offsets = torch.zeros(B + 1, dtype=_I32, device=dev)
+        self.tokens = torch.zeros(B * (k + 1), dtype=_I32, device=dev)
+        self.ws = Workspace(dev, N.OP_ALL, Bg, k, V)
+        self._lib = N.load()
+
+    def run(self, conf, lengths, p, q, d, u_acc=None, u_res=None, cap=None, events=None) -> None:
+        """events: optional 4 torch.cuda.Events recorded around select / verify / compact (kernel timing)."""
+        lib, ws, s = self._lib, self.ws, torch.cuda.current_stream().cuda_stream
+        B, k, V = self.B, self.k, self.V
+        if events is not None:
+            events[0].record()
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_gather_into_tensor(self.conf_all, conf, group=self.group)
+            dist.all_gather_into_tensor(self.len_all, lengths, group=self.group)
+            sel_conf, sel_len = self.conf_all, self.len_all
+        else:
+            sel_conf, sel_len = conf, lengths
+        rc = lib.tetris_select_f64(sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, 0,
+                                   self.windows_all.data_ptr(), self.win_offsets.data_ptr(), None,
+                                   self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        self._check(rc)
+        if events is not None:
+            events[1].record()
+        if self.mode == "stochastic":
+            woff = self.win_offsets.data_ptr() if self.u_layout == "packed" else None
+            rc = lib.tetris_verify_stochastic_f32(p.data_ptr(), q.data_ptr(), d.data_ptr(), self.windows.data_ptr(),
+                                                  woff, u_acc.data_ptr(), u_res.data_ptr(), B, k, V,
+                                                  self.accepted.data_ptr(), self.out_tok.data_ptr(),
+                                                  self.mass.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        else:
+            rc = lib.tetris_verify_greedy_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), B, k, V,
+                                              self.accepted.data_ptr(), self.out_tok.data_ptr(),
+                                              self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        self._check(rc)
+        if events is not None:
+            events[2].record()
+        rc = lib.tetris_compact(self.accepted.data_ptr(), self.out_tok.data_ptr(), d.data_ptr(), _ptr(cap), B, k,
+                                self.offsets.data_ptr(), self.tokens.data_ptr(), s)
+        self._check(rc)
+        if events is not None:
+            events[3].record()
+
+    def _check(self, rc: int) -> None:
+        if rc != N.OK:
+            msg = self._lib.tetris_last_error().decode(errors="replace")
+            raise ValueError(msg) if rc == N.INVALID_ARGUMENT else N.TetrisError(rc, msg)
+
+    launches_per_step = 3
+
+
+class _MappedTensor:
+    """Stand-in exposing a device address for a pinned host tensor (zero-copy reads by the kernels)."""
+
+    def __init__(self, host: torch.Tensor):
+        if host.is_cuda or not host.is_contiguous():
+            raise ValueError("expected a contiguous host tensor")
+        self.host = host
+        self._dev = N.map_host(host.data_ptr(), host.numel() * host.element_size())
+
+    def data_ptr(self) -> int:
+        return self._dev
+
+
+class HostTetrisStep:
+    """The same step for HOST-resident inputs (the end-to-end API): small per-request inputs (conf, lengths, draft
+    tokens, uniforms) are copied host->device; the large target/draft probability tensors stay in pinned host memory
+    and the streaming kernel reads only the rows it needs over the host link (zero-copy); the compacted token stream
+    and per-request results are copied back into pinned host buffers.  `run` is stream-ordered; call
+    `torch.cuda.current_stream().synchronize()` (or `wait()`) before reading `tokens_host`."""
+
+    def __init__(self, B: int, k: int, V: int, capacity: int, p_host: torch.Tensor, q_host: torch.Tensor,
+                 mode: str = "stochastic", device="cuda"):
+        self.step = TetrisStep(B, k, V, capacity, mode=mode, device=device)
+        dev = self.step.device
+        self.p = _MappedTensor(p_host)
+        self.q = _MappedTensor(q_host) if q_host is not None else None
+        self.conf = torch.empty(B, k, dtype=_F64, device=dev)
+        self.lengths = torch.empty(B, dtype=_I32, device=dev)
+        self.d = torch.empty(B, k, dtype=_I32, device=dev)
+        self.u_acc = torch.empty(B, k, dtype=_F64, device=dev)
+        self.u_res = torch.empty(B, dtype=_F64, device=dev)
+        self.offsets_host = torch.empty(B + 1, dtype=_I32).pin_memory()
+        self.tokens_host = torch.empty(B * (k + 1), dtype=_I32).pin_memory()
+        self.accepted_host = torch.empty(B, dtype=_I32).pin_memory()
+        self.B, self.k, self.V = B, k, V
+
+    def h2d_bytes(self) -> int:
+        B, k = self.B, self.k
+        return B * k * 8 + B * 4 + B * k * 4 + B * k * 8 + B * 8
+
+    def d2h_bytes(self) -> int:
+        return (self.B + 1) * 4 + self.B * (self.k + 1) * 4 + self.B * 4
+
+    def run(self, conf_h, lengths_h, d_h, u_acc_h=None, u_res_h=None) -> None:
+        self.conf.copy_(conf_h, non_blocking=True)
+        self.lengths.copy_(lengths_h, non_blocking=True)
+        self.d.copy_(d_h, non_blocking=True)
+        if u_acc_h is not None:
+            self.u_acc.copy_(u_acc_h, non_blocking=True)
+            self.u_res.copy_(u_res_h, non_blocking=True)
+        self.step.run(self.conf, self.lengths, self.p, self.q, self.d, self.u_acc, self.u_res)
+        self.offsets_host.copy_(self.step.offsets, non_blocking=True)
+        self.tokens_host.copy_(self.step.tokens, non_blocking=True)
+        self.accepted_host.copy_(self.step.accepted, non_blocking=True)

@@ -1,0 +1,256 @@
+"""GPU parity: every CUDA stage against the CPU oracle (oracle/tetris_oracle.c) on identical seeded inputs.
+
+Bar: bit-exact windows / stats / cum bits / accepted lengths / emitted tokens / compacted streams; fp64 residual
+values within the stated tolerance.  All calls go through the C ABI (paper_2502_15197_b200._native).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2502_15197_b200 import _native as N
+from paper_2502_15197_b200 import ops
+from paper_2502_15197_b200.synthetic import make_batch, selection_instance
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _check_select(alpha, lengths, C, vals_are_cum=False):
+    a = alpha.to(DEV).contiguous()
+    ln = None if lengths is None else lengths.to(DEV).contiguous()
+    res = ops.select(a, C, ln, vals_are_cum=vals_are_cum, want_cum=True)
+    w_ref, cum_ref, st_ref = O.select(_np(a), C, None if ln is None else _np(ln), vals_are_cum=vals_are_cum)
+    w = _np(res.windows)
+    assert np.array_equal(w, w_ref), f"windows differ at rows {np.nonzero(w != w_ref)[0][:10]}"
+    st = _np(res.stats)
+    assert st[0] == st_ref[0] and st[1] == st_ref[1] and st[2] == st_ref[2], (st, st_ref)
+    off = _np(res.win_offsets)
+    assert off[0] == 0 and np.array_equal(np.diff(off), w)
+    L = np.full(a.shape[0], a.shape[1]) if ln is None else _np(ln)
+    cum = _np(res.cum)
+    mask = np.arange(a.shape[1])[None, :] < L[:, None]
+    assert np.array_equal(cum[mask].view(np.uint64), cum_ref[mask].view(np.uint64)), "cum bits differ"
+    ops.raise_for_status(res.status)
+    return res
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_select_random_small(seed):
+    rng = np.random.default_rng(seed)
+    B = int(rng.integers(1, 40))
+    k = int(rng.integers(1, 9))
+    a = torch.from_numpy(rng.random((B, k)))
+    ln = torch.from_numpy(rng.integers(1, k + 1, B).astype(np.int32))
+    for C in (0, 1, int(rng.integers(0, B * k + 3)), B * k, B * k + 5):
+        _check_select(a, ln, C)
+
+
+@pytest.mark.parametrize("kind", ["quantized", "ties", "zeros", "ragged", "random"])
+@pytest.mark.parametrize("B,k", [(16, 5), (256, 8), (1024, 16), (3000, 7)])
+def test_select_adversarial(kind, B, k):
+    a, ln = selection_instance(B, k, kind, seed=B + k)
+    for C in (1, B, B * k // 2, B * k - 1):
+        _check_select(a, ln, C)
+
+
+@pytest.mark.parametrize("B,k,C", [(16, 5, 48), (256, 8, 1024), (1024, 16, 8192), (16384, 16, 131072)]
+                         + [(4096, 16, c) for c in (4096, 8192, 16384, 32768, 65536)])
+def test_select_configs(B, k, C):
+    batch_conf = torch.rand(B, k, dtype=torch.float64, generator=torch.Generator().manual_seed(B * 7 + C))
+    _check_select(batch_conf ** 0.25, None, C)
+
+
+def test_select_given_cum_nonmonotone():
+    """select_tetris over arbitrary Candidate.cum lists (heap merge == top-C over the prefix-min envelope)."""
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        B, k = int(rng.integers(1, 30)), int(rng.integers(1, 7))
+        cum = np.round(rng.random((B, k)) * 8) / 8  # many ties, non-monotone rows
+        ln = rng.integers(0, k + 1, B).astype(np.int32)
+        for C in (1, int(rng.integers(0, B * k + 1)), B * k):
+            _check_select(torch.from_numpy(cum), torch.from_numpy(ln), C, vals_are_cum=True)
+
+
+def test_heap_stats_exact_comparisons():
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        B, k = int(rng.integers(1, 64)), int(rng.integers(1, 10))
+        a = torch.from_numpy(rng.random((B, k))).to(DEV)
+        C = int(rng.integers(0, B * k + 2))
+        res = ops.select(a, C, want_cum=True)
+        st = _np(ops.heap_stats(res.cum, C))
+        _, _, st_ref = O.select(_np(a), C)
+        assert np.array_equal(st, st_ref), (st, st_ref)
+
+
+def test_select_negative_capacity():
+    with pytest.raises(ValueError):
+        ops.select(torch.rand(2, 2, dtype=torch.float64, device=DEV), -1)
+
+
+def test_select_bad_alpha_flagged():
+    a = torch.tensor([[0.5, 1.5]], dtype=torch.float64, device=DEV)
+    res = ops.select(a, 1)
+    with pytest.raises(ValueError):
+        ops.raise_for_status(res.status)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+def _stochastic_parity(B, k, V, C, seed, ragged=False, packed=False):
+    bt = make_batch(B, k, V, seed=seed, ragged=ragged)
+    sel = ops.select(bt.conf, C, bt.lengths)
+    if packed:
+        n = int(sel.win_offsets[-1].item())
+        u_acc = torch.rand(max(n, 1), dtype=torch.float64, device=DEV, generator=torch.Generator(DEV).manual_seed(seed))
+        res = ops.verify_stochastic(bt.p, bt.q, bt.d, sel.windows, u_acc, bt.u_res, sel.win_offsets, want_mass=True)
+        woff = _np(sel.win_offsets)
+    else:
+        u_acc = bt.u_acc
+        res = ops.verify_stochastic(bt.p, bt.q, bt.d, sel.windows, u_acc, bt.u_res, want_mass=True)
+        woff = None
+    ops.raise_for_status(res.status)
+    acc_ref, tok_ref, mass_ref = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), _np(sel.windows), _np(u_acc),
+                                                     _np(bt.u_res), woff, nthreads=8)
+    acc, tok, mass = _np(res.accepted), _np(res.out_tok), _np(res.mass)
+    assert np.array_equal(acc, acc_ref), f"accepted differ at {np.nonzero(acc != acc_ref)[0][:10]}"
+    assert np.array_equal(tok, tok_ref), f"tokens differ at {np.nonzero(tok != tok_ref)[0][:10]}"
+    assert np.array_equal(mass.view(np.uint64), mass_ref.view(np.uint64)), "mass bits differ"
+    off, toks = ops.compact(res.accepted, res.out_tok, bt.d)
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d))
+    assert np.array_equal(_np(off), off_ref)
+    assert np.array_equal(_np(toks)[: off_ref[-1]], toks_ref)
+    return acc, _np(sel.windows)
+
+
+@pytest.mark.parametrize("B,k,V,C,seed", [(16, 5, 32000, 48, 0), (256, 8, 32000, 1024, 1), (64, 8, 1000, 300, 2),
+                                          (33, 3, 8200, 40, 3), (7, 2, 13, 9, 4), (128, 16, 128256, 1024, 5)])
+def test_stochastic_parity(B, k, V, C, seed):
+    acc, w = _stochastic_parity(B, k, V, C, seed)
+    assert (acc <= w).all()
+
+
+def test_stochastic_parity_ragged_packed():
+    _stochastic_parity(100, 6, 4096, 333, 7, ragged=True, packed=True)
+
+
+def test_greedy_parity():
+    for (B, k, V, C, seed) in [(16, 5, 32000, 48, 0), (64, 4, 1003, 100, 1), (200, 8, 32000, 900, 2)]:
+        bt = make_batch(B, k, V, seed=seed, mode="greedy")
+        sel = ops.select(bt.conf, C, bt.lengths)
+        res = ops.verify_greedy(bt.p, bt.d, sel.windows)
+        ops.raise_for_status(res.status)
+        acc_ref, tok_ref = O.verify_greedy(_np(bt.p), _np(bt.d), _np(sel.windows), nthreads=8)
+        assert np.array_equal(_np(res.accepted), acc_ref)
+        assert np.array_equal(_np(res.out_tok), tok_ref)
+
+
+def test_greedy_ties_and_nan():
+    B, k, V = 4, 2, 300
+    p = torch.zeros(B, k + 1, V, dtype=torch.float32)
+    p[0, :, 5] = 1.0
+    p[0, :, 7] = 1.0          # tie -> first index 5
+    p[1, 0, 9] = float("nan")  # NaN ranks highest
+    p[1, 0, 3] = 2.0
+    p[2, :, 299] = 0.5
+    p[3, 1, 0] = -0.0
+    d = torch.tensor([[5, 5], [9, 1], [299, 299], [0, 1]], dtype=torch.int32)
+    w = torch.tensor([2, 2, 1, 2], dtype=torch.int32)
+    res = ops.verify_greedy(p.to(DEV), d.to(DEV), w.to(DEV))
+    acc_ref, tok_ref = O.verify_greedy(p.numpy(), d.numpy(), w.numpy())
+    assert np.array_equal(_np(res.accepted), acc_ref)
+    assert np.array_equal(_np(res.out_tok), tok_ref)
+
+
+def test_sample_rows_and_residual_f64():
+    rng = np.random.default_rng(3)
+    for V in (2, 3, 8, 100, 8191, 8192, 8193, 40000):
+        R = 5
+        ps = rng.dirichlet(np.ones(V), size=R)
+        pt = rng.dirichlet(np.ones(V), size=R)
+        u = rng.random(R)
+        rows = torch.arange(R, dtype=torch.int64, device=DEV)
+        idx, mass, st = ops.sample_rows(torch.from_numpy(pt).to(DEV), rows, torch.from_numpy(u).to(DEV),
+                                        q=torch.from_numpy(ps).to(DEV), q_row=rows)
+        ops.raise_for_status(st)
+        for r in range(R):
+            i_ref, m_ref = O.sample(pt[r], u[r], q=ps[r])
+            assert int(idx[r]) == i_ref and float(mass[r]) == m_ref
+        out, mass2, st = ops.residual(torch.from_numpy(ps).to(DEV), torch.from_numpy(pt).to(DEV))
+        ops.raise_for_status(st)
+        for r in range(R):
+            ref, m_ref, rc = O.residual(ps[r], pt[r])
+            assert rc == 0 and float(mass2[r]) == m_ref
+            assert np.array_equal(_np(out[r]), ref)
+            # against the reference's own formula (pairwise np.sum mass): fp64 tolerance
+            diff = np.clip(pt[r] - ps[r], 0.0, None)
+            np.testing.assert_allclose(_np(out[r]), diff / diff.sum(), rtol=1e-12, atol=1e-15)
+
+
+def test_residual_degenerate():
+    p = torch.tensor([[0.3, 0.7]], dtype=torch.float64, device=DEV)
+    _, _, st = ops.residual(p, p.clone())
+    from paper_2502_15197_b200.errors import DegenerateResidualError
+
+    with pytest.raises(DegenerateResidualError):
+        ops.raise_for_status(st)
+
+
+def test_verify_matrix_parity():
+    rng = np.random.default_rng(9)
+    B, k = 500, 9
+    alpha = rng.random((B, k))
+    w = rng.integers(0, k + 1, B).astype(np.int32)
+    off = np.zeros(B + 1, np.int32)
+    off[1:] = np.cumsum(w)
+    u = rng.random(max(1, off[-1]))
+    acc = ops.verify_matrix(torch.from_numpy(alpha).to(DEV), torch.from_numpy(w).to(DEV),
+                            torch.from_numpy(off).to(DEV), torch.from_numpy(u).to(DEV))
+    assert np.array_equal(_np(acc), O.verify_matrix(alpha, w, u))
+
+
+def test_expected_accepted_parity():
+    rng = np.random.default_rng(4)
+    alpha = rng.random((300, 7))
+    w = rng.integers(0, 8, 300).astype(np.int32)
+    v = ops.expected_accepted(torch.from_numpy(alpha).to(DEV), torch.from_numpy(w).to(DEV))
+    assert float(v) == O.expected_accepted(alpha, w)
+
+
+def test_compact_cap():
+    rng = np.random.default_rng(1)
+    B, k = 300, 6
+    acc = rng.integers(0, k + 1, B).astype(np.int32)
+    tok = rng.integers(0, 100, B).astype(np.int32)
+    d = rng.integers(0, 100, (B, k)).astype(np.int32)
+    cap = rng.integers(1, k + 3, B).astype(np.int32)
+    off, toks = ops.compact(*(torch.from_numpy(x).to(DEV) for x in (acc, tok, d, cap)))
+    off_ref, toks_ref = O.compact(acc, tok, d, cap)
+    assert np.array_equal(_np(off), off_ref)
+    assert np.array_equal(_np(toks)[: off_ref[-1]], toks_ref)
+
+
+def test_step_graph_capture_matches_eager():
+    B, k, V, C = 64, 8, 32000, 256
+    bt = make_batch(B, k, V, seed=21)
+    step = ops.TetrisStep(B, k, V, C)
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    ref = (step.accepted.clone(), step.out_tok.clone(), step.tokens.clone())
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        step.accepted.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(step.accepted, ref[0]) and torch.equal(step.out_tok, ref[1])
+    assert torch.equal(step.tokens, ref[2])
