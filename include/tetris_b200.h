@@ -111,6 +111,11 @@ int tetris_verify_matrix_f64(const double* alpha, const int32_t* len, const int3
                              const int32_t* win_offsets, const double* u, int32_t B, int32_t k,
                              int32_t* accepted, uint32_t* status, tetris_stream_t stream);
 
+/* Token-level verify_token (accept_model.py:291-313) for R independent (draft row, target row, token, u) tuples:
+ * s = p_draft[r][token[r]], m = p_target[r][token[r]]; accepted[r] = (s <= m) || (u[r] < m / s).  Rows are V f64. */
+int tetris_verify_tokens_f64(const double* p_draft, const double* p_target, const int32_t* token, const double* u,
+                             int32_t R, int32_t V, int32_t* accepted, uint32_t* status, tetris_stream_t stream);
+
 /* Stage (3) stochastic: per request b, positions j < windows[b] are tested with verify_token's rule
  * (accept_model.py:309-313): s=(double)q[b][j][d], m=(double)p[b][j][d]; accept iff s<=m or u<m/s.
  * accepted[b] = first rejection (or windows[b]).  On rejection the emitted token is sampled (sampling contract
@@ -123,6 +128,34 @@ int tetris_verify_stochastic_f32(const float* p, const float* q, const int32_t* 
                                  int32_t B, int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
                                  double* mass_out, uint32_t* status, void* ws, size_t ws_bytes,
                                  tetris_stream_t stream);
+
+/* The whole stochastic step in two launches (the product hot path), also callable as its two halves:
+ *   tetris_select_accept_f32 — select_kernel (cluster) with its epilogue: prefix products, global top-C windows +
+ *      win_offsets + stats, the accept test of every selected position, accepted[b], the row to resample from
+ *      (kept in the workspace), the compaction offsets (n_b = accepted[b]+1, capped by cap[b] when cap != NULL) and
+ *      the accepted-prefix tokens d[b][0..a_b);
+ *   tetris_resample_f32 — persist_stream_kernel: the TMA-pipelined residual / bonus sampler over the rows chosen by
+ *      the previous tetris_select_accept_f32 on the same workspace; writes out_tok[b] (and mass_out) and, when
+ *      tokens != NULL, drops the sample into tokens[offsets[b] + accepted[b]] if the cap leaves room.
+ * Same results as tetris_select_f64 + tetris_verify_stochastic_f32 + tetris_compact (u_packed selects the
+ * uniform layout as win_offsets != NULL does there).  Requires V % 8 == 0 and 16-byte aligned p, q.
+ * Request sharding: the selection runs over all B_sel rows of conf/len (every shard's scores, gathered) with the
+ * global capacity C and writes windows/win_offsets for all of them; the verification tensors (p, q, d, u_acc, u_res,
+ * cap, accepted, out_tok, mass_out, offsets, tokens) cover only this shard's rows [row0, row0 + B). */
+int tetris_select_accept_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                             int32_t row0, int32_t B, const float* p, const float* q, const int32_t* d,
+                             const double* u_acc, int32_t u_packed, const int32_t* cap, int32_t V, int32_t* windows,
+                             int32_t* win_offsets, int32_t* accepted, int32_t* offsets, int32_t* tokens,
+                             int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+int tetris_resample_f32(const float* p, const float* q, const double* u_res, int32_t B, int32_t k, int32_t V,
+                        const int32_t* accepted, const int32_t* offsets, int32_t* out_tok, double* mass_out,
+                        int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                               int32_t row0, int32_t B, const float* p, const float* q, const int32_t* d,
+                               const double* u_acc, int32_t u_packed, const double* u_res, const int32_t* cap,
+                               int32_t V, int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                               double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status,
+                               void* ws, size_t ws_bytes, tetris_stream_t stream);
 
 /* Stage (3) greedy: verify_token on one-hot distributions (accept_model.py:309-313): position j is accepted iff
  * d[b][j] == argmax_v p[b][j][v] (first maximal index, NaN ranks highest as in numpy.argmax); the emitted token is

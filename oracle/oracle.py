@@ -31,6 +31,8 @@ def _load():
         lib.oracle_select.argtypes = [_p, _p, C.c_int, C.c_int, C.c_int64, C.c_int, _p, _p, _p]
         lib.oracle_expected_accepted.restype = C.c_double
         lib.oracle_expected_accepted.argtypes = [_p, _p, _p, C.c_int, C.c_int]
+        lib.oracle_verify_token.restype = C.c_int
+        lib.oracle_verify_token.argtypes = [C.c_double, C.c_double, C.c_double]
         lib.oracle_verify_matrix.restype = None
         lib.oracle_verify_matrix.argtypes = [_p, _p, _p, _p, C.c_int, C.c_int, _p]
         lib.oracle_sample_f64.restype = C.c_int
@@ -78,6 +80,11 @@ def expected_accepted(alpha, windows, lengths=None):
     B, k = alpha.shape
     w = _a(windows, np.int32)
     return float(_load().oracle_expected_accepted(_ptr(alpha), None, _ptr(w), B, k))
+
+
+def verify_token(p_draft, p_target, token, u) -> bool:
+    """verify_token (accept_model.py:291-313) on fp64 rows."""
+    return bool(_load().oracle_verify_token(float(p_draft[token]), float(p_target[token]), float(u)))
 
 
 def verify_matrix(alpha, windows, u):

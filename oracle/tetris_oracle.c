@@ -163,6 +163,9 @@ double oracle_expected_accepted(const double* alpha, const int32_t* len, const i
   return value;
 }
 
+/* verify_token's rule (accept_model.py:309-313) on the two gathered masses. */
+int oracle_verify_token(double s, double m, double u) { return (s <= m) || (u < m / s); }
+
 void oracle_verify_matrix(const double* alpha, const int32_t* windows, const int32_t* win_off, const double* u,
                           int B, int k, int32_t* accepted) {
   for (int r = 0; r < B; ++r) {

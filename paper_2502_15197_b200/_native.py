@@ -59,8 +59,16 @@ _SIGNATURES = {
     "tetris_heap_stats_f64": (C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _sz, _p]),
     "tetris_expected_accepted_f64": (C.c_int, [_p, _p, _p, _i32, _i32, _p, _p, _p]),
     "tetris_verify_matrix_f64": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _p, _p, _p]),
+    "tetris_verify_tokens_f64": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _p, _p, _p]),
     "tetris_verify_stochastic_f32": (
         C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _p, _sz, _p]),
+    "tetris_select_accept_f32": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
+                  _sz, _p]),
+    "tetris_resample_f32": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "tetris_step_stochastic_f32": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p,
+                  _p, _p, _p, _sz, _p]),
     "tetris_verify_greedy_f32": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_sample_rows_f64": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_sample_rows_f32": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _sz, _p]),

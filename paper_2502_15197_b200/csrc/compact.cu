@@ -62,6 +62,25 @@ __global__ void verify_matrix_kernel(const double* __restrict__ alpha, const int
   set_status(status, bad);
 }
 
+__global__ void verify_tokens_kernel(const double* __restrict__ ps, const double* __restrict__ pt,
+                                     const int32_t* __restrict__ token, const double* __restrict__ u, int R, int V,
+                                     int32_t* __restrict__ accepted, uint32_t* status) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int t = token[r];
+  const double ur = u[r];
+  uint32_t bad = 0;
+  if (t < 0 || t >= V) bad |= TETRIS_ST_BAD_TOKEN;         // accept_model.py:305-306
+  if (!(ur >= 0.0 && ur < 1.0)) bad |= TETRIS_ST_BAD_UNIFORM;  // accept_model.py:307-308
+  int acc = 0;
+  if (!(bad & TETRIS_ST_BAD_TOKEN)) {
+    const double s = ps[(int64_t)r * V + t], m = pt[(int64_t)r * V + t];
+    acc = (s <= m) || (ur < m / s);  // accept_model.py:309-313
+  }
+  accepted[r] = acc;
+  set_status(status, bad);
+}
+
 }  // namespace tetris
 
 #include "abi_util.h"
@@ -86,5 +105,17 @@ extern "C" int tetris_verify_matrix_f64(const double* alpha, const int32_t* len,
   if (!alpha || !windows || !win_offsets || !accepted) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   verify_matrix_kernel<<<(B + 255) / 256, 256, 0, (cudaStream_t)stream>>>(alpha, len, windows, win_offsets, u, B, k,
                                                                           accepted, status);
+  return abi::launch_check();
+}
+
+extern "C" int tetris_verify_tokens_f64(const double* p_draft, const double* p_target, const int32_t* token,
+                                        const double* u, int32_t R, int32_t V, int32_t* accepted, uint32_t* status,
+                                        tetris_stream_t stream) {
+  using namespace tetris;
+  if (R < 0 || V < 1) return abi::fail(TETRIS_INVALID_ARGUMENT, "bad shape R=%d V=%d", R, V);
+  if (R == 0) return TETRIS_OK;
+  if (!p_draft || !p_target || !token || !u || !accepted) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  verify_tokens_kernel<<<(R + 255) / 256, 256, 0, (cudaStream_t)stream>>>(p_draft, p_target, token, u, R, V, accepted,
+                                                                          status);
   return abi::launch_check();
 }

@@ -1,0 +1,63 @@
+// Launch-level declarations shared by the kernel translation units (host + device visible).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tetris {
+
+struct SelectArgs {
+  const double* vals;
+  const int32_t* len;
+  int B, k;
+  long long C;
+  int vals_are_cum;
+  int32_t* windows;
+  int32_t* win_offsets;
+  double* cum_out;
+  long long* stats;
+  uint32_t* status;
+  int RB;  // rows per CTA
+  // fused accept + compaction epilogue (p == nullptr: off) for the local rows [ep_row0, ep_row0 + ep_rows); the
+  // per-request tensors below are indexed by local row (global row - ep_row0)
+  int ep_row0, ep_rows;
+  const float* p;
+  const float* q;
+  const int32_t* d;
+  const double* u_acc;
+  int u_packed;
+  int V;
+  const int32_t* cap;
+  int32_t* accepted;
+  long long* rowinfo;  // [B][2]: p row, q row (-1: bonus)
+  int32_t* offsets;    // [B+1]
+  int32_t* tokens;
+};
+
+struct StreamArgs {
+  const float* p;
+  const float* q;
+  int V, nch, R;
+  const long long* prow;     // p row of request b at prow[b * row_stride]
+  const long long* qrow;     // q row (-1: plain / bonus row) at qrow[b * row_stride]; nullptr: all plain
+  int row_stride;
+  const double* u;           // [R]
+  int32_t* out_idx;
+  double* mass_out;
+  uint32_t* status;
+  int* counters;
+  double* chunk_sums;
+  double* warp_sums;
+  // fused compaction (accepted == nullptr: off): tokens[offsets[b] + accepted[b]] = sample, if it fits the cap
+  const int32_t* accepted;
+  const int32_t* offsets;
+  int32_t* tokens;
+};
+
+int launch_select(const SelectArgs& a, cudaStream_t st);
+int launch_persist_stream(const StreamArgs& a, cudaStream_t st);
+bool persist_eligible(const float* p, const float* q, int V);
+int launch_accept(const float* p, const float* q, const int32_t* d, const int32_t* windows, const int32_t* win_off,
+                  const double* u_acc, int B, int k, int V, int32_t* accepted, long long* rowinfo, uint32_t* status,
+                  cudaStream_t st);
+
+}  // namespace tetris

@@ -14,6 +14,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "launch.h"
 
 namespace tetris {
 
@@ -375,7 +376,7 @@ int sample_rows_impl(const T* p, const T* q, const int64_t* p_row, const int64_t
   if (R == 0) return TETRIS_OK;
   if (!p || !p_row || !u || !out_idx) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(R, 0, V, ws, ws_bytes))) return rc;
-  const bool vec = (V % (32 / sizeof(T)) == 0) && aligned32(p) && (!q || aligned32(q));
+  const bool vec = (V % kLaneElems == 0) && aligned32(p) && (!q || aligned32(q));  // whole lanes only
   dim3 grid(n_chunks(V), R);
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_COUNTERS);
   double* cs = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_CHUNK_SUMS);
@@ -403,12 +404,34 @@ extern "C" int tetris_verify_stochastic_f32(const float* p, const float* q, cons
   if (!p || !q || !d || !windows || !u_acc || !u_res || !accepted || !out_tok)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
-  const bool vec = (V % 8 == 0) && aligned32(p) && aligned32(q);
-  dim3 grid(n_chunks(V), B);
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   double* cs = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
   double* wsum = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
   cudaStream_t st = (cudaStream_t)stream;
+  if (persist_eligible(p, q, V)) {
+    // accept test -> row choice -> persistent TMA-pipelined sampler
+    long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+    if ((rc = launch_accept(p, q, d, windows, win_offsets, u_acc, B, k, V, accepted, rowinfo, status, st))) return rc;
+    StreamArgs a = {};
+    a.p = p;
+    a.q = q;
+    a.V = V;
+    a.nch = n_chunks(V);
+    a.R = B;
+    a.prow = rowinfo;
+    a.qrow = rowinfo + 1;
+    a.row_stride = 2;
+    a.u = u_res;
+    a.out_idx = out_tok;
+    a.mass_out = mass_out;
+    a.status = status;
+    a.counters = cnt;
+    a.chunk_sums = cs;
+    a.warp_sums = wsum;
+    return launch_persist_stream(a, st);
+  }
+  const bool vec = (V % 8 == 0) && aligned32(p) && aligned32(q);
+  dim3 grid(n_chunks(V), B);
   if (vec)
     sample_kernel<float, true, true><<<grid, kStreamThreads, 0, st>>>(p, q, d, windows, win_offsets, u_acc, k,
                                                                       accepted, nullptr, nullptr, u_res, V, out_tok,
@@ -418,6 +441,102 @@ extern "C" int tetris_verify_stochastic_f32(const float* p, const float* q, cons
                                                                        accepted, nullptr, nullptr, u_res, V,
                                                                        out_tok, mass_out, status, cnt, cs, wsum);
   return abi::launch_check();
+}
+
+extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                        int32_t row0, int32_t B, const float* p, const float* q, const int32_t* d,
+                                        const double* u_acc, int32_t u_packed, const int32_t* cap, int32_t V,
+                                        int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* offsets,
+                                        int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                        tetris_stream_t stream) {
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
+  if (B == 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "empty batch");
+  if (B_sel < B || B_sel > TETRIS_MAX_SELECT_ROWS || row0 < 0 || row0 + B > B_sel)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "local rows [%d, %d) outside the %d selected rows", row0, row0 + B, B_sel);
+  if (u_packed && B != B_sel) return abi::fail(TETRIS_INVALID_ARGUMENT, "packed uniforms need the whole batch");
+  if (!conf || !p || !q || !d || !u_acc || !windows || !win_offsets || !accepted || !offsets || !tokens)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
+  SelectArgs sa = {};
+  sa.vals = conf;
+  sa.len = len;
+  sa.B = B_sel;
+  sa.k = k;
+  sa.C = (long long)C;
+  sa.windows = windows;
+  sa.win_offsets = win_offsets;
+  sa.stats = (long long*)stats4;
+  sa.status = status;
+  sa.ep_row0 = row0;
+  sa.ep_rows = B;
+  sa.p = p;
+  sa.q = q;
+  sa.d = d;
+  sa.u_acc = u_acc;
+  sa.u_packed = u_packed;
+  sa.V = V;
+  sa.cap = cap;
+  sa.accepted = accepted;
+  sa.rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+  sa.offsets = offsets;
+  sa.tokens = tokens;
+  return launch_select(sa, (cudaStream_t)stream);
+}
+
+extern "C" int tetris_resample_f32(const float* p, const float* q, const double* u_res, int32_t B, int32_t k, int32_t V,
+                                   const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
+                                   double* mass_out, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
+                                   tetris_stream_t stream) {
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (B == 0) return TETRIS_OK;
+  if (!p || !q || !u_res || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
+  if (!persist_eligible(p, q, V))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "the streaming sampler needs V %% 8 == 0 and 16-byte aligned p/q");
+  long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+  StreamArgs a = {};
+  a.p = p;
+  a.q = q;
+  a.V = V;
+  a.nch = n_chunks(V);
+  a.R = B;
+  a.prow = rowinfo;
+  a.qrow = rowinfo + 1;
+  a.row_stride = 2;
+  a.u = u_res;
+  a.out_idx = out_tok;
+  a.mass_out = mass_out;
+  a.status = status;
+  a.counters = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
+  a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
+  a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
+  if (tokens) {
+    if (!accepted || !offsets) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted and offsets");
+    a.accepted = accepted;
+    a.offsets = offsets;
+    a.tokens = tokens;
+  }
+  return launch_persist_stream(a, (cudaStream_t)stream);
+}
+
+extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k,
+                                          int64_t C, int32_t row0, int32_t B, const float* p, const float* q,
+                                          const int32_t* d, const double* u_acc, int32_t u_packed,
+                                          const double* u_res, const int32_t* cap, int32_t V, int32_t* windows,
+                                          int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                                          double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                          uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  if (!persist_eligible(p, q, V))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "fused step needs V %% 8 == 0 and 16-byte aligned p/q");
+  if (!u_res || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  int rc = tetris_select_accept_f32(conf, len, B_sel, k, C, row0, B, p, q, d, u_acc, u_packed, cap, V, windows,
+                                    win_offsets, accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
+  if (rc) return rc;
+  return tetris_resample_f32(p, q, u_res, B, k, V, accepted, offsets, out_tok, mass_out, tokens, status, ws, ws_bytes,
+                             stream);
 }
 
 extern "C" int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B,
@@ -452,6 +571,26 @@ extern "C" int tetris_sample_rows_f64(const double* p, const double* q, const in
 extern "C" int tetris_sample_rows_f32(const float* p, const float* q, const int64_t* p_row, const int64_t* q_row,
                                       const double* u, int32_t R, int32_t V, int32_t* out_idx, double* mass_out,
                                       uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  if (R > 0 && R <= 65535 && V >= 1 && p && p_row && u && out_idx && persist_eligible(p, q, V) &&
+      ws_bytes >= tetris_workspace_bytes(TETRIS_OP_VERIFY, R, 0, V) && ws) {
+    StreamArgs a = {};
+    a.p = p;
+    a.q = q;
+    a.V = V;
+    a.nch = n_chunks(V);
+    a.R = R;
+    a.prow = (const long long*)p_row;
+    a.qrow = (q && q_row) ? (const long long*)q_row : nullptr;
+    a.row_stride = 1;
+    a.u = u;
+    a.out_idx = out_idx;
+    a.mass_out = mass_out;
+    a.status = status;
+    a.counters = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_COUNTERS);
+    a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_CHUNK_SUMS);
+    a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_WARP_SUMS);
+    return launch_persist_stream(a, (cudaStream_t)stream);
+  }
   return sample_rows_impl<float>(p, q, p_row, q_row, u, R, V, out_idx, mass_out, status, ws, ws_bytes,
                                  (cudaStream_t)stream);
 }

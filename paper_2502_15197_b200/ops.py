@@ -187,6 +187,25 @@ def verify_matrix(alpha: torch.Tensor, windows: torch.Tensor, win_offsets: torch
     return acc
 
 
+def verify_tokens(p_draft: torch.Tensor, p_target: torch.Tensor, token: torch.Tensor, u: torch.Tensor,
+                  status: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """verify_token (accept_model.py:291-313) for R (draft row, target row, token, u) tuples; rows [R, V] f64."""
+    p_draft = _need_cuda("p_draft", p_draft, _F64, 2)
+    p_target = _need_cuda("p_target", p_target, _F64, 2)
+    if p_draft.shape != p_target.shape:
+        raise ValueError(f"vocabulary mismatch: draft {tuple(p_draft.shape)} vs target {tuple(p_target.shape)}")
+    R, V = p_draft.shape
+    token = _need_cuda("token", token, _I32, 1)
+    u = _need_cuda("u", u, _F64, 1)
+    acc = torch.empty(R, dtype=_I32, device=p_draft.device)
+    st = status if status is not None else new_status(p_draft.device)
+    N.call("tetris_verify_tokens_f64", _ptr(p_draft), _ptr(p_target), _ptr(token), _ptr(u), R, V, _ptr(acc), _ptr(st),
+           _stream_handle())
+    if status is None:
+        raise_for_status(st, "verify_token")
+    return acc
+
+
 @dataclass
 class VerifyResult:
     accepted: torch.Tensor  # [B] i32
@@ -343,7 +362,9 @@ class TetrisStep:
         self._lib = N.load()
 
     def run(self, conf, lengths, p, q, d, u_acc=None, u_res=None, cap=None, events=None) -> None:
-        """events: optional 4 torch.cuda.Events recorded around select / verify / compact (kernel timing)."""
+        """events: optional 4 torch.cuda.Events recorded around select / verify / compact (kernel timing).  The
+        stochastic step is two launches (select+accept+compaction offsets, then the streaming sampler), so its
+        events bracket [select kernel | sampler | nothing]."""
         lib, ws, s = self._lib, self.ws, torch.cuda.current_stream().cuda_stream
         B, k, V = self.B, self.k, self.V
         if events is not None:
@@ -356,22 +377,35 @@ class TetrisStep:
             sel_conf, sel_len = self.conf_all, self.len_all
         else:
             sel_conf, sel_len = conf, lengths
+        if self.mode == "stochastic":
+            # == tetris_step_stochastic_f32, called as its two halves so an event can sit between the kernels
+            rc = lib.tetris_select_accept_f32(
+                sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, self.rank * B, B, p.data_ptr(), q.data_ptr(),
+                d.data_ptr(), u_acc.data_ptr(), int(self.u_layout == "packed"), _ptr(cap), V,
+                self.windows_all.data_ptr(), self.win_offsets.data_ptr(), self.accepted.data_ptr(),
+                self.offsets.data_ptr(), self.tokens.data_ptr(), self.stats.data_ptr(), self.status.data_ptr(),
+                ws.ptr, ws.nbytes, s)
+            self._check(rc)
+            if events is not None:
+                events[1].record()
+            rc = lib.tetris_resample_f32(p.data_ptr(), q.data_ptr(), u_res.data_ptr(), B, k, V,
+                                         self.accepted.data_ptr(), self.offsets.data_ptr(), self.out_tok.data_ptr(),
+                                         self.mass.data_ptr(), self.tokens.data_ptr(), self.status.data_ptr(),
+                                         ws.ptr, ws.nbytes, s)
+            self._check(rc)
+            if events is not None:
+                events[2].record()
+                events[3].record()
+            return
         rc = lib.tetris_select_f64(sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, 0,
                                    self.windows_all.data_ptr(), self.win_offsets.data_ptr(), None,
                                    self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
         self._check(rc)
         if events is not None:
             events[1].record()
-        if self.mode == "stochastic":
-            woff = self.win_offsets.data_ptr() if self.u_layout == "packed" else None
-            rc = lib.tetris_verify_stochastic_f32(p.data_ptr(), q.data_ptr(), d.data_ptr(), self.windows.data_ptr(),
-                                                  woff, u_acc.data_ptr(), u_res.data_ptr(), B, k, V,
-                                                  self.accepted.data_ptr(), self.out_tok.data_ptr(),
-                                                  self.mass.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
-        else:
-            rc = lib.tetris_verify_greedy_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), B, k, V,
-                                              self.accepted.data_ptr(), self.out_tok.data_ptr(),
-                                              self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        rc = lib.tetris_verify_greedy_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), B, k, V,
+                                          self.accepted.data_ptr(), self.out_tok.data_ptr(),
+                                          self.status.data_ptr(), ws.ptr, ws.nbytes, s)
         self._check(rc)
         if events is not None:
             events[2].record()
@@ -386,7 +420,9 @@ class TetrisStep:
             msg = self._lib.tetris_last_error().decode(errors="replace")
             raise ValueError(msg) if rc == N.INVALID_ARGUMENT else N.TetrisError(rc, msg)
 
-    launches_per_step = 3
+    @property
+    def launches_per_step(self) -> int:
+        return 2 if self.mode == "stochastic" else 3
 
 
 class _MappedTensor:

@@ -1,0 +1,70 @@
+"""CPU: the C-ABI library builds for sm_100a, loads without a GPU, exports every symbol include/tetris_b200.h
+declares, and the Python binding's contract constants equal the header's."""
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2502_15197_b200 import _native as N
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "tetris_b200.h"
+
+
+def _declared():
+    txt = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(tetris_[a-z0-9_]+)\s*\(", txt)) - {"tetris_stream_t"})
+
+
+def test_library_loads_and_exports_header_symbols():
+    lib = N.load()
+    for name in _declared():
+        assert hasattr(lib, name), f"{name} declared in the header but not exported"
+    assert set(_declared()) == set(N.EXPORTS), "ctypes signature table out of sync with the header"
+    assert lib.tetris_abi_version() == 1
+
+
+def test_cubin_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(N.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_contract_constants_match_header():
+    txt = HEADER.read_text()
+
+    def define(name):
+        m = re.search(rf"#define {name} (\S+)", txt)
+        return m.group(1)
+
+    assert int(define("TETRIS_LANE_ELEMS")) == N.LANE_ELEMS
+    assert int(define("TETRIS_WARP_SEGS")) == N.WARP_SEGS
+    assert int(define("TETRIS_CHUNK_WARPS")) == N.CHUNK_WARPS
+    assert N.SEG_ELEMS == 32 * N.LANE_ELEMS and N.CHUNK_ELEMS == N.SEG_ELEMS * N.WARP_SEGS * N.CHUNK_WARPS
+    assert int(define("TETRIS_MAX_K")) == N.MAX_K
+    for name, val in [("TETRIS_OK", N.OK), ("TETRIS_INVALID_ARGUMENT", N.INVALID_ARGUMENT),
+                      ("TETRIS_DEGENERATE_RESIDUAL", N.DEGENERATE_RESIDUAL), ("TETRIS_CUDA_ERROR", N.CUDA_ERROR)]:
+        assert int(define(name)) == val
+
+
+def test_host_side_argument_errors_without_gpu():
+    """Argument validation happens before any launch, so it is testable here: negative capacity -> ValueError."""
+    with pytest.raises(ValueError, match="capacity"):
+        N.call("tetris_select_f64", None, None, 4, 2, -1, 0, None, None, None, None, None, None, 0, None)
+    with pytest.raises(ValueError, match="workspace"):
+        N.call("tetris_verify_stochastic_f32", 1, 1, 1, 1, None, 1, 1, 4, 2, 128, 1, 1, None, None, None, 0, None)
+    assert N.workspace_bytes(N.OP_ALL, 1024, 16, 128256) > N.workspace_bytes(N.OP_SELECT, 1024, 16, 0)
+
+
+def test_no_cpu_fallback_in_product_path():
+    """The product modules never import the oracle and fail loudly without CUDA tensors."""
+    import torch
+
+    from paper_2502_15197_b200 import ops
+
+    pkg = ROOT / "paper_2502_15197_b200"
+    for f in pkg.glob("*.py"):
+        src = f.read_text()
+        assert "import oracle" not in src and "reference_port" not in src, f
+    with pytest.raises(ValueError, match="CUDA"):
+        ops.select(torch.zeros(2, 2, dtype=torch.float64), 1)

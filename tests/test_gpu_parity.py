@@ -254,3 +254,78 @@ def test_step_graph_capture_matches_eager():
     torch.cuda.synchronize()
     assert torch.equal(step.accepted, ref[0]) and torch.equal(step.out_tok, ref[1])
     assert torch.equal(step.tokens, ref[2])
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# the fused two-launch step (select+accept+offsets, persistent TMA sampler) == the stage-by-stage oracle
+def _fused_vs_oracle(B, k, V, C, seed, ragged=False, packed=False, cap=False):
+    bt = make_batch(B, k, V, seed=seed, ragged=ragged)
+    step = ops.TetrisStep(B, k, V, C, u_layout="packed" if packed else "dense")
+    g = torch.Generator(DEV).manual_seed(seed + 1)
+    u_acc = torch.rand(B * k, dtype=torch.float64, device=DEV, generator=g) if packed else bt.u_acc
+    capt = torch.randint(1, k + 3, (B,), dtype=torch.int32, device=DEV, generator=g) if cap else None
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, u_acc, bt.u_res, cap=capt)
+    torch.cuda.synchronize()
+    ops.raise_for_status(step.status)
+    w_ref, _, st_ref = O.select(_np(bt.conf), C, _np(bt.lengths))
+    assert np.array_equal(_np(step.windows), w_ref)
+    assert list(_np(step.stats)[:3]) == list(st_ref[:3])
+    woff = np.concatenate([[0], np.cumsum(w_ref)]).astype(np.int32)
+    acc_ref, tok_ref, mass_ref = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), w_ref, _np(u_acc),
+                                                     _np(bt.u_res), woff if packed else None, nthreads=8)
+    assert np.array_equal(_np(step.accepted), acc_ref)
+    assert np.array_equal(_np(step.out_tok), tok_ref)
+    assert np.array_equal(_np(step.mass).view(np.uint64), mass_ref.view(np.uint64))
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None if capt is None else _np(capt))
+    assert np.array_equal(_np(step.offsets), off_ref)
+    assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
+
+
+@pytest.mark.parametrize("B,k,V,C,seed", [(16, 5, 32000, 48, 0), (256, 8, 32000, 1024, 1), (300, 7, 8200, 900, 2),
+                                          (1, 1, 8, 1, 3), (64, 16, 128256, 512, 4), (2000, 4, 1024, 3000, 5)])
+def test_fused_step_parity(B, k, V, C, seed):
+    _fused_vs_oracle(B, k, V, C, seed)
+
+
+def test_fused_step_ragged_packed_cap():
+    _fused_vs_oracle(200, 6, 4096, 700, 11, ragged=True, packed=True, cap=True)
+    _fused_vs_oracle(200, 6, 4096, 700, 12, ragged=True, packed=False, cap=True)
+
+
+def test_fused_step_full_cfg3_bit_exact():
+    """BASELINE cfg3 at full size (B=1024, k=16, C=8192, V=128256): every request's accepted length, emitted token
+    and row mass against the oracle.  Only the rows the oracle needs are copied to the host."""
+    B, k, V, C = 1024, 16, 128256, 8192
+    bt = make_batch(B, k, V, seed=42)
+    step = ops.TetrisStep(B, k, V, C)
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    ops.raise_for_status(step.status)
+    w_ref, _, _ = O.select(_np(bt.conf), C)
+    assert np.array_equal(_np(step.windows), w_ref)
+    # accept test from gathered values (torch gather, independent of the kernels)
+    d = bt.d.long()
+    m = bt.p[:, :k].gather(2, d.unsqueeze(-1)).squeeze(-1).double().cpu().numpy()
+    s = bt.q.gather(2, d.unsqueeze(-1)).squeeze(-1).double().cpu().numpy()
+    u = _np(bt.u_acc)
+    acc_ref = np.zeros(B, np.int64)
+    for b in range(B):
+        a = w_ref[b]
+        for j in range(w_ref[b]):
+            if not (s[b, j] <= m[b, j] or u[b, j] < m[b, j] / s[b, j]):
+                a = j
+                break
+        acc_ref[b] = a
+    assert np.array_equal(_np(step.accepted), acc_ref)
+    ures = _np(bt.u_res)
+    tok = _np(step.out_tok)
+    mass = _np(step.mass)
+    for b0 in range(0, B, 128):
+        bs = np.arange(b0, min(B, b0 + 128))
+        a = acc_ref[bs]
+        rej = a < w_ref[bs]
+        prow = bt.p[torch.from_numpy(bs).to(DEV), torch.from_numpy(np.where(rej, a, w_ref[bs])).to(DEV)].cpu().numpy()
+        qrow = bt.q[torch.from_numpy(bs).to(DEV), torch.from_numpy(np.minimum(a, k - 1)).to(DEV)].cpu().numpy()
+        for i, b in enumerate(bs):
+            t, mm = O.sample(prow[i], ures[b], q=qrow[i] if rej[i] else None)
+            assert tok[b] == t and mass[b] == mm, b
