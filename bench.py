@@ -271,7 +271,7 @@ def run_tetris(args):
                          "alg_bytes_per_launch": alg_bytes / args.steps,
                          "traffic": _load_traffic(args.config)},
             "clocks": clk,
-            "gpu_launches": ops.TetrisStep.launches_per_step * args.steps,
+            "gpu_launches": step.launches_per_step * args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

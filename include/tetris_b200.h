@@ -80,6 +80,9 @@ const char* tetris_last_error(void);
 int tetris_map_host(void* host_ptr, size_t bytes, void** dev_ptr);
 int tetris_abi_version(void);
 
+/* Diagnostics: when dev_buf != NULL the selector writes clock64() stamps of its phases (CTA 0) into dev_buf[0..9]. */
+int tetris_debug_timestamps(void* dev_buf);
+
 /* Stages (1)+(2): prefix products and capacity-constrained greedy selection.
  * Replaces cumulative_products (selector.py:95-110) + select_tetris (selector.py:133-176).
  * vals_are_cum = 0: vals are acceptance rates alpha (AcceptanceMatrix rows, accept_model.py:37-70) and
@@ -132,11 +135,12 @@ int tetris_verify_stochastic_f32(const float* p, const float* q, const int32_t* 
 /* The whole stochastic step in two launches (the product hot path), also callable as its two halves:
  *   tetris_select_accept_f32 — select_kernel (cluster) with its epilogue: prefix products, global top-C windows +
  *      win_offsets + stats, the accept test of every selected position, accepted[b], the row to resample from
- *      (kept in the workspace), the compaction offsets (n_b = accepted[b]+1, capped by cap[b] when cap != NULL) and
- *      the accepted-prefix tokens d[b][0..a_b);
- *   tetris_resample_f32 — persist_stream_kernel: the TMA-pipelined residual / bonus sampler over the rows chosen by
- *      the previous tetris_select_accept_f32 on the same workspace; writes out_tok[b] (and mass_out) and, when
- *      tokens != NULL, drops the sample into tokens[offsets[b] + accepted[b]] if the cap leaves room.
+ *      (kept in the workspace) and the compaction offsets (n_b = accepted[b]+1, capped by cap[b] when cap != NULL);
+ *      with dense uniforms the accept test of every drafted position runs first in a full-grid pre_accept_kernel;
+ *   tetris_resample_f32 — persist_stream_kernel (the TMA-pipelined residual / bonus sampler over the rows chosen by
+ *      the previous tetris_select_accept_f32 on the same workspace) + finalize_kernel (one warp per request: the
+ *      descent, out_tok[b], mass_out and, when tokens != NULL, the compacted stream d[b][0..a_b) ++ [out_tok[b]],
+ *      cut at offsets[b+1]).
  * Same results as tetris_select_f64 + tetris_verify_stochastic_f32 + tetris_compact (u_packed selects the
  * uniform layout as win_offsets != NULL does there).  Requires V % 8 == 0 and 16-byte aligned p, q.
  * Request sharding: the selection runs over all B_sel rows of conf/len (every shard's scores, gathered) with the
@@ -148,7 +152,7 @@ int tetris_select_accept_f32(const double* conf, const int32_t* len, int32_t B_s
                              int32_t* win_offsets, int32_t* accepted, int32_t* offsets, int32_t* tokens,
                              int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
 int tetris_resample_f32(const float* p, const float* q, const double* u_res, int32_t B, int32_t k, int32_t V,
-                        const int32_t* accepted, const int32_t* offsets, int32_t* out_tok, double* mass_out,
+                        const int32_t* d, const int32_t* accepted, const int32_t* offsets, int32_t* out_tok, double* mass_out,
                         int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
 int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
                                int32_t row0, int32_t B, const float* p, const float* q, const int32_t* d,

@@ -52,6 +52,7 @@ _sz = C.c_size_t
 _SIGNATURES = {
     "tetris_last_error": (C.c_char_p, []),
     "tetris_abi_version": (C.c_int, []),
+    "tetris_debug_timestamps": (C.c_int, [_p]),
     "tetris_map_host": (C.c_int, [_p, _sz, C.POINTER(C.c_void_p)]),
     "tetris_workspace_bytes": (_sz, [C.c_int, _i32, _i32, _i32]),
     "tetris_workspace_init": (C.c_int, [_p, _sz, _p]),
@@ -65,7 +66,7 @@ _SIGNATURES = {
     "tetris_select_accept_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
                   _sz, _p]),
-    "tetris_resample_f32": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "tetris_resample_f32": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "tetris_step_stochastic_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p,
                   _p, _p, _p, _sz, _p]),

@@ -1,5 +1,6 @@
 // Library-wide C-ABI entry points: error string, version, workspace sizing/initialisation.
 #include "abi_util.h"
+#include "launch.h"
 
 namespace tetris {
 namespace abi {
@@ -36,5 +37,10 @@ extern "C" int tetris_map_host(void* host_ptr, size_t bytes, void** dev_ptr) {
   if (e != cudaSuccess) return tetris::abi::cuda_fail(e);
   e = cudaHostGetDevicePointer(dev_ptr, host_ptr, 0);
   if (e != cudaSuccess) return tetris::abi::cuda_fail(e);
+  return TETRIS_OK;
+}
+
+extern "C" int tetris_debug_timestamps(void* dev_buf) {
+  tetris::set_debug_buffer((long long*)dev_buf);
   return TETRIS_OK;
 }

@@ -33,7 +33,7 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-enum Region { WS_KEYS, WS_COUNTERS, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_END };
+enum Region { WS_KEYS, WS_COUNTERS, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_END };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -43,7 +43,7 @@ constexpr size_t kCounterSlots = 65536;
 
 inline size_t region_offset(int op, int B, int k, int V, Region which) {
   const size_t nch = (size_t)((V + TETRIS_CHUNK_ELEMS - 1) / TETRIS_CHUNK_ELEMS);
-  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0};
+  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   sizes[WS_COUNTERS] = kCounterSlots * 4;
   if (op & TETRIS_OP_SELECT) {
     const size_t keys = (size_t)B * k * 8, heap = (size_t)B * 16;  // radix keys / heap-replay items
@@ -57,9 +57,10 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
     sizes[WS_ARG_IDX] = (size_t)B * (k + 1) * nch * 4;
     sizes[WS_SCRATCH] = align_up((size_t)B * 8) * 3 + align_up((size_t)B * 4);  // residual: rows, u, idx
     sizes[WS_ROWINFO] = (size_t)B * 16;  // accept result: row to resample from (p row, q row)
+    sizes[WS_ACCBYTES] = (size_t)B * k;  // pre-accept verdicts
   }
   const Region order[WS_END] = {WS_COUNTERS, WS_KEYS,    WS_CHUNK_SUMS, WS_WARP_SUMS,
-                                WS_ARG_VAL,  WS_ARG_IDX, WS_SCRATCH,    WS_ROWINFO};
+                                WS_ARG_VAL,  WS_ARG_IDX, WS_SCRATCH,    WS_ROWINFO, WS_ACCBYTES};
   size_t off = 0;
   for (int i = 0; i < WS_END; ++i) {
     if (order[i] == which) return off;

@@ -30,8 +30,14 @@ struct SelectArgs {
   int32_t* accepted;
   long long* rowinfo;  // [B][2]: p row, q row (-1: bonus)
   int32_t* offsets;    // [B+1]
-  int32_t* tokens;
+  uint8_t* acc_bytes;  // pre-accept verdicts [ep_rows][k] (nullptr: gather in the epilogue)
+  int accept_ctas;     // > 0: CTAs after cluster 0 compute acc_bytes concurrently with the selection
+  int* acc_counter;    // arrivals of those CTAs (zero between launches)
+  long long* dbg;      // diagnostics: per-phase clock64() stamps of CTA 0 (nullptr: off)
 };
+
+void set_debug_buffer(long long* p);
+long long* debug_buffer();
 
 struct StreamArgs {
   const float* p;
@@ -47,15 +53,19 @@ struct StreamArgs {
   int* counters;
   double* chunk_sums;
   double* warp_sums;
-  // fused compaction (accepted == nullptr: off): tokens[offsets[b] + accepted[b]] = sample, if it fits the cap
+  // fused compaction (accepted == nullptr: off): tokens[offsets[b] ..) = d[b][0..a_b) ++ [sample], cut at the cap
   const int32_t* accepted;
   const int32_t* offsets;
   int32_t* tokens;
+  const int32_t* d;
+  int k;
 };
 
 int launch_select(const SelectArgs& a, cudaStream_t st);
 int launch_persist_stream(const StreamArgs& a, cudaStream_t st);
 bool persist_eligible(const float* p, const float* q, int V);
+int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,
+                      int B, int k, int V, uint8_t* acc_bytes, cudaStream_t st);
 int launch_accept(const float* p, const float* q, const int32_t* d, const int32_t* windows, const int32_t* win_off,
                   const double* u_acc, int B, int k, int V, int32_t* accepted, long long* rowinfo, uint32_t* status,
                   cudaStream_t st);

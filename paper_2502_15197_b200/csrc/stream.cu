@@ -7,10 +7,10 @@
 //   warps 0..7  consumers: each folds one 1024-element warp run of the staged chunk into the sampling-contract
 //               sums (lane: 8 elements left to right; segment: xor butterfly; warp: 4 segments left to right) and
 //               hands the 8 warp sums to the finalizer through a shared-memory ring;
-//   warp 9      finalizer: folds the chunk sum, publishes chunk + warp sums, bumps the request's arrival counter
-//               (atom.acq_rel.gpu, result consumed one item later so its latency overlaps) and, for the last chunk of
-//               a request, runs the descent T = u*mass -> chunk -> warp -> segment -> lane -> element, re-reading only
-//               the one 1024-element warp run that holds the sample.
+//   warp 9      publisher: folds the chunk sum and stores chunk + warp sums.
+// Then finalize_kernel (one warp per request) runs the descent T = u*mass -> chunk -> warp -> segment -> lane ->
+// element, re-reading only the one 1024-element warp run that holds the sample.  (An in-kernel last-arrival descent
+// was measured 2x slower: a CTA that falls behind becomes the last arrival of every request it touches.)
 // HBM is touched once per streamed element; the descent's re-read is 4-8 KB per request.  The accept test and the
 // row choice come from the select kernel's epilogue (rowinfo), so the producer never waits on a dependent gather.
 #include "common.cuh"
@@ -19,11 +19,13 @@
 namespace tetris {
 
 constexpr int kStages = 3;
-constexpr int kConsumerWarps = kChunkWarps;  // 8
-constexpr int kProducerWarp = 8;
-constexpr int kFinalWarp = 9;
-constexpr int kPersistThreads = 10 * 32;
-constexpr int kRing = 32;
+constexpr int kConsumerWarps = 16;                         // 2 segments of the staged chunk each
+constexpr int kSegsPerChunk = kChunkElems / kSegElems;     // 32
+constexpr int kSegsPerConsumer = kSegsPerChunk / kConsumerWarps;
+constexpr int kProducerWarp = kConsumerWarps;
+constexpr int kPublisherWarp = kConsumerWarps + 1;
+constexpr int kPersistThreads = (kConsumerWarps + 2) * 32;
+constexpr int kRing = 64;
 constexpr size_t kStageRowBytes = (size_t)kChunkElems * sizeof(float);  // 32 KB
 constexpr size_t kStageBytes = 2 * kStageRowBytes;                         // p + q chunk
 constexpr size_t kPersistSmem = kStages * kStageBytes;                     // 192 KB dynamic
@@ -41,33 +43,41 @@ struct PersistShared {
   uint64_t ring_free[kRing];
   StageMeta meta[kStages];
   StageMeta ring_meta[kRing];
-  double ring_w[kRing][kChunkWarps];
+  double ring_g[kRing][kSegsPerChunk];  // segment sums of each published chunk
 };
 
-__device__ __forceinline__ void consume_warp_run(const float* __restrict__ sp, const float* __restrict__ sq, bool res,
-                                                 int64_t e0, int off0, int V, int lane, double (&G)[kWarpSegs]) {
+// Lane l's 8 elements are two 16-byte halves; lanes with bit 2 set read the upper half first, so each quarter-warp
+// phase of an LDS.128 touches 8 distinct 4-bank groups (no 2-way conflict between lanes l and l+4).
+__device__ __forceinline__ void lds8_swz(const float* p, int lane, float (&v)[8]) {
+  const int sw = (lane >> 2) & 1;
+  const float4 x = *reinterpret_cast<const float4*>(p + 4 * sw);
+  const float4 y = *reinterpret_cast<const float4*>(p + 4 * (1 - sw));
+  const float4 lo = sw ? y : x, hi = sw ? x : y;
+  v[0] = lo.x, v[1] = lo.y, v[2] = lo.z, v[3] = lo.w, v[4] = hi.x, v[5] = hi.y, v[6] = hi.z, v[7] = hi.w;
+}
+
+// Segment sum (lane fold + xor butterfly) of the staged segment at chunk offset `off0` (element e0 of the row).
+__device__ __forceinline__ double consume_segment(const float* __restrict__ sp, const float* __restrict__ sq, bool res,
+                                                  int64_t e0, int off0, int V, int lane) {
+  const int off = off0 + lane * kLaneElems;
+  double w[8];
+  if (e0 + lane * kLaneElems < V) {
+    float pv[8];
+    lds8_swz(sp + off, lane, pv);
+    if (res) {
+      float qv[8];
+      lds8_swz(sq + off, lane, qv);
 #pragma unroll
-  for (int s = 0; s < kWarpSegs; ++s) {
-    const int off = off0 + s * kSegElems + lane * kLaneElems;
-    double w[8];
-    if (e0 + s * kSegElems + lane * kLaneElems < V) {
-      float pv[8];
-      lds8(sp + off, pv);
-      if (res) {
-        float qv[8];
-        lds8(sq + off, qv);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = w_res((double)pv[i], (double)qv[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = w_plain((double)pv[i]);
-      }
+      for (int i = 0; i < 8; ++i) w[i] = w_res((double)pv[i], (double)qv[i]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = 0.0;
+      for (int i = 0; i < 8; ++i) w[i] = w_plain((double)pv[i]);
     }
-    G[s] = seg_sum(fold8(w));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = 0.0;
   }
+  return seg_sum(fold8(w));
 }
 
 // descent below the warp level, reading the warp run from global memory (all 32 lanes, T uniform)
@@ -123,43 +133,80 @@ __device__ int descend_global(const float* __restrict__ P, const float* __restri
   return (int)(e0 + s * kSegElems + g * kLaneElems + li);
 }
 
-// The last chunk of request b has been published: mass, T = u*mass, descent, outputs (finalizer warp).
+// Descent for request b after every chunk sum is published (one warp): the chunk and warp sums of all chunks are
+// fetched in one round trip (lane l holds sums l, l+32, ...), then the one warp run holding the sample is re-read.
 __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane) {
   const int nch = a.nch;
   const long long prow = a.prow[(int64_t)b * a.row_stride];
   const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
-  double S[64];
-  double mass = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    S[c] = __ldcg(&a.chunk_sums[(int64_t)b * nch + c]);
-    mass = mass + S[c];
+  const double* cs = a.chunk_sums + (int64_t)b * nch;
+  const double* ws = a.warp_sums + (int64_t)b * nch * kChunkWarps;
+  double s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
+  double s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
+  double wv[16];  // warp sums i = lane + 32*x, x < 16 (nch <= 64 -> 512 sums)
+#pragma unroll
+  for (int x = 0; x < 16; ++x) {
+    const int i = lane + 32 * x;
+    wv[x] = i < nch * kChunkWarps ? __ldcg(ws + i) : 0.0;
   }
-  uint32_t bad = 0;
+  // accepted-prefix tokens of the compacted stream, in parallel with the loads above
+  int acc = 0, off = 0, end = 0;
+  if (a.accepted) {
+    acc = a.accepted[b];
+    off = a.offsets[b];
+    end = a.offsets[b + 1];
+    for (int j = lane; j < acc && off + j < end; j += 32) a.tokens[off + j] = a.d[(int64_t)b * a.k + j];
+  }
   const double u = a.u[b];
+  uint32_t bad = 0;
   if (!(u >= 0.0 && u < 1.0)) bad |= TETRIS_ST_BAD_UNIFORM;
+  // mass = chunk sums folded left to right (every lane holds the same value)
+  double mass = 0.0;
+  for (int c = 0; c < nch; ++c) mass = mass + __shfl_sync(kFull, c < 32 ? s_lo : s_hi, c & 31);
   int tok = -1;
   if (mass > 0.0) {
     double T = u * mass;
-    const int cc = seq_find(S, nch, T);
+    // chunk level (left to right), then warp level of the chosen chunk
+    double P = 0.0;
+    int cc = -1, last_pos = -1;
+    for (int c = 0; c < nch; ++c) {
+      const double v = __shfl_sync(kFull, c < 32 ? s_lo : s_hi, c & 31);
+      if (v > 0.0) last_pos = c;
+      if (cc < 0) {
+        const double Pn = P + v;
+        if (Pn > T) {
+          T = T - P;
+          cc = c;
+        }
+        P = Pn;
+      }
+    }
+    if (cc < 0) {
+      cc = last_pos;
+      T = __longlong_as_double(0x7ff0000000000000ll);
+    }
     double Wc[kChunkWarps];
 #pragma unroll
-    for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __ldcg(&a.warp_sums[((int64_t)b * nch + cc) * kChunkWarps + w]);
+    for (int w = 0; w < kChunkWarps; ++w) {
+      const int i = cc * kChunkWarps + w;
+      double v = 0.0;
+#pragma unroll
+      for (int x = 0; x < 16; ++x) v = (x == (i >> 5)) ? wv[x] : v;
+      Wc[w] = __shfl_sync(kFull, v, i & 31);
+    }
     const int ww = seq_find(Wc, kChunkWarps, T);
-    const int64_t e0 = (int64_t)cc * kChunkElems + ww * kWarpElems;
-    const float* P = a.p + prow * (int64_t)a.V;
-    tok = res ? descend_global<true>(P, a.q + qrow * (int64_t)a.V, e0, a.V, lane, T)
-              : descend_global<false>(P, nullptr, e0, a.V, lane, T);
+    if (cc >= 0 && ww >= 0) {
+      const int64_t e0 = (int64_t)cc * kChunkElems + ww * kWarpElems;
+      const float* Pr = a.p + prow * (int64_t)a.V;
+      tok = res ? descend_global<true>(Pr, a.q + qrow * (int64_t)a.V, e0, a.V, lane, T)
+                : descend_global<false>(Pr, nullptr, e0, a.V, lane, T);
+    }
   }
   if (tok < 0) bad |= TETRIS_ST_DEGENERATE;
   if (lane == 0) {
-    a.counters[b] = 0;
     a.out_idx[b] = tok;
     if (a.mass_out) a.mass_out[b] = mass;
-    if (a.accepted) {
-      const int acc = a.accepted[b];
-      const int pos = a.offsets[b] + acc;
-      if (pos < a.offsets[b + 1]) a.tokens[pos] = tok;  // the sample is emitted unless the cap cut it
-    }
+    if (a.accepted && off + acc < end) a.tokens[off + acc] = tok;  // the sample is emitted unless the cap cut it
     set_status(a.status, bad);
   }
 }
@@ -224,39 +271,46 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
       mbar_wait(&sh.full[s], (uint32_t)((t / kStages) & 1));
       const StageMeta m = sh.meta[s];
       const float* sp = reinterpret_cast<const float*>(stage_mem + s * kStageBytes);
-      double Gs[kWarpSegs];
-      const int off0 = warp * kWarpElems;
-      consume_warp_run(sp, sp + kChunkElems, m.res != 0, (int64_t)m.c * kChunkElems + off0, off0, a.V, lane, Gs);
+      double Gs[kSegsPerConsumer];
+#pragma unroll
+      for (int x = 0; x < kSegsPerConsumer; ++x) {
+        const int seg = warp * kSegsPerConsumer + x;
+        Gs[x] = consume_segment(sp, sp + kChunkElems, m.res != 0, (int64_t)m.c * kChunkElems + seg * kSegElems,
+                                seg * kSegElems, a.V, lane);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.empty[s]);
-      double W = 0.0;
-#pragma unroll
-      for (int x = 0; x < kWarpSegs; ++x) W = W + Gs[x];
       const int slot = t % kRing;
       if (t >= kRing) mbar_wait(&sh.ring_free[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
       if (lane == 0) {
-        sh.ring_w[slot][warp] = W;
+#pragma unroll
+        for (int x = 0; x < kSegsPerConsumer; ++x) sh.ring_g[slot][warp * kSegsPerConsumer + x] = Gs[x];
         if (warp == 0) sh.ring_meta[slot] = m;
         mbar_arrive(&sh.ring_full[slot]);
       }
       __syncwarp();
     }
   } else {
-    // ---------------------------------------------------------------- finalizer
-    int prev_b = -1, prev_res = 0, prev_old = -1;
-    int t = 0;
-    for (long long i = blockIdx.x; i < total; i += G, ++t) {
-      const int slot = t % kRing;
-      mbar_wait(&sh.ring_full[slot], (uint32_t)((t / kRing) & 1));
-      const StageMeta m = sh.ring_meta[slot];
-      __syncwarp();
-      int old = 0;
-      if (lane == 0) {
+    // ---------------------------------------------------------------- publisher
+    // Folds the chunk sum and stores chunk + warp sums; the descent runs in finalize_kernel after this grid, so no
+    // streaming CTA ever waits on another (a slow CTA cannot be handed extra work).
+    const long long first = blockIdx.x;
+    const int my_items = first < total ? (int)((total - 1 - first) / G + 1) : 0;
+    for (int t0 = 0; t0 < my_items; t0 += 32) {  // lane l publishes item t0 + l
+      const int j = t0 + lane;
+      const bool mine = j < my_items;
+      const int slot = j % kRing;
+      if (mine) mbar_wait(&sh.ring_full[slot], (uint32_t)((j / kRing) & 1));
+      if (mine) {
+        const StageMeta m = sh.ring_meta[slot];
         double W[kChunkWarps];
         double S = 0.0;
 #pragma unroll
-        for (int w = 0; w < kChunkWarps; ++w) {
-          W[w] = sh.ring_w[slot][w];
+        for (int w = 0; w < kChunkWarps; ++w) {  // warp run = 4 segments left to right; chunk = 8 runs left to right
+          double x = 0.0;
+#pragma unroll
+          for (int q = 0; q < kWarpSegs; ++q) x = x + sh.ring_g[slot][w * kWarpSegs + q];
+          W[w] = x;
           S = S + W[w];
         }
         mbar_arrive(&sh.ring_free[slot]);
@@ -264,18 +318,46 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
         __stcg(&a.chunk_sums[cs], S);
 #pragma unroll
         for (int w = 0; w < kChunkWarps; ++w) __stcg(&a.warp_sums[cs * kChunkWarps + w], W[w]);
-        old = atomic_add_acq_rel_gpu(&a.counters[m.b], 1);
       }
-      // the previous item's arrival result has landed by now; finalize its request if it was the last chunk
-      const int po = __shfl_sync(kFull, prev_old, 0);
-      if (prev_b >= 0 && po == nch - 1) finalize_request(a, prev_b, prev_res != 0, lane);
-      prev_b = m.b;
-      prev_res = m.res;
-      prev_old = old;
     }
-    const int po = __shfl_sync(kFull, prev_old, 0);
-    if (prev_b >= 0 && po == nch - 1) finalize_request(a, prev_b, prev_res != 0, lane);
   }
+}
+
+// One warp per request: mass, T = u*mass, descent (after persist_stream_kernel has published every chunk).
+__global__ void __launch_bounds__(128) finalize_kernel(const StreamArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (b >= a.R) return;
+  const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+  finalize_request(a, b, qrow >= 0, lane);
+}
+
+// ---- pre-accept: verify_token on every drafted position, one thread each (runs before the selection) -----------
+// The accept test of position (b, j) does not depend on the selection, so all B*k random gathers of p[b][j][d] and
+// q[b][j][d] are issued at once by a full grid instead of serially by the selector's single cluster.  Verdict byte:
+// bit0 accept (accept_model.py:311-313), bit1 draft token outside the vocabulary, bit2 uniform outside [0, 1).
+__global__ void pre_accept_kernel(const float* __restrict__ p, const float* __restrict__ q,
+                                  const int32_t* __restrict__ d, const double* __restrict__ u_acc,
+                                  const int32_t* __restrict__ len, int B, int k, int V, uint8_t* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)B * k) return;
+  const int b = (int)(e / k), j = (int)(e - (int64_t)b * k);
+  const int L = len ? len[b] : k;
+  if (j >= L) {
+    out[e] = 0;
+    return;
+  }
+  const int t = d[e];
+  const double u = u_acc[e];
+  uint8_t v = (u >= 0.0 && u < 1.0) ? 0 : 4;
+  if (t < 0 || t >= V) {
+    v |= 2;  // rejected
+  } else {
+    const double s = (double)q[e * V + t];
+    const double m = (double)p[((int64_t)b * (k + 1) + j) * V + t];
+    v |= ((s <= m) || (u < m / s)) ? 1 : 0;
+  }
+  out[e] = v;
 }
 
 // ---- stand-alone accept test (verify_stochastic without the fused selector epilogue) ----------------------------
@@ -353,12 +435,23 @@ int launch_persist_stream(const StreamArgs& a, cudaStream_t st) {
   const long long items = (long long)a.R * a.nch;
   const int grid = (int)(items < g_num_sms ? items : g_num_sms);
   persist_stream_kernel<<<grid, kPersistThreads, kPersistSmem, st>>>(a);
+  int rc = abi::launch_check();
+  if (rc) return rc;
+  finalize_kernel<<<(a.R + 3) / 4, 128, 0, st>>>(a);
   return abi::launch_check();
 }
 
 bool persist_eligible(const float* p, const float* q, int V) {
   return (V % kLaneElems == 0) && (((uintptr_t)p & 15u) == 0) && (!q || (((uintptr_t)q & 15u) == 0)) &&
          n_chunks(V) <= 64;
+}
+
+int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,
+                      int B, int k, int V, uint8_t* acc_bytes, cudaStream_t st) {
+  const long long n = (long long)B * k;
+  if (n == 0) return TETRIS_OK;
+  pre_accept_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, q, d, u_acc, len, B, k, V, acc_bytes);
+  return abi::launch_check();
 }
 
 int launch_accept(const float* p, const float* q, const int32_t* d, const int32_t* windows, const int32_t* win_off,

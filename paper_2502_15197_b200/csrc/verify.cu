@@ -481,12 +481,19 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
   sa.accepted = accepted;
   sa.rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
   sa.offsets = offsets;
-  sa.tokens = tokens;
+  (void)tokens;  // the accepted-prefix tokens are written by tetris_resample_f32's finalize kernel
+  if (!u_packed) {
+    // dense uniforms: every position's verdict is independent of the selection, so extra CTAs of the same launch
+    // compute them (one thread per position) while cluster 0 selects
+    sa.acc_bytes = (uint8_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ACCBYTES);
+    sa.acc_counter = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + (abi::kCounterSlots - 1);
+    sa.accept_ctas = 1;
+  }
   return launch_select(sa, (cudaStream_t)stream);
 }
 
 extern "C" int tetris_resample_f32(const float* p, const float* q, const double* u_res, int32_t B, int32_t k, int32_t V,
-                                   const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
+                                   const int32_t* d, const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
                                    double* mass_out, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
                                    tetris_stream_t stream) {
   int rc = check_shape(B, k, V);
@@ -514,10 +521,12 @@ extern "C" int tetris_resample_f32(const float* p, const float* q, const double*
   a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
   a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
   if (tokens) {
-    if (!accepted || !offsets) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted and offsets");
+    if (!accepted || !offsets || !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted, offsets, d");
     a.accepted = accepted;
     a.offsets = offsets;
     a.tokens = tokens;
+    a.d = d;
+    a.k = k;
   }
   return launch_persist_stream(a, (cudaStream_t)stream);
 }
@@ -535,8 +544,8 @@ extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len
   int rc = tetris_select_accept_f32(conf, len, B_sel, k, C, row0, B, p, q, d, u_acc, u_packed, cap, V, windows,
                                     win_offsets, accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
   if (rc) return rc;
-  return tetris_resample_f32(p, q, u_res, B, k, V, accepted, offsets, out_tok, mass_out, tokens, status, ws, ws_bytes,
-                             stream);
+  return tetris_resample_f32(p, q, u_res, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status, ws,
+                             ws_bytes, stream);
 }
 
 extern "C" int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B,

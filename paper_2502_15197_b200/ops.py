@@ -388,7 +388,7 @@ class TetrisStep:
             self._check(rc)
             if events is not None:
                 events[1].record()
-            rc = lib.tetris_resample_f32(p.data_ptr(), q.data_ptr(), u_res.data_ptr(), B, k, V,
+            rc = lib.tetris_resample_f32(p.data_ptr(), q.data_ptr(), u_res.data_ptr(), B, k, V, d.data_ptr(),
                                          self.accepted.data_ptr(), self.offsets.data_ptr(), self.out_tok.data_ptr(),
                                          self.mass.data_ptr(), self.tokens.data_ptr(), self.status.data_ptr(),
                                          ws.ptr, ws.nbytes, s)

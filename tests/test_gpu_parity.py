@@ -65,6 +65,15 @@ def test_select_configs(B, k, C):
     _check_select(batch_conf ** 0.25, None, C)
 
 
+@pytest.mark.parametrize("kind", ["quantized", "ties", "random", "ragged"])
+@pytest.mark.parametrize("B,k", [(300, 20), (2000, 40), (70, 255), (12000, 17)])
+def test_select_shared_memory_path(kind, B, k):
+    """k > 16 (or more than 16384 rows) takes the shared-memory key path instead of the register path."""
+    a, ln = selection_instance(B, k, kind, seed=B * k)
+    for C in (1, B, B * k // 3, B * k - 1):
+        _check_select(a, ln, C)
+
+
 def test_select_given_cum_nonmonotone():
     """select_tetris over arbitrary Candidate.cum lists (heap merge == top-C over the prefix-min envelope)."""
     rng = np.random.default_rng(5)
