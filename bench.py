@@ -265,8 +265,8 @@ def run_tetris(args):
                          "compact": 1e3 * statistics.median(cmp_ms)},
             "select_verify_latency_us": 1e3 * statistics.median([a + b for a, b in zip(sel_ms, ver_ms)]),
             "tokens_per_step": total_tokens / args.steps,
-            "roofline": {"bound": "hbm", "kernel": "sample_kernel<float,VEC,FUSED> (tetris_verify_stochastic_f32)"
-                         if mode == "stochastic" else "greedy_kernel", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": "persist_stream_kernel + finalize_kernel (tetris_resample_f32; "
+                         "CUDA events bracket both launches)" if mode == "stochastic" else "greedy_kernel", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "alg_bytes_per_launch": alg_bytes / args.steps,
                          "traffic": _load_traffic(args.config)},

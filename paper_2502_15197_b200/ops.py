@@ -422,7 +422,9 @@ class TetrisStep:
 
     @property
     def launches_per_step(self) -> int:
-        return 2 if self.mode == "stochastic" else 3
+        # stochastic: select_kernel (+ accept CTAs), persist_stream_kernel, finalize_kernel; greedy: select_kernel,
+        # greedy_kernel, compact_kernel
+        return 3
 
 
 class _MappedTensor:
