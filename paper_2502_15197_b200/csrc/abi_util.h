@@ -39,7 +39,12 @@ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Workspace layout.  The arrival counters sit in a fixed-size region at offset 0 (one slot per possible request),
 // so a workspace reused across calls of different shapes never finds stale sums where counters must be zero.
-constexpr size_t kCounterSlots = 65536;
+constexpr size_t kRequestSlots = 65536;                 // per-request arrival counters [0, 65536)
+constexpr size_t kSlotAccCounter = kRequestSlots;        // accept-CTA arrivals of the fused select launch
+constexpr size_t kSlotGridCount = kRequestSlots + 1;     // grid barrier of the persistent sampler: arrivals
+constexpr size_t kSlotGridGen = kRequestSlots + 2;       //   ... and generation
+constexpr size_t kCounterSlots = kRequestSlots + 64;
+static_assert(kSlotGridGen == kSlotGridCount + 1, "grid_barrier reads the generation at bar + 1");
 
 inline size_t region_offset(int op, int B, int k, int V, Region which) {
   const size_t nch = (size_t)((V + TETRIS_CHUNK_ELEMS - 1) / TETRIS_CHUNK_ELEMS);

@@ -59,9 +59,13 @@ struct StreamArgs {
   int32_t* tokens;
   const int32_t* d;
   int k;
+  unsigned* grid_bar;  // [2] arrivals, generation (zero-initialised workspace): the descent runs in-kernel after a
+                       // grid barrier (cooperative launch); nullptr -> a separate finalize_kernel launch
 };
 
 int launch_select(const SelectArgs& a, cudaStream_t st);
+bool select1_eligible(int B, int k);
+int launch_select1(const SelectArgs& a, cudaStream_t st);  // single-CTA selector (select1.cu)
 int launch_persist_stream(const StreamArgs& a, cudaStream_t st);
 bool persist_eligible(const float* p, const float* q, int V);
 int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,

@@ -211,6 +211,26 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane)
   }
 }
 
+// Sense-free generation barrier over the whole (co-resident, cooperative) grid; called by one thread per CTA after a
+// __syncthreads.  bar[0] counts arrivals and is reset by the last arrival, which then bumps the generation bar[1].
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n) {
+  unsigned g0;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(bar + 1) : "memory");
+  __threadfence();
+  const int old = atomic_add_acq_rel_gpu(reinterpret_cast<int*>(bar), 1);
+  if ((unsigned)old == n - 1) {
+    bar[0] = 0u;
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(g0 + 1u) : "memory");
+  } else {
+    unsigned g;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      if (g != g0) break;
+      __nanosleep(32);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(const StreamArgs a) {
   extern __shared__ __align__(128) uint8_t stage_mem[];
   __shared__ PersistShared sh;
@@ -319,6 +339,18 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
 #pragma unroll
         for (int w = 0; w < kChunkWarps; ++w) __stcg(&a.warp_sums[cs * kChunkWarps + w], W[w]);
       }
+    }
+  }
+  if (a.grid_bar != nullptr) {
+    // every chunk of every request is published once all CTAs pass the barrier; then one warp per request runs
+    // the descent (requests strided over the CTAs so the re-reads spread over all SMs)
+    __syncthreads();
+    if (tid == 0) grid_barrier(a.grid_bar, (unsigned)G);
+    __syncthreads();
+    constexpr int kWarps = kPersistThreads / 32;
+    for (int b = warp * G + blockIdx.x; b < a.R; b += G * kWarps) {
+      const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+      finalize_request(a, b, qrow >= 0, lane);
     }
   }
 }
@@ -434,6 +466,22 @@ int launch_persist_stream(const StreamArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return abi::cuda_fail(e);
   const long long items = (long long)a.R * a.nch;
   const int grid = (int)(items < g_num_sms ? items : g_num_sms);
+  if (a.grid_bar != nullptr) {
+    // one launch: streaming + grid barrier + descent; cooperative so the barrier's CTAs are co-resident
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kPersistThreads, 1, 1);
+    cfg.dynamicSmemBytes = kPersistSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, persist_stream_kernel, a);
+    if (e != cudaSuccess) return abi::cuda_fail(e);
+    return abi::launch_check();
+  }
   persist_stream_kernel<<<grid, kPersistThreads, kPersistSmem, st>>>(a);
   int rc = abi::launch_check();
   if (rc) return rc;

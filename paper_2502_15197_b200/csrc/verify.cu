@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Stage (3): batched verification + residual / bonus resampling, and the row sampler it is built on (sm_100a).
 //
 // The HBM-bound part of the path.  For every request exactly one vocabulary row (bonus: p[b][w]) or row pair
@@ -428,6 +429,7 @@ extern "C" int tetris_verify_stochastic_f32(const float* p, const float* q, cons
     a.counters = cnt;
     a.chunk_sums = cs;
     a.warp_sums = wsum;
+    a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
     return launch_persist_stream(a, st);
   }
   const bool vec = (V % 8 == 0) && aligned32(p) && aligned32(q);
@@ -486,8 +488,15 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
     // dense uniforms: every position's verdict is independent of the selection, so extra CTAs of the same launch
     // compute them (one thread per position) while cluster 0 selects
     sa.acc_bytes = (uint8_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ACCBYTES);
-    sa.acc_counter = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + (abi::kCounterSlots - 1);
+    sa.acc_counter = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + abi::kSlotAccCounter;
     sa.accept_ctas = 1;
+    static const bool sep = getenv("TETRIS_EXP_SEPARATE_ACCEPT") != nullptr;  // experiment switch
+    if (sep) {
+      sa.accept_ctas = 0;
+      int rc2 = launch_pre_accept(p, q, d, u_acc, len ? len + row0 : nullptr, B, k, V, sa.acc_bytes,
+                                  (cudaStream_t)stream);
+      if (rc2) return rc2;
+    }
   }
   return launch_select(sa, (cudaStream_t)stream);
 }
@@ -520,6 +529,7 @@ extern "C" int tetris_resample_f32(const float* p, const float* q, const double*
   a.counters = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
   a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
+  a.grid_bar = (unsigned*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + abi::kSlotGridCount;
   if (tokens) {
     if (!accepted || !offsets || !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted, offsets, d");
     a.accepted = accepted;
@@ -598,6 +608,7 @@ extern "C" int tetris_sample_rows_f32(const float* p, const float* q, const int6
     a.counters = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_COUNTERS);
     a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_CHUNK_SUMS);
     a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_WARP_SUMS);
+    a.grid_bar = (unsigned*)a.counters + abi::kSlotGridCount;
     return launch_persist_stream(a, (cudaStream_t)stream);
   }
   return sample_rows_impl<float>(p, q, p_row, q_row, u, R, V, out_idx, mass_out, status, ws, ws_bytes,

@@ -422,9 +422,9 @@ class TetrisStep:
 
     @property
     def launches_per_step(self) -> int:
-        # stochastic: select_kernel (+ accept CTAs), persist_stream_kernel, finalize_kernel; greedy: select_kernel,
-        # greedy_kernel, compact_kernel
-        return 3
+        # stochastic: select_kernel (+ accept CTAs), persist_stream_kernel (streaming + grid barrier + descent);
+        # greedy: select_kernel, greedy_kernel, compact_kernel
+        return 2 if self.mode == "stochastic" else 3
 
 
 class _MappedTensor:
