@@ -29,6 +29,8 @@ CONFIGS = {
     "cfg1": dict(B=16, k=5, C=48, V=32000, mode="greedy"),
     "cfg2": dict(B=256, k=8, C=1024, V=32000, mode="stochastic"),
     "cfg3": dict(B=1024, k=16, C=8192, V=128256, mode="stochastic"),
+    # cfg4: selection-only capacity sweep (BASELINE.json configs[3]); timed by run_select_sweep
+    "cfg4": dict(B=4096, k=16, C=None, V=32000, mode="select", sweep=(4096, 8192, 16384, 32768, 65536)),
     # cfg5: B=16384 requests sharded over the GPUs (strong scaling), C assumed B*8
     "cfg5": dict(B=16384, k=16, C=131072, V=128256, mode="stochastic", strong=True),
 }
@@ -183,7 +185,9 @@ def run_tetris(args):
         C = cfg["C"] * world
     k, V, mode = cfg["k"], cfg["V"], cfg["mode"]
     dev = torch.device("cuda", local)
-    nsets = args.sets
+    # rotate enough input sets that consecutive steps never find their inputs in L2 (126 MB on B200)
+    set_bytes = B_local * ((k + 1) + k) * V * 4
+    nsets = max(args.sets, -(-2 * 126 * 2**20 // set_bytes))
     sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
             for s in range(nsets)]
     step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None)
@@ -287,8 +291,8 @@ def run_tetris(args):
             "data": "synthetic (seeded spiked-softmax draft/target distributions, paper_2502_15197_b200/synthetic.py)",
             "config": {"workload": f"{args.config}: B={B_local * world} k={k} C={C} V={V} {mode}",
                        "B_per_gpu": B_local, "k": k, "C": C, "V": V, "verify": mode, "input_sets": nsets,
-                       "l2": "inputs larger than L2 (%.1f GB per set), %d sets rotated" % (
-                           (B_local * ((k + 1) + k) * V * 4) / 1e9, nsets),
+                       "l2": "rotated input sets larger than L2 together (%.3f GB per set, %d sets)" % (
+                           set_bytes / 1e9, nsets),
                        "parallelism": f"request-sharded dp{world}" + (" + NCCL all-gather select" if world > 1 else ""),
                        "launch": "CUDA graph replay" if use_graph else "eager"},
             "stage_us": {"select": 1e3 * statistics.median(sel_ms), "verify": 1e3 * statistics.median(ver_ms),
@@ -476,6 +480,90 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_select_sweep(args):
+    """cfg4: selection-only top-C (prefix products + global top-C + windows/offsets/stats) at B=4096, k=16 for each
+    capacity of the sweep; CUDA-graph replays over rotated conf sets (together larger than L2).  With --impl
+    reference (or on rank 0 beside the GPU numbers) the reference's cumulative_products + select_tetris (heapq) is
+    timed on the host for the same inputs."""
+    import numpy as np
+    import torch
+
+    from paper_2502_15197_b200 import ops
+
+    cfg = CONFIGS["cfg4"]
+    B, k = cfg["B"], cfg["k"]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    g = torch.Generator().manual_seed(args.seed)
+    nsets = 300  # 300 x 512 KB = 154 MB of conf > L2
+    host_sets = [torch.rand(B, k, dtype=torch.float64, generator=g) ** 0.25 for _ in range(min(nsets, 4))]
+    sweep = {}
+    cpu = {}
+    if args.impl != "reference":
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        sets = [host_sets[i % len(host_sets)].to(dev) * (1.0 - 1e-9 * i) for i in range(nsets)]
+        for C in cfg["sweep"]:
+            res = ops.select(sets[0], C)
+            torch.cuda.synchronize()
+            graphs = []
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                for i in range(nsets):
+                    ops.select(sets[i], C, out=res)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for i in range(nsets):
+                    ops.select(sets[i], C, out=res)
+            for _ in range(args.warmup):
+                gr.replay()
+            torch.cuda.synchronize()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, args.steps // 20)
+            t0.record()
+            for _ in range(reps):
+                gr.replay()
+            t1.record()
+            torch.cuda.synchronize()
+            us = t0.elapsed_time(t1) * 1e3 / (reps * nsets)
+            ops.raise_for_status(res.status)
+            sweep[str(C)] = {"us_per_select": us, "selections_per_s": 1e6 / us, "cells_per_s": B * k * 1e6 / us}
+    if not args.no_cpu_baseline or args.impl == "reference":
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import reference_port as RP
+
+        rows = [list(map(float, r)) for r in host_sets[0].numpy()]
+        for C in cfg["sweep"]:
+            t = time.perf_counter()
+            RP.select_tetris(RP.cumulative_products(rows), C)
+            cpu[str(C)] = (time.perf_counter() - t) * 1e6
+    main_C = "8192"
+    if args.impl == "reference":
+        v = cpu[main_C]
+        line = {"metric": "selection-only top-C latency", "value": v, "unit": "us", "n_gpus": args.gpus,
+                "steps": 1, "warmup": 0, "higher_is_better": False, "impl": "reference", "vs_baseline": None,
+                "config": {"workload": f"cfg4: B={B} k={k} C=sweep, selection only", "sweep_us": cpu},
+                "cpu_baseline": {"value": v, "unit": "us", "cores": 1, "kind": "port",
+                                 "sample": "cumulative_products + heapq select_tetris over the full batch, 1 thread"},
+                "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    else:
+        v = sweep[main_C]["us_per_select"]
+        line = {"metric": "selection-only top-C latency", "value": v, "unit": "us", "n_gpus": 1,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": False, "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic conf = U(0,1)^0.25",
+                "config": {"workload": f"cfg4: B={B} k={k} C=8192 (sweep in 'sweep')", "B": B, "k": k,
+                           "l2": f"{nsets} rotated conf sets ({nsets * B * k * 8 / 1e6:.0f} MB > L2)",
+                           "launch": "CUDA graph replay"},
+                "sweep": sweep,
+                "cpu_baseline": {"sweep_us": cpu, "unit": "us", "cores": 1, "kind": "port"} if cpu else None,
+                "gpu_launches": nsets * reps * len(cfg["sweep"])}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -491,7 +579,9 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="time eager launches instead of CUDA graphs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)  # timing rule: at least 3 untimed warm-up steps
-    if args.impl == "reference":
+    if args.config == "cfg4":
+        run_select_sweep(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_tetris(args)
