@@ -338,3 +338,48 @@ def test_fused_step_full_cfg3_bit_exact():
         for i, b in enumerate(bs):
             t, mm = O.sample(prow[i], ures[b], q=qrow[i] if rej[i] else None)
             assert tok[b] == t and mass[b] == mm, b
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# the request-sharded step of rank r in a world of W (what TetrisStep(group=...) launches after the all-gather),
+# simulated on one GPU: the selection runs over the gathered W*B rows with the global capacity, the verification
+# tensors cover only this rank's rows
+@pytest.mark.parametrize("W,B,k,V,C,rank", [(2, 512, 16, 8192, 8192, 1), (4, 1024, 16, 4096, 32768, 3),
+                                             (8, 1024, 16, 2048, 65536, 5), (2, 300, 7, 4096, 2000, 0)])
+def test_sharded_step_matches_global_selection(W, B, k, V, C, rank):
+    shards = [make_batch(B, k, V, seed=100 + r) for r in range(W)]
+    conf_all = torch.cat([s.conf for s in shards]).contiguous()
+    len_all = torch.cat([s.lengths for s in shards]).contiguous()
+    bt = shards[rank]
+    Bg = W * B
+    lib = N.load()
+    dev = bt.p.device
+    windows = torch.zeros(Bg, dtype=torch.int32, device=dev)
+    woff = torch.zeros(Bg + 1, dtype=torch.int32, device=dev)
+    acc = torch.zeros(B, dtype=torch.int32, device=dev)
+    tok = torch.zeros(B, dtype=torch.int32, device=dev)
+    mass = torch.zeros(B, dtype=torch.float64, device=dev)
+    offs = torch.zeros(B + 1, dtype=torch.int32, device=dev)
+    toks = torch.zeros(B * (k + 1), dtype=torch.int32, device=dev)
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    status = ops.new_status(dev)
+    ws = ops.Workspace(dev, N.OP_ALL, Bg, k, V)
+    rc = lib.tetris_step_stochastic_f32(
+        conf_all.data_ptr(), len_all.data_ptr(), Bg, k, C, rank * B, B, bt.p.data_ptr(), bt.q.data_ptr(),
+        bt.d.data_ptr(), bt.u_acc.data_ptr(), 0, bt.u_res.data_ptr(), None, V, windows.data_ptr(), woff.data_ptr(),
+        acc.data_ptr(), tok.data_ptr(), mass.data_ptr(), offs.data_ptr(), toks.data_ptr(), stats.data_ptr(),
+        status.data_ptr(), ws.ptr, ws.nbytes, torch.cuda.current_stream().cuda_stream)
+    assert rc == N.OK, lib.tetris_last_error()
+    torch.cuda.synchronize()
+    ops.raise_for_status(status)
+    w_ref, _, st_ref = O.select(_np(conf_all), C, _np(len_all))
+    assert np.array_equal(_np(windows), w_ref)
+    assert list(_np(stats)[:3]) == list(st_ref[:3])
+    wl = w_ref[rank * B:(rank + 1) * B]
+    acc_ref, tok_ref, mass_ref = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), wl, _np(bt.u_acc),
+                                                     _np(bt.u_res), None, nthreads=8)
+    assert np.array_equal(_np(acc), acc_ref)
+    assert np.array_equal(_np(tok), tok_ref)
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
+    assert np.array_equal(_np(offs), off_ref)
+    assert np.array_equal(_np(toks)[: off_ref[-1]], toks_ref)
