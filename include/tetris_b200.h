@@ -43,6 +43,7 @@ typedef struct CUstream_st* tetris_stream_t; /* == cudaStream_t */
 #define TETRIS_ST_BAD_TOKEN 4u     /* draft token outside [0,V)                     (accept_model.py:305-306)     */
 #define TETRIS_ST_BAD_UNIFORM 8u   /* uniform outside [0,1)                         (accept_model.py:307-308)     */
 #define TETRIS_ST_BAD_WINDOW 16u   /* window deeper than the row                    (sim_engine.py:389-392)       */
+#define TETRIS_ST_STREAM_EXHAUSTED 32u /* tetris_sim_step: uniform or target-length stream too short               */
 
 /* ---- the sampling contract ---------------------------------------------------------------------------------
  * Inverse-CDF sampling of a weight row w[0..V) with a uniform u (accept_model.py:364,368 use numpy's
@@ -187,6 +188,24 @@ int tetris_residual_f64(const double* p_draft, const double* p_target, int32_t R
  * offsets[B+1] = exclusive scan of n_b; tokens[offsets[b] + i] = (d[b][0..accepted[b]) ++ [out_tok[b]])[i]. */
 int tetris_compact(const int32_t* accepted, const int32_t* out_tok, const int32_t* d, const int32_t* cap,
                    int32_t B, int32_t k, int32_t* offsets, int32_t* tokens, tetris_stream_t stream);
+
+/* GPU-resident simulator step (everything run_step, sim_engine.py:454-495, does after the draft phase) for B <= 1024
+ * active requests in the reference's row order.  truth[B][K] (K = k + extra) holds the step's truth acceptance rows,
+ * truth_len[B] their depths, which must equal min(K, target - served) (sim_engine.py:343).  policy: 0 = tetris
+ * (windows[] given, e.g. by tetris_select_f64 on the surrogate), 1 = sd (min(k_base, depth), :358-360), 2 = dsd
+ * (select_dsd's common window from *alpha_hat, selector.py:193-222, clamped to each depth, :361-368).  Verification
+ * consumes uniforms[counters[0] ..) in row order (apply_verification, :374-404); accepted[], credited[] = min(acc + 1,
+ * remaining) (:467-471), *expected = expected_accepted (selector.py:286-306), *alpha_hat updated (:473-478); then
+ * refill_batch (:428-451) rewrites ids/target/served/arrival in place (survivors in order, then one replacement per
+ * completion with the next length_stream[counters[1] ..] entry and arrival = step + 1), listing the completed requests
+ * in done_ids/done_arrival, and next_depths[] = the next step's draft depths.  counters[7] (device):
+ * {uniform offset, length offset, next id, step, completions, sent, accepted}. */
+int tetris_sim_step(const double* truth, const int32_t* truth_len, int32_t B, int32_t K, int32_t policy,
+                    int32_t k_base, int64_t capacity, double dsd_decay, const double* uniforms, int64_t n_uniforms,
+                    const int32_t* length_stream, int64_t n_lengths, int32_t* windows, int64_t* ids, int32_t* target,
+                    int32_t* served, int32_t* arrival, double* alpha_hat, int64_t* counters, int32_t* accepted,
+                    int32_t* credited, double* expected, int64_t* done_ids, int32_t* done_arrival,
+                    int32_t* next_depths, uint32_t* status, tetris_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ ST_DEGENERATE = 2
 ST_BAD_TOKEN = 4
 ST_BAD_UNIFORM = 8
 ST_BAD_WINDOW = 16
+ST_STREAM_EXHAUSTED = 32
 
 OP_SELECT = 1
 OP_VERIFY = 2
@@ -75,6 +76,9 @@ _SIGNATURES = {
     "tetris_sample_rows_f32": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_residual_f64": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_compact": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _p, _p, _p]),
+    "tetris_sim_step": (
+        C.c_int, [_p, _p, _i32, _i32, _i32, _i32, _i64, C.c_double, _p, _i64, _p, _i64, _p, _p, _p, _p, _p, _p, _p,
+                  _p, _p, _p, _p, _p, _p, _p, _p]),
 }
 EXPORTS = tuple(_SIGNATURES)
 

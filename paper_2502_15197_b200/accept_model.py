@@ -96,7 +96,7 @@ def _check_pair(p_draft: TokenDistribution, p_target: TokenDistribution) -> None
 
 def _rows(*dists: TokenDistribution):
     dev = _device()
-    return [torch.from_numpy(np.ascontiguousarray(d.probs)).view(1, -1).to(dev) for d in dists]
+    return [torch.from_numpy(np.array(d.probs)).view(1, -1).to(dev) for d in dists]
 
 
 def verify_token(p_draft: TokenDistribution, p_target: TokenDistribution, token: int, u: float) -> bool:

@@ -97,6 +97,8 @@ def raise_for_status(status: torch.Tensor, context: str = "") -> None:
         raise ValueError(f"selection window deeper than the drafted row{where}")
     if s & N.ST_BAD_VALUE:
         raise ValueError(f"acceptance value outside [0, 1] or NaN{where}")
+    if s & N.ST_STREAM_EXHAUSTED:
+        raise ValueError(f"uniform or target-length stream exhausted{where}")
     if s & N.ST_DEGENERATE:
         raise DegenerateResidualError(f"target never rejects the draft; there is no residual to sample{where}")
     raise RuntimeError(f"unknown status bits {s:#x}{where}")

@@ -3,16 +3,18 @@ count (:407-409) and the per-request credit `min(acc + 1, remaining)` (:467-471)
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import Sequence
 
 import numpy as np
 import torch
 
+from . import _native as N
 from . import ops
 from .accept_model import AcceptanceMatrix, _device
 from .selector import Selection
 
-__all__ = ["apply_verification", "bonus_tokens", "credit"]
+__all__ = ["apply_verification", "bonus_tokens", "credit", "GpuSimulator", "GpuStepOutcome"]
 
 
 def apply_verification(selection: Selection, truth: AcceptanceMatrix, rng: np.random.Generator) -> tuple:
@@ -50,3 +52,132 @@ def credit(accepted: Sequence[int], remaining: Sequence[int]) -> tuple:
     tok = torch.zeros(B, dtype=torch.int32, device=dev)
     offsets, _ = ops.compact(acc, tok, d, cap)
     return tuple(int(x) for x in torch.diff(offsets).cpu().numpy())
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# GPU-resident simulator step
+# ---------------------------------------------------------------------------------------------------------------
+POLICY_CODES = {"tetris": 0, "sd": 1, "dsd": 2}
+
+
+@dataclass(frozen=True)
+class GpuStepOutcome:
+    """The observable fields of StepOutcome (sim_engine.py:278-295) produced on the device for one step."""
+
+    step: int
+    windows: tuple
+    accepted: tuple
+    credited: tuple
+    bonus: int
+    expected_accepted: float
+    stats: object  # PolicyStats (tetris, comparisons = -1) or None
+    completions: tuple  # ((request id, arrival step), ...) in active-list order
+    alpha_hat: float
+
+
+class GpuSimulator:
+    """run_step (sim_engine.py:454-495) with the batch state resident on the GPU.
+
+    The draft phase stays with the caller (the draft model / acceptance source produces the truth and surrogate rows
+    for the depths `depths()` reports, sim_engine.py:338-346); everything after it — policy windows, the cascade over
+    the verify uniform stream, expected_accepted, credit, the DSD estimate and refill_batch — runs in
+    tetris_select_f64 (tetris) + tetris_sim_step.  `uniforms` is the verify generator's stream (the reference draws
+    rng.random(w_i) per row in order, i.e. one flat stream, sim_engine.py:393-396) and `lengths` the target-length
+    stream: the first batch_size entries are the initial batch (init_state, :311-330), the rest feed refill_batch in
+    completion order."""
+
+    def __init__(self, batch_size: int, k: int, capacity: int, *, extra: int = 0, policy: str = "tetris",
+                 dsd_decay: float = 0.9, dsd_initial_estimate: float = 0.5, uniforms=None, lengths=None, device=None):
+        if policy not in POLICY_CODES:
+            raise ValueError(f"policy must be one of {tuple(POLICY_CODES)}, got {policy!r}")
+        if batch_size < 1 or batch_size > 1024:
+            raise ValueError(f"batch_size must lie in [1, 1024], got {batch_size}")
+        dev = _device() if device is None else torch.device(device)
+        self.B, self.k, self.K, self.C, self.policy = batch_size, k, k + extra, int(capacity), policy
+        self.dsd_decay = float(dsd_decay)
+        lengths = np.ascontiguousarray(lengths, dtype=np.int32)
+        if lengths.shape[0] < batch_size:
+            raise ValueError("the length stream must cover the initial batch")
+        self.uniforms = torch.from_numpy(np.array(uniforms, dtype=np.float64)).to(dev)
+        self.lengths = torch.from_numpy(lengths[batch_size:].copy() if lengths.shape[0] > batch_size
+                                        else np.ones(1, np.int32)).to(dev)
+        self.n_lengths = max(0, lengths.shape[0] - batch_size)
+        B = batch_size
+        self.ids = torch.arange(B, dtype=torch.int64, device=dev)
+        self.target = torch.from_numpy(lengths[:B].copy()).to(dev)
+        self.served = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.arrival = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.alpha_hat = torch.tensor([dsd_initial_estimate], dtype=torch.float64, device=dev)
+        self.counters = torch.tensor([0, 0, B, 0, 0, 0, 0], dtype=torch.int64, device=dev)
+        self.windows = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.accepted = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.credited = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.expected = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.done_ids = torch.zeros(B, dtype=torch.int64, device=dev)
+        self.done_arrival = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.depths_dev = torch.clamp(self.target, max=self.K).to(torch.int32)
+        self.status = ops.new_status(dev)
+        self.device = dev
+
+    def depths(self) -> tuple:
+        """Draft depths of the next step, min(k + extra, remaining) per active request (sim_engine.py:343)."""
+        return tuple(int(x) for x in self.depths_dev.cpu().numpy())
+
+    def step(self, truth, surrogate=None) -> GpuStepOutcome:
+        """One simulator step given the draft phase's truth (and surrogate) rows, ragged lists or [B, K] arrays whose
+        row lengths are the current depths."""
+        B, K, dev = self.B, self.K, self.device
+        depths = self.depths()
+        tr = self._pack(truth, depths)
+        lens = torch.tensor(depths, dtype=torch.int32, device=dev)
+        stats = None
+        if self.policy == "tetris":
+            sg = self._pack(truth if surrogate is None else surrogate, depths)
+            res = ops.select(sg, self.C, lens, want_cum=True)
+            self.windows.copy_(res.windows)
+            stats_t = ops.heap_stats(res.cum, self.C, lens)  # exact PolicyStats incl. heapq comparisons
+        N.call("tetris_sim_step", tr.data_ptr(), lens.data_ptr(), B, K, POLICY_CODES[self.policy], self.k, self.C,
+               self.dsd_decay, self.uniforms.data_ptr(), self.uniforms.numel(), self.lengths.data_ptr(),
+               self.n_lengths, self.windows.data_ptr(), self.ids.data_ptr(), self.target.data_ptr(),
+               self.served.data_ptr(), self.arrival.data_ptr(), self.alpha_hat.data_ptr(), self.counters.data_ptr(),
+               self.accepted.data_ptr(), self.credited.data_ptr(), self.expected.data_ptr(), self.done_ids.data_ptr(),
+               self.done_arrival.data_ptr(), self.depths_dev.data_ptr(), self.status.data_ptr(),
+               torch.cuda.current_stream(dev).cuda_stream)
+        ops.raise_for_status(self.status, "sim step")
+        cnt = self.counters.cpu().numpy()
+        n_done = int(cnt[4])
+        if self.policy == "tetris":
+            from .selector import PolicyStats
+
+            st = stats_t.cpu().numpy()
+            stats = PolicyStats(int(st[0]), int(st[1]), int(st[2]), int(st[3]))
+        comps = tuple(zip((int(x) for x in self.done_ids[:n_done].cpu().numpy()),
+                          (int(x) for x in self.done_arrival[:n_done].cpu().numpy())))
+        return GpuStepOutcome(
+            step=int(cnt[3]) - 1,
+            windows=tuple(int(x) for x in self.windows.cpu().numpy()),
+            accepted=tuple(int(x) for x in self.accepted.cpu().numpy()),
+            credited=tuple(int(x) for x in self.credited.cpu().numpy()),
+            bonus=B,
+            expected_accepted=float(self.expected.item()),
+            stats=stats,
+            completions=comps,
+            alpha_hat=float(self.alpha_hat.item()),
+        )
+
+    def _pack(self, rows, depths) -> torch.Tensor:
+        B, K = self.B, self.K
+        if isinstance(rows, torch.Tensor):
+            return rows.to(self.device, torch.float64).contiguous()
+        if isinstance(rows, np.ndarray) and rows.ndim == 2:
+            return torch.from_numpy(np.ascontiguousarray(rows, np.float64)).to(self.device)
+        if hasattr(rows, "rows"):  # an AcceptanceMatrix
+            rows = rows.rows
+        out = np.zeros((B, K), np.float64)
+        if len(rows) != B:
+            raise ValueError(f"expected {B} rows, got {len(rows)}")
+        for i, (r, d) in enumerate(zip(rows, depths)):
+            if len(r) != d:
+                raise ValueError(f"row {i} has {len(r)} entries, the draft depth is {d}")
+            out[i, :d] = r
+        return torch.from_numpy(out).to(self.device)

@@ -1,0 +1,41 @@
+"""GPU: the device-resident simulator step (GpuSimulator: tetris_select_f64 + tetris_sim_step) replays the
+reference's run_step traces (tests/golden/sim.json) exactly — windows, accepted, credited, expected_accepted bits,
+PolicyStats, completions, DSD estimate — given the recorded draft-phase rows and the reference's random streams."""
+import pytest
+
+from _sim_golden import runs
+from paper_2502_15197_b200.sim_engine import GpuSimulator
+
+pytestmark = pytest.mark.gpu
+RUNS = runs()
+
+
+@pytest.mark.parametrize("run", RUNS, ids=[r["tag"] for r in RUNS])
+def test_gpu_sim_matches_reference_trace(run):
+    sim = GpuSimulator(run["batch_size"], run["k"], run["capacity"], extra=run["extra"], policy=run["policy"],
+                       dsd_decay=run["dsd_decay"], dsd_initial_estimate=run["dsd_initial_estimate"],
+                       uniforms=run["uniforms"], lengths=run["lengths"], device="cuda")
+    for i, s in enumerate(run["steps"]):
+        assert list(sim.depths()) == s["depths"], i
+        out = sim.step(s["truth_rows"], s["surrogate_rows"])
+        assert out.step == i
+        assert list(out.windows) == s["windows"], i
+        assert list(out.accepted) == s["accepted"], i
+        assert list(out.credited) == s["credited"], i
+        assert out.bonus == s["bonus"]
+        assert out.expected_accepted == s["expected"], i
+        assert [list(c) for c in out.completions] == s["completions"], i
+        assert out.alpha_hat == s["alpha"], i
+        if s["stats"] is not None:
+            st = out.stats
+            assert [st.extracts, st.inserts, st.peak_queue, st.comparisons] == s["stats"], i
+
+
+def test_gpu_sim_rejects_wrong_depths():
+    run = RUNS[0]
+    sim = GpuSimulator(run["batch_size"], run["k"], run["capacity"], extra=run["extra"], policy="sd",
+                       uniforms=run["uniforms"], lengths=run["lengths"], device="cuda")
+    s = run["steps"][0]
+    bad = [r[:-1] if len(r) > 1 else r for r in s["truth_rows"]]
+    with pytest.raises(ValueError):
+        sim.step(bad, bad)
