@@ -190,7 +190,8 @@ def run_tetris(args):
     nsets = max(args.sets, -(-2 * 126 * 2**20 // set_bytes))
     sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
             for s in range(nsets)]
-    step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None)
+    step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None,
+                          policy=args.policy)
 
     def run(i, events=None):
         bt = sets[i % nsets]
@@ -294,7 +295,7 @@ def run_tetris(args):
                        "l2": "rotated input sets larger than L2 together (%.3f GB per set, %d sets)" % (
                            set_bytes / 1e9, nsets),
                        "parallelism": f"request-sharded dp{world}" + (" + NCCL all-gather select" if world > 1 else ""),
-                       "launch": "CUDA graph replay" if use_graph else "eager"},
+                       "launch": "CUDA graph replay" if use_graph else "eager", "policy": args.policy},
             "stage_us": {"select": 1e3 * statistics.median(sel_ms), "verify": 1e3 * statistics.median(ver_ms),
                          "compact": 1e3 * statistics.median(cmp_ms)},
             "select_verify_latency_us": 1e3 * statistics.median([a + b for a, b in zip(sel_ms, ver_ms)]),
@@ -577,6 +578,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="time eager launches instead of CUDA graphs")
+    ap.add_argument("--policy", default="tetris", choices=["tetris", "fixed"],
+                    help="fixed: the fixed-window baseline (window C/B per request) through the same kernels")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)  # timing rule: at least 3 untimed warm-up steps
     if args.config == "cfg4":

@@ -189,6 +189,12 @@ int tetris_residual_f64(const double* p_draft, const double* p_target, int32_t R
 int tetris_compact(const int32_t* accepted, const int32_t* out_tok, const int32_t* d, const int32_t* cap,
                    int32_t B, int32_t k, int32_t* offsets, int32_t* tokens, tetris_stream_t stream);
 
+/* Baseline policies (select_fixed_window, selector.py:179-190; the simulator's sd / dsd windows, sim_engine.py:358-368):
+ * windows[b] = min(window, len[b]) (len NULL: k) and, when win_offsets != NULL, their exclusive scan [B+1].  The DSD
+ * common window is select_dsd's scalar argmax (selector.py:193-222), computed by the caller. */
+int tetris_uniform_windows(const int32_t* len, int32_t B, int32_t k, int32_t window, int32_t* windows,
+                           int32_t* win_offsets, tetris_stream_t stream);
+
 /* GPU-resident simulator step (everything run_step, sim_engine.py:454-495, does after the draft phase) for B <= 1024
  * active requests in the reference's row order.  truth[B][K] (K = k + extra) holds the step's truth acceptance rows,
  * truth_len[B] their depths, which must equal min(K, target - served) (sim_engine.py:343).  policy: 0 = tetris

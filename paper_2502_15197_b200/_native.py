@@ -76,6 +76,7 @@ _SIGNATURES = {
     "tetris_sample_rows_f32": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_residual_f64": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_compact": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _p, _p, _p]),
+    "tetris_uniform_windows": (C.c_int, [_p, _i32, _i32, _i32, _p, _p, _p]),
     "tetris_sim_step": (
         C.c_int, [_p, _p, _i32, _i32, _i32, _i32, _i64, C.c_double, _p, _i64, _p, _i64, _p, _p, _p, _p, _p, _p, _p,
                   _p, _p, _p, _p, _p, _p, _p, _p]),

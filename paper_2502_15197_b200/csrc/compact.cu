@@ -37,6 +37,35 @@ __global__ void __launch_bounds__(1024, 1)
   if (tid == 0) offsets[B] = (int32_t)total;
 }
 
+// Baseline policies on the tensor API: one common window for every request, clamped to what the
+// request drafted — select_fixed_window (selector.py:179-190) / the simulator's sd policy min(k, depth)
+// (sim_engine.py:358-360) and select_dsd's common window clamped the same way (:361-368).  Writes windows and their
+// exclusive scan (the uniform / token offsets of the verification).  Same one-CTA layout as compact_kernel.
+__global__ void __launch_bounds__(1024, 1)
+    uniform_windows_kernel(const int32_t* __restrict__ len, int B, int k, int window, int32_t* __restrict__ windows,
+                           int32_t* __restrict__ win_offsets) {
+  __shared__ long long s_tmp[33];
+  const int tid = threadIdx.x;
+  const int R = (B + blockDim.x - 1) / blockDim.x;
+  const int r0 = min(B, tid * R), r1 = min(B, r0 + R);
+  long long local = 0;
+  for (int r = r0; r < r1; ++r) {
+    const int L = len ? len[r] : k;
+    const int w = window < L ? window : L;
+    windows[r] = w < 0 ? 0 : w;
+    local += w < 0 ? 0 : w;
+  }
+  long long total;
+  long long off = block_excl_scan<long long>(local, s_tmp, total);
+  if (win_offsets) {
+    for (int r = r0; r < r1; ++r) {
+      win_offsets[r] = (int32_t)off;
+      off += windows[r];
+    }
+    if (tid == 0) win_offsets[B] = (int32_t)total;
+  }
+}
+
 __global__ void verify_matrix_kernel(const double* __restrict__ alpha, const int32_t* __restrict__ len,
                                      const int32_t* __restrict__ windows, const int32_t* __restrict__ win_off,
                                      const double* __restrict__ u, int B, int k, int32_t* __restrict__ accepted,
@@ -93,6 +122,22 @@ extern "C" int tetris_compact(const int32_t* accepted, const int32_t* out_tok, c
   if (B > 0 && (!accepted || !out_tok || !tokens || (k > 0 && !d)))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   compact_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(accepted, out_tok, d, cap, B, k, offsets, tokens);
+  return abi::launch_check();
+}
+
+extern "C" int tetris_uniform_windows(const int32_t* len, int32_t B, int32_t k, int32_t window, int32_t* windows,
+                                      int32_t* win_offsets, tetris_stream_t stream) {
+  using namespace tetris;
+  if (B < 0 || k < 0 || window < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "bad shape B=%d k=%d window=%d", B, k, window);
+  if (B == 0) {
+    if (win_offsets) {
+      cudaError_t e = cudaMemsetAsync(win_offsets, 0, sizeof(int32_t), (cudaStream_t)stream);
+      if (e != cudaSuccess) return abi::cuda_fail(e);
+    }
+    return TETRIS_OK;
+  }
+  if (!windows) return abi::fail(TETRIS_INVALID_ARGUMENT, "windows is required");
+  uniform_windows_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(len, B, k, window, windows, win_offsets);
   return abi::launch_check();
 }
 

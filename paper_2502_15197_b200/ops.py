@@ -141,6 +141,50 @@ def select(vals: torch.Tensor, capacity: int, lengths: Optional[torch.Tensor] = 
     return out
 
 
+def dsd_window(alpha_estimate: float, n_rows: int, capacity: int, depth_limit: int) -> int:
+    """select_dsd's common window (selector.py:193-222): argmax over k in [1, min(depth_limit, capacity // n_rows)] of
+    sum_{j<=k} alpha^j with the same fp64 running product / sum, first maximum wins; 0 when no token per row fits."""
+    if not 0.0 <= alpha_estimate <= 1.0:
+        raise ValueError(f"alpha_estimate {alpha_estimate!r} outside [0, 1]")
+    if n_rows < 1:
+        raise ValueError(f"n_rows must be >= 1, got {n_rows}")
+    if depth_limit < 1:
+        raise ValueError(f"depth_limit must be >= 1, got {depth_limit}")
+    k_max = min(depth_limit, capacity // n_rows)
+    if k_max < 1:
+        return 0
+    best_k, best, value, power = 1, alpha_estimate, alpha_estimate, alpha_estimate
+    for k in range(2, k_max + 1):
+        power *= alpha_estimate
+        value += power
+        if value > best:
+            best, best_k = value, k
+    return best_k
+
+
+def uniform_windows(window: int, lengths: Optional[torch.Tensor] = None, B: Optional[int] = None, k: int = 0, *,
+                    windows: Optional[torch.Tensor] = None, win_offsets: Optional[torch.Tensor] = None,
+                    device=None, stream: Optional[torch.cuda.Stream] = None):
+    """Baseline policies on the tensor API: windows[b] = min(window, lengths[b]) (fixed window / sd / dsd common
+    window clamped to each drafted depth, sim_engine.py:358-368) and their exclusive scan, on the device."""
+    if window < 0:
+        raise ValueError(f"window must be >= 0, got {window}")
+    lengths = _need_cuda("lengths", lengths, _I32, 1, optional=True)
+    if lengths is not None:
+        B = lengths.shape[0]
+        device = lengths.device
+    if B is None:
+        raise ValueError("give lengths or B")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if windows is None:
+        windows = torch.empty(B, dtype=_I32, device=dev)
+    if win_offsets is None:
+        win_offsets = torch.empty(B + 1, dtype=_I32, device=dev)
+    N.call("tetris_uniform_windows", _ptr(lengths), B, k, int(window), _ptr(windows), _ptr(win_offsets),
+           _stream_handle(stream))
+    return windows, win_offsets
+
+
 def heap_stats(cum: torch.Tensor, capacity: int, lengths: Optional[torch.Tensor] = None,
                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """Exact PolicyStats incl. heapq comparisons (selector.py:151-176); single-thread accounting kernel."""
@@ -329,9 +373,14 @@ class TetrisStep:
     all buffers are preallocated, nothing synchronises the host, so `run` can be captured in a CUDA graph."""
 
     def __init__(self, B: int, k: int, V: int, capacity: int, mode: str = "stochastic", device="cuda",
-                 u_layout: str = "dense", group=None):
+                 u_layout: str = "dense", group=None, policy: str = "tetris"):
         if mode not in ("stochastic", "greedy"):
             raise ValueError(f"mode must be 'stochastic' or 'greedy', got {mode!r}")
+        if policy not in ("tetris", "fixed"):
+            raise ValueError(f"policy must be 'tetris' or 'fixed', got {policy!r}")
+        if policy == "fixed" and group is not None:
+            raise ValueError("the fixed-window baseline needs no global exchange; run it per shard without a group")
+        self.policy = policy
         self.B, self.k, self.V, self.C, self.mode = B, k, V, int(capacity), mode
         self.u_layout = u_layout
         dev = torch.device(device)
@@ -363,7 +412,7 @@ class TetrisStep:
         self.ws = Workspace(dev, N.OP_ALL, Bg, k, V)
         self._lib = N.load()
 
-    def run(self, conf, lengths, p, q, d, u_acc=None, u_res=None, cap=None, events=None) -> None:
+    def run(self, conf, lengths, p, q, d, u_acc=None, u_res=None, cap=None, events=None, window=None) -> None:
         """events: optional 4 torch.cuda.Events recorded around select / verify / compact (kernel timing).  The
         stochastic step is two launches (select+accept+compaction offsets, then the streaming sampler), so its
         events bracket [select kernel | sampler | nothing]."""
@@ -371,6 +420,9 @@ class TetrisStep:
         B, k, V = self.B, self.k, self.V
         if events is not None:
             events[0].record()
+        if self.policy == "fixed":
+            self._run_fixed(lengths, p, q, d, u_acc, u_res, cap, events, window)
+            return
         if self.world > 1:
             import torch.distributed as dist
 
@@ -417,6 +469,33 @@ class TetrisStep:
         if events is not None:
             events[3].record()
 
+    def _run_fixed(self, lengths, p, q, d, u_acc, u_res, cap, events, window) -> None:
+        """Baseline step (fixed window / sd / dsd common window, clamped to each depth): windows kernel, then the same
+        verification and compaction kernels as the TETRIS step, so step times compare apples to apples."""
+        lib, ws, s = self._lib, self.ws, torch.cuda.current_stream().cuda_stream
+        B, k, V = self.B, self.k, self.V
+        w = self.C // B if window is None else int(window)
+        self._check(lib.tetris_uniform_windows(_ptr(lengths), B, k, w, self.windows.data_ptr(),
+                                               self.win_offsets.data_ptr(), s))
+        if events is not None:
+            events[1].record()
+        if self.mode == "stochastic":
+            self._check(lib.tetris_verify_stochastic_f32(
+                p.data_ptr(), q.data_ptr(), d.data_ptr(), self.windows.data_ptr(),
+                self.win_offsets.data_ptr() if self.u_layout == "packed" else None, u_acc.data_ptr(),
+                u_res.data_ptr(), B, k, V, self.accepted.data_ptr(), self.out_tok.data_ptr(), self.mass.data_ptr(),
+                self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+        else:
+            self._check(lib.tetris_verify_greedy_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), B, k, V,
+                                                     self.accepted.data_ptr(), self.out_tok.data_ptr(),
+                                                     self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+        if events is not None:
+            events[2].record()
+        self._check(lib.tetris_compact(self.accepted.data_ptr(), self.out_tok.data_ptr(), d.data_ptr(), _ptr(cap), B,
+                                       k, self.offsets.data_ptr(), self.tokens.data_ptr(), s))
+        if events is not None:
+            events[3].record()
+
     def _check(self, rc: int) -> None:
         if rc != N.OK:
             msg = self._lib.tetris_last_error().decode(errors="replace")
@@ -425,7 +504,10 @@ class TetrisStep:
     @property
     def launches_per_step(self) -> int:
         # stochastic: select_kernel (+ accept CTAs), persist_stream_kernel (streaming + grid barrier + descent);
-        # greedy: select_kernel, greedy_kernel, compact_kernel
+        # greedy: select_kernel, greedy_kernel, compact_kernel; fixed-window baseline: windows, accept, stream,
+        # compact (stochastic) or windows, greedy, compact
+        if self.policy == "fixed":
+            return 4 if self.mode == "stochastic" else 3
         return 2 if self.mode == "stochastic" else 3
 
 

@@ -18,7 +18,7 @@ from .accept_model import AcceptanceMatrix, _device
 from .errors import CapacityExceededError, OracleSizeExceededError  # noqa: F401  (re-exported names)
 
 __all__ = ["Candidate", "Selection", "PolicyStats", "cumulative_products", "select_tetris", "expected_accepted",
-           "select_tensor"]
+           "select_tensor", "select_fixed_window", "select_dsd"]
 
 
 @dataclass(frozen=True)
@@ -119,6 +119,23 @@ def select_tetris(candidates: Sequence, capacity: int, *, exact_stats: bool = Tr
     ops.raise_for_status(res.status, "select_tetris")
     windows = tuple(int(x) for x in res.windows.cpu().numpy())
     return Selection(windows), PolicyStats(int(st[0]), int(st[1]), int(st[2]), int(st[3]))
+
+
+def select_fixed_window(n_rows: int, window: int, capacity: int) -> Selection:
+    """Classic batched speculation: every row sends the same `window` tokens (selector.py:179-190)."""
+    if n_rows < 1:
+        raise ValueError(f"n_rows must be >= 1, got {n_rows}")
+    if window < 0:
+        raise ValueError(f"window must be >= 0, got {window}")
+    if n_rows * window > capacity:
+        raise CapacityExceededError(
+            f"{n_rows} rows x window {window} = {n_rows * window} tokens exceeds capacity {capacity}")
+    return Selection((window,) * n_rows)
+
+
+def select_dsd(alpha_estimate: float, n_rows: int, capacity: int, depth_limit: int) -> Selection:
+    """Adaptive common window from a scalar acceptance-rate estimate (selector.py:193-222)."""
+    return Selection((ops.dsd_window(alpha_estimate, n_rows, capacity, depth_limit),) * n_rows)
 
 
 def expected_accepted(selection: Selection, probs: AcceptanceMatrix) -> float:

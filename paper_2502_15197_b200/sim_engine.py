@@ -70,9 +70,14 @@ class GpuStepOutcome:
     credited: tuple
     bonus: int
     expected_accepted: float
-    stats: object  # PolicyStats (tetris, comparisons = -1) or None
+    stats: object  # PolicyStats (tetris, with the exact heapq comparison count) or None
     completions: tuple  # ((request id, arrival step), ...) in active-list order
     alpha_hat: float
+    tau: float = 0.0  # step wall time under the configured pipeline (sim_engine.py:412-425)
+
+    @property
+    def sent(self) -> int:
+        return sum(self.windows)
 
 
 class GpuSimulator:
@@ -87,7 +92,13 @@ class GpuSimulator:
     completion order."""
 
     def __init__(self, batch_size: int, k: int, capacity: int, *, extra: int = 0, policy: str = "tetris",
-                 dsd_decay: float = 0.9, dsd_initial_estimate: float = 0.5, uniforms=None, lengths=None, device=None):
+                 dsd_decay: float = 0.9, dsd_initial_estimate: float = 0.5, uniforms=None, lengths=None, device=None,
+                 pipeline: str = "sequential", draft_time_per_token: float = 0.0025,
+                 selection_overhead: float = 0.0003, verify_time: float = 0.025):
+        if pipeline not in ("sequential", "parallel"):
+            raise ValueError(f"pipeline must be 'sequential' or 'parallel', got {pipeline!r}")
+        self.pipeline, self.draft_time_per_token = pipeline, draft_time_per_token
+        self.selection_overhead, self.verify_time = selection_overhead, verify_time
         if policy not in POLICY_CODES:
             raise ValueError(f"policy must be one of {tuple(POLICY_CODES)}, got {policy!r}")
         if batch_size < 1 or batch_size > 1024:
@@ -154,6 +165,7 @@ class GpuSimulator:
         comps = tuple(zip((int(x) for x in self.done_ids[:n_done].cpu().numpy()),
                           (int(x) for x in self.done_arrival[:n_done].cpu().numpy())))
         return GpuStepOutcome(
+            tau=self.step_time(depths),
             step=int(cnt[3]) - 1,
             windows=tuple(int(x) for x in self.windows.cpu().numpy()),
             accepted=tuple(int(x) for x in self.accepted.cpu().numpy()),
@@ -164,6 +176,15 @@ class GpuSimulator:
             completions=comps,
             alpha_hat=float(self.alpha_hat.item()),
         )
+
+    def step_time(self, drafted_depths) -> float:
+        """step_time (sim_engine.py:412-425): drafting + selection, then verification (sequential) or the slower of
+        the two (parallel)."""
+        draft_path = self.draft_time_per_token * (max(drafted_depths) if drafted_depths else 0) + \
+            self.selection_overhead
+        if self.pipeline == "sequential":
+            return draft_path + self.verify_time
+        return max(draft_path, self.verify_time)
 
     def _pack(self, rows, depths) -> torch.Tensor:
         B, K = self.B, self.K

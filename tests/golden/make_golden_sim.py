@@ -28,6 +28,7 @@ def main():
     sys.path.insert(0, str(REF))
     import tetris_sched.sim_engine as E
     from tetris_sched.accept_model import BetaSource, MixSource, SurrogateConfig
+    from tetris_sched.trace_io import write_trace
 
     runs = []
     cases = [
@@ -65,9 +66,11 @@ def main():
 
         E.draft_phase = recording_draft
         steps = []
+        outs = []
         try:
             for _ in range(cfg.steps):
                 out = E.run_step(state, cfg)
+                outs.append(out)
                 truth, surrogate = rec[-1]
                 depths = [len(r) for r in truth.rows]
                 K = cfg.k + cfg.extra
@@ -86,6 +89,8 @@ def main():
                 })
         finally:
             E.draft_phase = real_draft
+        trace = OUT.parent / f"sim_trace_{c['tag']}.jsonl"
+        write_trace(outs, trace)  # the reference's own JSONL writer (trace_io.py:166-173)
         used = sum(sum(s["windows"]) for s in steps)
         assert np.array_equal(uniforms[:used], np.random.default_rng(
             np.random.SeedSequence(cfg.seed).spawn(4)[3]).random(used))
