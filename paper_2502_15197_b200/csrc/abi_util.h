@@ -41,10 +41,13 @@ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 // so a workspace reused across calls of different shapes never finds stale sums where counters must be zero.
 constexpr size_t kRequestSlots = 65536;                 // per-request arrival counters [0, 65536)
 constexpr size_t kSlotAccCounter = kRequestSlots;        // accept-CTA arrivals of the fused select launch
-constexpr size_t kSlotGridCount = kRequestSlots + 1;     // grid barrier of the persistent sampler: arrivals
-constexpr size_t kSlotGridGen = kRequestSlots + 2;       //   ... and generation
+constexpr size_t kSlotGridCount = kRequestSlots + 2;     // grid barrier of the persistent sampler: arrivals
+constexpr size_t kSlotGridGen = kRequestSlots + 3;       //   ... and generation
+constexpr size_t kSlotWorkCounter = kRequestSlots + 4;   // the sampler's dynamic work counter (64-bit, 2 slots)
 constexpr size_t kCounterSlots = kRequestSlots + 64;
 static_assert(kSlotGridGen == kSlotGridCount + 1, "grid_barrier reads the generation at bar + 1");
+static_assert(kSlotWorkCounter == kSlotGridCount + 2 && (kSlotWorkCounter % 2) == 0,
+              "persist_stream_kernel reads its 8-byte-aligned work counter at grid_bar + 2");
 
 inline size_t region_offset(int op, int B, int k, int V, Region which) {
   const size_t nch = (size_t)((V + TETRIS_CHUNK_ELEMS - 1) / TETRIS_CHUNK_ELEMS);

@@ -91,22 +91,25 @@ __device__ int descend_global(const float* __restrict__ P, const float* __restri
     load_lane<float, true>(P, e0 + s * kSegElems + lane * kLaneElems, V, pv[s]);
     if (RES) load_lane<float, true>(Q, e0 + s * kSegElems + lane * kLaneElems, V, qv[s]);
   }
-  double wl[kWarpSegs][8];
 #pragma unroll
   for (int s = 0; s < kWarpSegs; ++s) {
+    double wl[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) wl[s][i] = RES ? w_res((double)pv[s][i], (double)qv[s][i]) : w_plain((double)pv[s][i]);
-    G[s] = seg_sum(fold8(wl[s]));
+    for (int i = 0; i < 8; ++i) wl[i] = RES ? w_res((double)pv[s][i], (double)qv[s][i]) : w_plain((double)pv[s][i]);
+    G[s] = seg_sum(fold8(wl));
   }
   const int s = seq_find(G, kWarpSegs, T);
   if (s < 0) return -1;
-  double w[8];
+  double w[8];  // the chosen segment's weights, recomputed from the loaded lanes (identical arithmetic)
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    double x = wl[0][i];
+    float pp = pv[0][i], qq = RES ? qv[0][i] : 0.f;
 #pragma unroll
-    for (int ss = 1; ss < kWarpSegs; ++ss) x = (s == ss) ? wl[ss][i] : x;
-    w[i] = x;
+    for (int ss = 1; ss < kWarpSegs; ++ss) {
+      pp = (s == ss) ? pv[ss][i] : pp;
+      if (RES) qq = (s == ss) ? qv[ss][i] : qq;
+    }
+    w[i] = RES ? w_res((double)pp, (double)qq) : w_plain((double)pp);
   }
   double lv[5];
   lv[0] = fold8(w);
@@ -143,12 +146,6 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane)
   const double* ws = a.warp_sums + (int64_t)b * nch * kChunkWarps;
   double s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
   double s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
-  double wv[16];  // warp sums i = lane + 32*x, x < 16 (nch <= 64 -> 512 sums)
-#pragma unroll
-  for (int x = 0; x < 16; ++x) {
-    const int i = lane + 32 * x;
-    wv[x] = i < nch * kChunkWarps ? __ldcg(ws + i) : 0.0;
-  }
   // accepted-prefix tokens of the compacted stream, in parallel with the loads above
   int acc = 0, off = 0, end = 0;
   if (a.accepted) {
@@ -185,15 +182,11 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane)
       cc = last_pos;
       T = __longlong_as_double(0x7ff0000000000000ll);
     }
+    // the 8 warp sums of the chosen chunk (lanes 0..7 load, then broadcast)
+    const double wl = (cc >= 0 && lane < kChunkWarps) ? __ldcg(ws + (int64_t)cc * kChunkWarps + lane) : 0.0;
     double Wc[kChunkWarps];
 #pragma unroll
-    for (int w = 0; w < kChunkWarps; ++w) {
-      const int i = cc * kChunkWarps + w;
-      double v = 0.0;
-#pragma unroll
-      for (int x = 0; x < 16; ++x) v = (x == (i >> 5)) ? wv[x] : v;
-      Wc[w] = __shfl_sync(kFull, v, i & 31);
-    }
+    for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __shfl_sync(kFull, wl, w);
     const int ww = seq_find(Wc, kChunkWarps, T);
     if (cc >= 0 && ww >= 0) {
       const int64_t e0 = (int64_t)cc * kChunkElems + ww * kWarpElems;
@@ -220,6 +213,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n) {
   const int old = atomic_add_acq_rel_gpu(reinterpret_cast<int*>(bar), 1);
   if ((unsigned)old == n - 1) {
     bar[0] = 0u;
+    *reinterpret_cast<unsigned long long*>(bar + 2) = 0ull;  // the sampler's work counter (every CTA is done with it)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(g0 + 1u) : "memory");
   } else {
     unsigned g;
@@ -238,6 +232,11 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
   const int nch = a.nch;
   const long long total = (long long)a.R * nch;
   const int G = gridDim.x;
+  // dynamic work distribution: items (request b, chunk c) are handed out in order from one global counter, so the
+  // SMs stream neighbouring chunks at any moment (DRAM locality, like a round robin) and an SM that drew more
+  // residual (p + q) items simply takes fewer items (balance).  The counter sits beside the grid barrier and is reset
+  // by the barrier's last arrival.
+  unsigned long long* work = reinterpret_cast<unsigned long long*>(a.grid_bar + 2);
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -253,24 +252,36 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
   __syncthreads();
 
   if (warp == kProducerWarp) {
-    // ---------------------------------------------------------------- producer
-    long long pr_p = 0, pr_q = -1;
-    int t = 0;
-    for (long long i = blockIdx.x; i < total; i += G, ++t) {
-      if ((t & 31) == 0) {  // refill 32 items of row info, one per lane
-        const long long ii = i + (long long)lane * G;
-        if (ii < total) {
-          const int bb = (int)(ii / nch);
-          pr_p = a.prow[(int64_t)bb * a.row_stride];
-          pr_q = a.qrow ? a.qrow[(int64_t)bb * a.row_stride] : -1;
-        }
+    // ---------------------------------------------------------------- producer (lane 0)
+    if (lane == 0) {
+      // two items of look-ahead on the counter and the row info, so neither round trip stalls the copies
+      long long i_next = (long long)atomicAdd(work, 1ull);
+      long long i_next2 = (long long)atomicAdd(work, 1ull);
+      long long pn = 0, qn = -1;
+      if (i_next < total) {
+        const int bb = (int)(i_next / nch);
+        pn = a.prow[(int64_t)bb * a.row_stride];
+        qn = a.qrow ? a.qrow[(int64_t)bb * a.row_stride] : -1;
       }
-      const long long prow = __shfl_sync(kFull, pr_p, t & 31);
-      const long long qrow = __shfl_sync(kFull, pr_q, t & 31);
-      const int s = t % kStages;
-      const uint32_t ph = (uint32_t)((t / kStages) & 1);
-      if (t >= kStages) mbar_wait(&sh.empty[s], ph ^ 1u);
-      if (lane == 0) {
+      for (int t = 0;; ++t) {
+        const long long i = i_next;
+        const long long prow = pn, qrow = qn;
+        i_next = i_next2;
+        if (i < total) {
+          i_next2 = (long long)atomicAdd(work, 1ull);
+          if (i_next < total) {
+            const int bb = (int)(i_next / nch);
+            pn = a.prow[(int64_t)bb * a.row_stride];
+            qn = a.qrow ? a.qrow[(int64_t)bb * a.row_stride] : -1;
+          }
+        }
+        const int s = t % kStages;
+        if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
+        if (i >= total) {  // end of stream: a sentinel stage without data
+          sh.meta[s] = StageMeta{-1, 0, 0, 0};
+          mbar_arrive(&sh.full[s]);
+          break;
+        }
         const int b = (int)(i / nch), c = (int)(i % nch);
         const int n = min(kChunkElems, a.V - c * kChunkElems);
         const uint32_t bytes = (uint32_t)n * sizeof(float);
@@ -281,15 +292,23 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
         bulk_g2s(sp, a.p + prow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s]);
         if (res) bulk_g2s(sp + kChunkElems, a.q + qrow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s]);
       }
-      __syncwarp();
     }
+    __syncwarp();
   } else if (warp < kConsumerWarps) {
     // ---------------------------------------------------------------- consumers
-    int t = 0;
-    for (long long i = blockIdx.x; i < total; i += G, ++t) {
+    for (int t = 0;; ++t) {
       const int s = t % kStages;
       mbar_wait(&sh.full[s], (uint32_t)((t / kStages) & 1));
       const StageMeta m = sh.meta[s];
+      const int slot = t % kRing;
+      if (t >= kRing) mbar_wait(&sh.ring_free[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
+      if (m.b < 0) {  // forward the end of stream to the publisher
+        if (lane == 0) {
+          if (warp == 0) sh.ring_meta[slot] = m;
+          mbar_arrive(&sh.ring_full[slot]);
+        }
+        break;
+      }
       const float* sp = reinterpret_cast<const float*>(stage_mem + s * kStageBytes);
       double Gs[kSegsPerConsumer];
 #pragma unroll
@@ -299,10 +318,8 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
                                 seg * kSegElems, a.V, lane);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.empty[s]);
-      const int slot = t % kRing;
-      if (t >= kRing) mbar_wait(&sh.ring_free[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
       if (lane == 0) {
+        mbar_arrive(&sh.empty[s]);
 #pragma unroll
         for (int x = 0; x < kSegsPerConsumer; ++x) sh.ring_g[slot][warp * kSegsPerConsumer + x] = Gs[x];
         if (warp == 0) sh.ring_meta[slot] = m;
@@ -312,33 +329,26 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
     }
   } else {
     // ---------------------------------------------------------------- publisher
-    // Folds the chunk sum and stores chunk + warp sums; the descent runs in finalize_kernel after this grid, so no
-    // streaming CTA ever waits on another (a slow CTA cannot be handed extra work).
-    const long long first = blockIdx.x;
-    const int my_items = first < total ? (int)((total - 1 - first) / G + 1) : 0;
-    for (int t0 = 0; t0 < my_items; t0 += 32) {  // lane l publishes item t0 + l
-      const int j = t0 + lane;
-      const bool mine = j < my_items;
-      const int slot = j % kRing;
-      if (mine) mbar_wait(&sh.ring_full[slot], (uint32_t)((j / kRing) & 1));
-      if (mine) {
-        const StageMeta m = sh.ring_meta[slot];
-        double W[kChunkWarps];
-        double S = 0.0;
+    // One published chunk per iteration: lanes 0..7 fold a warp run each (4 segments left to right), lane 0 folds the
+    // chunk sum over the 8 runs left to right, and the sums go to global memory for the descent.
+    for (int t = 0;; ++t) {
+      const int slot = t % kRing;
+      mbar_wait(&sh.ring_full[slot], (uint32_t)((t / kRing) & 1));
+      const StageMeta m = sh.ring_meta[slot];
+      if (m.b < 0) break;
+      double x = 0.0;
+      if (lane < kChunkWarps) {
 #pragma unroll
-        for (int w = 0; w < kChunkWarps; ++w) {  // warp run = 4 segments left to right; chunk = 8 runs left to right
-          double x = 0.0;
-#pragma unroll
-          for (int q = 0; q < kWarpSegs; ++q) x = x + sh.ring_g[slot][w * kWarpSegs + q];
-          W[w] = x;
-          S = S + W[w];
-        }
-        mbar_arrive(&sh.ring_free[slot]);
-        const int64_t cs = (int64_t)m.b * nch + m.c;
-        __stcg(&a.chunk_sums[cs], S);
-#pragma unroll
-        for (int w = 0; w < kChunkWarps; ++w) __stcg(&a.warp_sums[cs * kChunkWarps + w], W[w]);
+        for (int q = 0; q < kWarpSegs; ++q) x = x + sh.ring_g[slot][lane * kWarpSegs + q];
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.ring_free[slot]);
+      double S = 0.0;
+#pragma unroll
+      for (int w = 0; w < kChunkWarps; ++w) S = S + __shfl_sync(kFull, x, w);
+      const int64_t cs = (int64_t)m.b * nch + m.c;
+      if (lane < kChunkWarps) __stcg(&a.warp_sums[cs * kChunkWarps + lane], x);
+      if (lane == 0) __stcg(&a.chunk_sums[cs], S);
     }
   }
   if (a.grid_bar != nullptr) {
