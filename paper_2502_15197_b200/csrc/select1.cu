@@ -99,6 +99,9 @@ template <int RPT>
 __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(16) S1Shared sh;
+  // programmatic dependent launch: the sampler that follows may be scheduled onto the SMs this grid leaves idle and
+  // run its prologue; it reads nothing of ours before its griddepcontrol.wait (= this grid complete and flushed)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (blockIdx.x > 0) {
     accept_role(a, blockIdx.x - 1, gridDim.x - 1);
     return;

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Stage (3) streaming: the persistent, warp-specialised residual / bonus sampler (sm_100a, fp32 rows, V % 8 == 0).
 //
 // One CTA per SM, 10 warps:
@@ -250,6 +251,9 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
     mbar_fence_init();
   }
   __syncthreads();
+  // launched as a programmatic dependent of the selector: wait for it (and its memory) before the first read of the
+  // row info it wrote; no-op for a plain launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kProducerWarp) {
     // ---------------------------------------------------------------- producer (lane 0)
@@ -483,12 +487,20 @@ int launch_persist_stream(const StreamArgs& a, cudaStream_t st) {
     cfg.blockDim = dim3(kPersistThreads, 1, 1);
     cfg.dynamicSmemBytes = kPersistSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap our launch with the selector's tail
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const int pdl = getenv("TETRIS_NO_PDL") ? 0 : 1;
+    cfg.numAttrs = 1 + pdl;
     e = cudaLaunchKernelEx(&cfg, persist_stream_kernel, a);
+    if (e != cudaSuccess && pdl) {  // cooperative + programmatic not accepted: plain stream order
+      cudaGetLastError();
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, persist_stream_kernel, a);
+    }
     if (e != cudaSuccess) return abi::cuda_fail(e);
     return abi::launch_check();
   }
