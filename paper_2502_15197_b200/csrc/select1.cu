@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
       }
       __syncthreads();
     }
+    if (stamp) a.dbg[6] = clock64();
     int nr[RPT];
     long long my_emit = 0;
 #pragma unroll

@@ -18,8 +18,8 @@ for it in range(5):
     step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
     torch.cuda.synchronize()
     d = dbg.cpu().tolist()
-    print('cycles: keys %d (staging %d) radix %d (passes %d) windows %d epilogue %d total %d' % (
-        d[1] - d[0], d[5] - d[0], d[2] - d[1], d[9], d[3] - d[2], d[4] - d[3], d[4] - d[0]))
+    print('cycles: keys %d (staging %d) radix %d (passes %d) windows %d epilogue %d (accept wait %d) total %d' % (
+        d[1] - d[0], d[5] - d[0], d[2] - d[1], d[9], d[3] - d[2], d[4] - d[3], d[6] - d[3], d[4] - d[0]))
     prev = d[1]
     parts = []
     for p in range(d[9]):
