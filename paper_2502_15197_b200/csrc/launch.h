@@ -59,8 +59,9 @@ struct StreamArgs {
   int32_t* tokens;
   const int32_t* d;
   int k;
-  unsigned* grid_bar;  // [2] arrivals, generation (zero-initialised workspace): the descent runs in-kernel after a
-                       // grid barrier (cooperative launch); nullptr -> a separate finalize_kernel launch
+  unsigned* grid_bar;  // [0]: CTAs done, [2..3]: 64-bit work counter (zero-initialised workspace, left at zero)
+  int* req_cnt;        // [R] per-request published-chunk counters (zero, left at zero): the descent runs in the same
+                       // launch as each request completes; nullptr -> a separate finalize_kernel launch
 };
 
 int launch_select(const SelectArgs& a, cudaStream_t st);

@@ -205,27 +205,6 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane)
   }
 }
 
-// Sense-free generation barrier over the whole (co-resident, cooperative) grid; called by one thread per CTA after a
-// __syncthreads.  bar[0] counts arrivals and is reset by the last arrival, which then bumps the generation bar[1].
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n) {
-  unsigned g0;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(bar + 1) : "memory");
-  __threadfence();
-  const int old = atomic_add_acq_rel_gpu(reinterpret_cast<int*>(bar), 1);
-  if ((unsigned)old == n - 1) {
-    bar[0] = 0u;
-    *reinterpret_cast<unsigned long long*>(bar + 2) = 0ull;  // the sampler's work counter (every CTA is done with it)
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(g0 + 1u) : "memory");
-  } else {
-    unsigned g;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
-      if (g != g0) break;
-      __nanosleep(32);
-    }
-  }
-}
-
 __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(const StreamArgs a) {
   extern __shared__ __align__(128) uint8_t stage_mem[];
   __shared__ PersistShared sh;
@@ -334,7 +313,17 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
   } else {
     // ---------------------------------------------------------------- publisher
     // One published chunk per iteration: lanes 0..7 fold a warp run each (4 segments left to right), lane 0 folds the
-    // chunk sum over the 8 runs left to right, and the sums go to global memory for the descent.
+    // chunk sum over the 8 runs left to right, and the sums go to global memory for the descent.  Arrivals on the
+    // per-request counters are batched: after 32 published chunks (and at the end) one release fence, then one
+    // relaxed increment per chunk (lane i for the i-th pending chunk).
+    int pend_b = 0, npend = 0;
+    auto flush = [&]() {
+      if (npend == 0 || a.req_cnt == nullptr) return;
+      __syncwarp();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (lane < npend) atomicAdd(a.req_cnt + pend_b, 1);
+      npend = 0;
+    };
     for (int t = 0;; ++t) {
       const int slot = t % kRing;
       mbar_wait(&sh.ring_full[slot], (uint32_t)((t / kRing) & 1));
@@ -353,18 +342,39 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
       const int64_t cs = (int64_t)m.b * nch + m.c;
       if (lane < kChunkWarps) __stcg(&a.warp_sums[cs * kChunkWarps + lane], x);
       if (lane == 0) __stcg(&a.chunk_sums[cs], S);
+      if (lane == npend) pend_b = m.b;
+      if (++npend == 32) flush();
     }
+    flush();
   }
-  if (a.grid_bar != nullptr) {
-    // every chunk of every request is published once all CTAs pass the barrier; then one warp per request runs
-    // the descent (requests strided over the CTAs so the re-reads spread over all SMs)
-    __syncthreads();
-    if (tid == 0) grid_barrier(a.grid_bar, (unsigned)G);
+  if (a.req_cnt != nullptr) {
+    // Descent, one warp per request (requests strided over the CTAs so the re-reads spread over all SMs), as soon
+    // as the request's nch chunks are published.  A warp only ever waits for chunks already claimed from the work
+    // counter by CTAs that are running, so no co-residency (cooperative launch) is needed.
     __syncthreads();
     constexpr int kWarps = kPersistThreads / 32;
     for (int b = warp * G + blockIdx.x; b < a.R; b += G * kWarps) {
+      if (lane == 0) {
+        int seen;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.req_cnt + b) : "memory");
+          if (seen >= nch) break;
+          __nanosleep(64);
+        }
+        a.req_cnt[b] = 0;  // every arrival is in: ready for the next launch
+      }
+      __syncwarp();
       const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
       finalize_request(a, b, qrow >= 0, lane);
+    }
+    // the last CTA out resets the work counter (every producer is done with it)
+    __syncthreads();
+    if (tid == 0) {
+      unsigned* done = a.grid_bar;
+      if (atomicAdd(done, 1u) == (unsigned)G - 1) {
+        *work = 0ull;
+        *done = 0u;
+      }
     }
   }
 }
@@ -480,27 +490,19 @@ int launch_persist_stream(const StreamArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return abi::cuda_fail(e);
   const long long items = (long long)a.R * a.nch;
   const int grid = (int)(items < g_num_sms ? items : g_num_sms);
-  if (a.grid_bar != nullptr) {
-    // one launch: streaming + grid barrier + descent; cooperative so the barrier's CTAs are co-resident
+  if (a.req_cnt != nullptr) {
+    // one launch: streaming + per-request completion counters + descent
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kPersistThreads, 1, 1);
     cfg.dynamicSmemBytes = kPersistSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap our launch with the selector's tail
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap our launch with the selector's tail
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    static const int pdl = getenv("TETRIS_NO_PDL") ? 0 : 1;
-    cfg.numAttrs = 1 + pdl;
+    cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, persist_stream_kernel, a);
-    if (e != cudaSuccess && pdl) {  // cooperative + programmatic not accepted: plain stream order
-      cudaGetLastError();
-      cfg.numAttrs = 1;
-      e = cudaLaunchKernelEx(&cfg, persist_stream_kernel, a);
-    }
     if (e != cudaSuccess) return abi::cuda_fail(e);
     return abi::launch_check();
   }

@@ -430,6 +430,7 @@ extern "C" int tetris_verify_stochastic_f32(const float* p, const float* q, cons
     a.chunk_sums = cs;
     a.warp_sums = wsum;
     a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
+    a.req_cnt = cnt;
     return launch_persist_stream(a, st);
   }
   const bool vec = (V % 8 == 0) && aligned32(p) && aligned32(q);
@@ -530,6 +531,7 @@ extern "C" int tetris_resample_f32(const float* p, const float* q, const double*
   a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
   a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
   a.grid_bar = (unsigned*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + abi::kSlotGridCount;
+  a.req_cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   if (tokens) {
     if (!accepted || !offsets || !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted, offsets, d");
     a.accepted = accepted;
@@ -609,6 +611,7 @@ extern "C" int tetris_sample_rows_f32(const float* p, const float* q, const int6
     a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_CHUNK_SUMS);
     a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, R, 0, V, abi::WS_WARP_SUMS);
     a.grid_bar = (unsigned*)a.counters + abi::kSlotGridCount;
+    a.req_cnt = a.counters;
     return launch_persist_stream(a, (cudaStream_t)stream);
   }
   return sample_rows_impl<float>(p, q, p_row, q_row, u, R, V, out_idx, mass_out, status, ws, ws_bytes,
