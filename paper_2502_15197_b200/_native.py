@@ -5,10 +5,13 @@ There is no fallback: if the shared library is missing or fails to load, every o
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "_native" / "libtetris_b200.so"
+if os.environ.get("TETRIS_LIB_VARIANT"):  # A/B experiments: another build of the same ABI under _native/
+    LIB_PATH = LIB_PATH.parent / os.environ["TETRIS_LIB_VARIANT"]
 
 OK = 0
 INVALID_ARGUMENT = 1
