@@ -662,8 +662,7 @@ void set_debug_buffer(long long* p) { g_debug = p; }
 long long* debug_buffer() { return g_debug; }
 
 int launch_select(const SelectArgs& args_in, cudaStream_t st) {
-  static const bool force_cluster = getenv("TETRIS_EXP_CLUSTER_SELECT") != nullptr;  // experiment switch
-  if (!force_cluster && select1_eligible(args_in.B, args_in.k)) return launch_select1(args_in, st);
+  if (select1_eligible(args_in.B, args_in.k)) return launch_select1(args_in, st);
   SelectArgs a = args_in;
   a.dbg = g_debug;
   const SelShape sh = select_shape(a.B, a.k);

@@ -491,13 +491,6 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
     sa.acc_bytes = (uint8_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ACCBYTES);
     sa.acc_counter = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + abi::kSlotAccCounter;
     sa.accept_ctas = 1;
-    static const bool sep = getenv("TETRIS_EXP_SEPARATE_ACCEPT") != nullptr;  // experiment switch
-    if (sep) {
-      sa.accept_ctas = 0;
-      int rc2 = launch_pre_accept(p, q, d, u_acc, len ? len + row0 : nullptr, B, k, V, sa.acc_bytes,
-                                  (cudaStream_t)stream);
-      if (rc2) return rc2;
-    }
   }
   return launch_select(sa, (cudaStream_t)stream);
 }

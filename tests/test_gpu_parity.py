@@ -383,3 +383,39 @@ def test_sharded_step_matches_global_selection(W, B, k, V, C, rank):
     off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
     assert np.array_equal(_np(offs), off_ref)
     assert np.array_equal(_np(toks)[: off_ref[-1]], toks_ref)
+
+
+def _adversarial_rows(V, rng):
+    """fp32 rows the sampler must treat exactly like the oracle: sparse spikes, exact zeros, subnormals, p == q ties,
+    tiny residual mass, huge dynamic range."""
+    rows = []
+    sub = np.float32(1e-40)  # subnormal
+    a = np.zeros(V, np.float32); a[rng.integers(0, V, 3)] = [0.5, 0.25, 0.25]; rows.append(a)
+    b = np.full(V, sub, np.float32); b[V // 2] = 1.0; rows.append(b)
+    c = rng.random(V).astype(np.float32) * np.float32(1e-30); c[::7] = 0; rows.append(c)
+    d = (rng.random(V) ** 8).astype(np.float32); rows.append(d)
+    e = np.zeros(V, np.float32); e[-1] = 1e-38; e[0] = 3e-39; rows.append(e)
+    return rows
+
+
+def test_sampler_adversarial_rows_f32():
+    rng = np.random.default_rng(77)
+    for V in (8, 8192, 8200, 32000, 128256):
+        P = _adversarial_rows(V, rng)
+        Q = [np.roll(x, 1) for x in P]  # residual partners; row 0 vs its shift, ties where both are 0
+        Q[3] = P[3].copy(); Q[3][::3] = 0  # p == q on two thirds of the row: tiny residual
+        R = len(P)
+        p = torch.from_numpy(np.stack(P)).to(DEV)
+        q = torch.from_numpy(np.stack(Q)).to(DEV)
+        rows = torch.arange(R, dtype=torch.int64, device=DEV)
+        for u_val in (0.0, 0.37, 1.0 - 2.0 ** -53):
+            u = torch.full((R,), u_val, dtype=torch.float64, device=DEV)
+            for residual in (False, True):
+                idx, mass, st = ops.sample_rows(p, rows, u, q=q if residual else None,
+                                                q_row=rows if residual else None)
+                torch.cuda.synchronize()
+                for r in range(R):
+                    i_ref, m_ref = O.sample(P[r], u_val, q=Q[r] if residual else None)
+                    assert float(mass[r]) == m_ref, (V, r, residual)
+                    if m_ref > 0:
+                        assert int(idx[r]) == i_ref, (V, r, u_val, residual)
