@@ -52,25 +52,28 @@ class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_ms: int = 20):
         self.gpu = gpu_index
+        self.period_ms = period_ms
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host time the line arrived, text)
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def stop(self):
+    def stop(self, window=None):
+        """Summary of the samples taken inside `window` = (t0, t1) host seconds (all samples when None or when the
+        window caught none)."""
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -79,7 +82,12 @@ class ClockSampler:
                 self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if window is not None:
+            inside = [x for x in lines if window[0] <= x[0] <= window[1] + self.period_ms / 1e3]
+            lines = inside or lines
+        in_window = window is not None and bool(lines) and lines is not self.lines
+        for _, ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -93,7 +101,8 @@ class ClockSampler:
                     reasons.add(n)
         load = [x for x in sm if x > 500] or sm
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "period_ms": self.period_ms,
+                "scope": "timed region" if in_window else "whole run (no sample inside the timed region)"}
 
 
 # ----------------------------------------------------------------------------------------------------------------
@@ -185,6 +194,8 @@ def run_tetris(args):
         C = cfg["C"] * world
     k, V, mode = cfg["k"], cfg["V"], cfg["mode"]
     dev = torch.device("cuda", local)
+    clocks = ClockSampler(local)
+    clocks.start()  # early, so nvidia-smi is sampling by the time the timed region starts
     # rotate enough input sets that consecutive steps never find their inputs in L2 (126 MB on B200)
     set_bytes = B_local * ((k + 1) + k) * V * 4
     nsets = max(args.sets, -(-2 * 126 * 2**20 // set_bytes))
@@ -232,8 +243,6 @@ def run_tetris(args):
         else:
             run(i)
 
-    clocks = ClockSampler(local)
-    clocks.start()
     for i in range(args.warmup):
         step_i(i)
     torch.cuda.synchronize()
@@ -241,14 +250,16 @@ def run_tetris(args):
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
     t0.record()
     for i in range(args.steps):
         step_i(i)
     t1.record()
     torch.cuda.synchronize()
+    w1 = time.time()
     _barrier(group)
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.stop(window=(w0, w1))
     elapsed_ms = t0.elapsed_time(t1)
     # stage breakdown and the streaming kernel's duration: the same steps again, eager, with events between the
     # launches (on the launching stream)
@@ -300,8 +311,8 @@ def run_tetris(args):
                          "compact": 1e3 * statistics.median(cmp_ms)},
             "select_verify_latency_us": 1e3 * statistics.median([a + b for a, b in zip(sel_ms, ver_ms)]),
             "tokens_per_step": total_tokens / args.steps,
-            "roofline": {"bound": "hbm", "kernel": "persist_stream_kernel (tetris_resample_f32: streaming + grid "
-                         "barrier + descent; CUDA events around the launch, eager pass)" if mode == "stochastic" else "greedy_kernel", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": "persist_stream_kernel (tetris_resample_f32: streaming + per-"
+                         "request descent in the same launch; CUDA events around the launch, eager pass)" if mode == "stochastic" else "greedy_kernel", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "alg_bytes_per_launch": alg_bytes / args.steps,
                          "traffic": _load_traffic(args.config)},
