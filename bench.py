@@ -186,12 +186,14 @@ def run_tetris(args):
 
     world, rank, local, group = _setup_dist(args.gpus)
     cfg = dict(CONFIGS[args.config])
+    sim_w = args.simulate_world if world == 1 else 0
+    wsel = sim_w or world  # ranks whose requests the selection covers
     if cfg.get("strong"):
-        B_local = cfg["B"] // world
+        B_local = cfg["B"] // wsel
         C = cfg["C"]
     else:
         B_local = cfg["B"]
-        C = cfg["C"] * world
+        C = cfg["C"] * wsel
     k, V, mode = cfg["k"], cfg["V"], cfg["mode"]
     dev = torch.device("cuda", local)
     clocks = ClockSampler(local)
@@ -202,11 +204,23 @@ def run_tetris(args):
     sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
             for s in range(nsets)]
     step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None,
-                          policy=args.policy)
+                          policy=args.policy, shard=(sim_w, 0) if sim_w else None)
+    if sim_w:
+        # one rank's share of a sharded step on one GPU: this rank's requests (rank 0) + the other ranks' scores as
+        # they would arrive from the all-gather (synthetic U(0,1)^0.3 confidences; their p/q live on other GPUs)
+        gcpu = torch.Generator().manual_seed(args.seed + 1)
+        for bt in sets:
+            # the other ranks' scores: this rank's rows in shuffled orders (same distribution as real drafts)
+            others = [bt.conf[torch.randperm(B_local, generator=gcpu).to(dev)] for _ in range(sim_w - 1)]
+            bt.conf_all = torch.cat([bt.conf] + others).contiguous()
+            bt.len_all = bt.lengths.repeat(sim_w).contiguous()
 
     def run(i, events=None):
         bt = sets[i % nsets]
-        step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, events=events)
+        if sim_w:
+            step.run(bt.conf_all, bt.len_all, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, events=events)
+        else:
+            step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, events=events)
 
     # per-set verified tokens / bytes (the step is deterministic for a given input set)
     tokens_per_set, bytes_per_set = [], []
@@ -281,10 +295,10 @@ def run_tetris(args):
     assert int(step.offsets[-1].item()) == tokens_per_set[(args.steps - 1) % nsets]
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not sim_w:
         e2e = _e2e(args, cfg, step, sets[0], B_local, k, V, C, mode, group, world, dev)
     cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+    if world == 1 and rank == 0 and not args.no_cpu_baseline and not sim_w:
         cpu = _cpu_baseline(cfg, sets[0], step, B_local, C, args)
 
     if rank == 0:
@@ -306,7 +320,8 @@ def run_tetris(args):
                        "l2": "rotated input sets larger than L2 together (%.3f GB per set, %d sets)" % (
                            set_bytes / 1e9, nsets),
                        "parallelism": f"request-sharded dp{world}" + (" + NCCL all-gather select" if world > 1 else ""),
-                       "launch": "CUDA graph replay" if use_graph else "eager", "policy": args.policy},
+                       "launch": "CUDA graph replay" if use_graph else "eager", "policy": args.policy,
+                       "simulated_shard": f"rank 0 of {sim_w} on one GPU (no exchange timed)" if sim_w else None},
             "stage_us": {"select": 1e3 * statistics.median(sel_ms), "verify": 1e3 * statistics.median(ver_ms),
                          "compact": 1e3 * statistics.median(cmp_ms)},
             "select_verify_latency_us": 1e3 * statistics.median([a + b for a, b in zip(sel_ms, ver_ms)]),
@@ -589,6 +604,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="time eager launches instead of CUDA graphs")
+    ap.add_argument("--simulate-world", type=int, default=0,
+                    help="on 1 GPU: time rank 0's share of a step sharded over this many ranks (the other ranks' "
+                         "gathered scores are this rank's rows reshuffled; no NCCL exchange in the timed region)")
     ap.add_argument("--policy", default="tetris", choices=["tetris", "fixed"],
                     help="fixed: the fixed-window baseline (window C/B per request) through the same kernels")
     args = ap.parse_args()

@@ -34,6 +34,7 @@ struct SelectArgs {
   int accept_ctas;     // > 0: CTAs after cluster 0 compute acc_bytes concurrently with the selection
   int* acc_counter;    // arrivals of those CTAs (zero between launches)
   long long* dbg;      // diagnostics: per-phase clock64() stamps of CTA 0 (nullptr: off)
+  void* gscratch;      // workspace region WS_GSEL (grid selector), zero-initialised
 };
 
 void set_debug_buffer(long long* p);
@@ -67,6 +68,8 @@ struct StreamArgs {
 int launch_select(const SelectArgs& a, cudaStream_t st);
 bool select1_eligible(int B, int k);
 int launch_select1(const SelectArgs& a, cudaStream_t st);  // single-CTA selector (select1.cu)
+int launch_gselect(const SelectArgs& a, void* scratch, cudaStream_t st);  // grid-wide selector (gselect.cu)
+size_t gselect_scratch_bytes();
 int launch_persist_stream(const StreamArgs& a, cudaStream_t st);
 bool persist_eligible(const float* p, const float* q, int V);
 int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,

@@ -663,6 +663,7 @@ long long* debug_buffer() { return g_debug; }
 
 int launch_select(const SelectArgs& args_in, cudaStream_t st) {
   if (select1_eligible(args_in.B, args_in.k)) return launch_select1(args_in, st);
+  if (args_in.gscratch != nullptr) return launch_gselect(args_in, args_in.gscratch, st);
   SelectArgs a = args_in;
   a.dbg = g_debug;
   const SelShape sh = select_shape(a.B, a.k);
@@ -736,8 +737,6 @@ extern "C" int tetris_select_f64(const double* vals, const int32_t* len, int32_t
                                  int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
                                  tetris_stream_t stream) {
   using namespace tetris;
-  (void)ws;
-  (void)ws_bytes;  // the selector keeps everything in (distributed) shared memory
   if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
   if (B < 0 || B > TETRIS_MAX_SELECT_ROWS) return abi::fail(TETRIS_INVALID_ARGUMENT, "B=%d outside [0, 65535]", B);
   if (k < 0 || k > TETRIS_MAX_K) return abi::fail(TETRIS_INVALID_ARGUMENT, "k=%d outside [0, 255]", k);
@@ -765,6 +764,8 @@ extern "C" int tetris_select_f64(const double* vals, const int32_t* len, int32_t
   a.cum_out = cum_out;
   a.stats = (long long*)stats4;
   a.status = status;
+  if (ws && ws_bytes >= abi::region_offset(TETRIS_OP_SELECT, B, k, 0, abi::WS_GSEL) + abi::kGselScratchBytes)
+    a.gscratch = abi::ws_region(ws, TETRIS_OP_SELECT, B, k, 0, abi::WS_GSEL);
   return launch_select(a, (cudaStream_t)stream);
 }
 

@@ -63,38 +63,6 @@ __device__ void accept_role(const SelectArgs& a, int acta, int nacta) {
   }
 }
 
-// Warp 0: the digit holding the need-th undecided cell of histogram h[0..2048).  Lane l owns bins [64l, 64l+64)
-// (loaded in a rotated order so 8 consecutive lanes hit 8 distinct bank groups); a warp scan of the lane totals finds
-// the owning 64-bin block, then the whole warp scans that block (2 bins per lane) to find the bin.  Also returns
-// the histogram total.  Counts fit 32 bits (at most 16384 cells).
-__device__ __forceinline__ void pick_digit_warp(const uint32_t* h, uint32_t need, int lane, int* digit,
-                                                long long* need_out, int* done, uint32_t* total) {
-  const uint4* h4 = reinterpret_cast<const uint4*>(h) + lane * 16;
-  uint32_t s = 0;
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    const uint4 x = h4[(c + lane) & 15];
-    s += x.x + x.y + x.z + x.w;
-  }
-  const uint32_t incl = warp_incl_scan<uint32_t>(s, lane);
-  *total = __shfl_sync(kFull, incl, 31);
-  const unsigned own = __ballot_sync(kFull, incl - s < need && need <= incl);
-  const int ol = own ? __ffs(own) - 1 : 0;
-  const uint32_t before = __shfl_sync(kFull, incl - s, ol);  // cells in blocks before the owning block
-  const uint2 b2 = reinterpret_cast<const uint2*>(h)[ol * 32 + lane];  // bins 64*ol + 2*lane, +1
-  const uint32_t pair = b2.x + b2.y;
-  const uint32_t pin = warp_incl_scan<uint32_t>(pair, lane) + before;
-  const uint32_t pex = pin - pair;
-  const unsigned hit = __ballot_sync(kFull, own != 0 && pex < need && need <= pin);
-  if (hit && lane == __ffs(hit) - 1) {
-    const bool first = need <= pex + b2.x;
-    const uint32_t base = first ? pex : pex + b2.x, cnt = first ? b2.x : b2.y;
-    *digit = ol * 64 + 2 * lane + (first ? 0 : 1);
-    *need_out = (long long)(need - base);
-    *done = (need - base == cnt);
-  }
-}
-
 template <int RPT>
 __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];

@@ -483,6 +483,7 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
   sa.cap = cap;
   sa.accepted = accepted;
   sa.rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+  sa.gscratch = abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_GSEL);
   sa.offsets = offsets;
   (void)tokens;  // the accepted-prefix tokens are written by tetris_resample_f32's finalize kernel
   if (!u_packed) {

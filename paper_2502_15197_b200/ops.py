@@ -373,7 +373,7 @@ class TetrisStep:
     all buffers are preallocated, nothing synchronises the host, so `run` can be captured in a CUDA graph."""
 
     def __init__(self, B: int, k: int, V: int, capacity: int, mode: str = "stochastic", device="cuda",
-                 u_layout: str = "dense", group=None, policy: str = "tetris"):
+                 u_layout: str = "dense", group=None, policy: str = "tetris", shard=None):
         if mode not in ("stochastic", "greedy"):
             raise ValueError(f"mode must be 'stochastic' or 'greedy', got {mode!r}")
         if policy not in ("tetris", "fixed"):
@@ -392,6 +392,12 @@ class TetrisStep:
             import torch.distributed as dist
 
             self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        elif shard is not None:
+            # (world, rank) without a process group: the caller hands run() the already gathered [world*B, k] scores
+            # and lengths (single-GPU measurement of one rank's share of a sharded step)
+            self.world, self.rank = int(shard[0]), int(shard[1])
+            if not 0 <= self.rank < self.world:
+                raise ValueError(f"shard rank {self.rank} outside world {self.world}")
         Bg = B * self.world
         self.Bg = Bg
         if self.world > 1:
@@ -423,13 +429,13 @@ class TetrisStep:
         if self.policy == "fixed":
             self._run_fixed(lengths, p, q, d, u_acc, u_res, cap, events, window)
             return
-        if self.world > 1:
+        if self.world > 1 and self.group is not None:
             import torch.distributed as dist
 
             dist.all_gather_into_tensor(self.conf_all, conf, group=self.group)
             dist.all_gather_into_tensor(self.len_all, lengths, group=self.group)
             sel_conf, sel_len = self.conf_all, self.len_all
-        else:
+        else:  # world 1, or a shard given the gathered scores directly
             sel_conf, sel_len = conf, lengths
         if self.mode == "stochastic":
             # == tetris_step_stochastic_f32, called as its two halves so an event can sit between the kernels
