@@ -19,18 +19,46 @@ inline int fail(int code, const char* fmt, ...) {
   return code;
 }
 
-inline int cuda_fail(cudaError_t e) { return fail(TETRIS_CUDA_ERROR, "CUDA error: %s", cudaGetErrorString(e)); }
+// the call site (file:line of the ABI code) is part of the message, so a failing launch can be located
+inline int cuda_fail(cudaError_t e, const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
+  const char* base = file;
+  for (const char* c = file; *c; ++c)
+    if (*c == '/') base = c + 1;
+  return fail(TETRIS_CUDA_ERROR, "CUDA error: %s (%s:%d)", cudaGetErrorString(e), base, line);
+}
 
-inline int launch_check() {
+inline int launch_check(const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e);
+  if (e != cudaSuccess) return cuda_fail(e, file, line);
   return TETRIS_OK;
 }
 
+// Raise the kernel's dynamic shared-memory limit to `bytes` when needed.  The 48 KB default covers static + dynamic
+// together, so any dynamic size is set explicitly (a kernel with 17 KB of static shared memory fails to launch with
+// 40 KB dynamic otherwise); the largest size set so far per kernel is remembered to skip redundant driver calls.
 template <typename K>
 inline cudaError_t ensure_smem(K kernel, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  struct Entry {
+    const void* fn;
+    size_t max;
+  };
+  static Entry table[64];
+  const void* fn = reinterpret_cast<const void*>(kernel);
+  int slot = -1;
+  for (int i = 0; i < 64; ++i) {
+    if (table[i].fn == fn) {
+      if (table[i].max >= bytes) return cudaSuccess;
+      slot = i;
+      break;
+    }
+    if (table[i].fn == nullptr) {
+      slot = i;
+      break;
+    }
+  }
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && slot >= 0) table[slot] = Entry{fn, bytes};
+  return e;
 }
 
 enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_END };
