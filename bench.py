@@ -201,6 +201,12 @@ def run_tetris(args):
     # rotate enough input sets that consecutive steps never find their inputs in L2 (126 MB on B200)
     set_bytes = B_local * ((k + 1) + k) * V * 4
     nsets = max(args.sets, -(-2 * 126 * 2**20 // set_bytes))
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    if nsets * set_bytes > 0.9 * free_b:
+        nsets = max(1, int(0.9 * free_b // set_bytes))  # one set larger than L2 already defeats caching
+    if set_bytes > 0.9 * free_b:
+        raise SystemExit(f"{args.config}: {set_bytes / 1e9:.1f} GB of p/q per rank does not fit this GPU "
+                         f"({free_b / 1e9:.1f} GB free); shard it over more GPUs (--gpus N under torchrun)")
     sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
             for s in range(nsets)]
     step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None,
