@@ -29,6 +29,8 @@ CONFIGS = {
     "cfg1": dict(B=16, k=5, C=48, V=32000, mode="greedy"),
     "cfg2": dict(B=256, k=8, C=1024, V=32000, mode="stochastic"),
     "cfg3": dict(B=1024, k=16, C=8192, V=128256, mode="stochastic"),
+    # cfg3 shape with greedy verification (not a BASELINE config; measures the greedy kernel at scale)
+    "cfg3g": dict(B=1024, k=16, C=8192, V=128256, mode="greedy"),
     # cfg4: selection-only capacity sweep (BASELINE.json configs[3]); timed by run_select_sweep
     "cfg4": dict(B=4096, k=16, C=None, V=32000, mode="select", sweep=(4096, 8192, 16384, 32768, 65536)),
     # cfg5: B=16384 requests sharded over the GPUs (strong scaling), C assumed B*8

@@ -61,7 +61,7 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes) {
   return e;
 }
 
-enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_END };
+enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP, WS_END };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -80,7 +80,7 @@ static_assert(kSlotWorkCounter == kSlotGridCount + 2 && (kSlotWorkCounter % 2) =
 
 inline size_t region_offset(int op, int B, int k, int V, Region which) {
   const size_t nch = (size_t)((V + TETRIS_CHUNK_ELEMS - 1) / TETRIS_CHUNK_ELEMS);
-  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   sizes[WS_COUNTERS] = kCounterSlots * 4;
   sizes[WS_GSEL] = kGselScratchBytes;  // shape-independent, right after the counters: a fixed offset in every layout
   if (op & TETRIS_OP_SELECT) {
@@ -96,9 +96,10 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
     sizes[WS_SCRATCH] = align_up((size_t)B * 8) * 3 + align_up((size_t)B * 4);  // residual: rows, u, idx
     sizes[WS_ROWINFO] = (size_t)B * 16;  // accept result: row to resample from (p row, q row)
     sizes[WS_ACCBYTES] = (size_t)B * k;  // pre-accept verdicts
+    sizes[WS_ROWMAP] = 256 + (size_t)B * (k + 1) * 4;  // greedy: [0] selected-row count, then row -> (b, j)
   }
   const Region order[WS_END] = {WS_COUNTERS, WS_GSEL, WS_KEYS,    WS_CHUNK_SUMS, WS_WARP_SUMS,
-                                WS_ARG_VAL,  WS_ARG_IDX, WS_SCRATCH,    WS_ROWINFO, WS_ACCBYTES};
+                                WS_ARG_VAL,  WS_ARG_IDX, WS_SCRATCH,    WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP};
   size_t off = 0;
   for (int i = 0; i < WS_END; ++i) {
     if (order[i] == which) return off;

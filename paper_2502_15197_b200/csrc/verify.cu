@@ -223,12 +223,43 @@ __device__ __forceinline__ bool arg_better(float av, int ai, float bv, int bi) {
   return ai < bi;
 }
 
+// The rows greedy verification reads — positions 0..w_b of every request, w_b clamped to [0, k] — listed in request
+// order: rowmap[1 + r] = b << 8 | j, rowmap[0] = their count (one CTA; each thread a contiguous block of requests).
+__global__ void __launch_bounds__(1024, 1)
+    greedy_rowmap_kernel(const int32_t* __restrict__ windows, int B, int k, int32_t* __restrict__ rowmap) {
+  __shared__ long long s_tmp[33];
+  const int tid = threadIdx.x;
+  const int R = (B + blockDim.x - 1) / blockDim.x;
+  const int r0 = min(B, tid * R), r1 = min(B, r0 + R);
+  long long local = 0;
+  for (int b = r0; b < r1; ++b) {
+    const int w = windows[b];
+    local += (w < 0 ? 0 : (w > k ? k : w)) + 1;
+  }
+  long long total;
+  long long off = block_excl_scan<long long>(local, s_tmp, total);
+  for (int b = r0; b < r1; ++b) {
+    int w = windows[b];
+    w = w < 0 ? 0 : (w > k ? k : w);
+    for (int j = 0; j <= w; ++j) rowmap[1 + off + j] = (b << 8) | j;
+    off += w + 1;
+  }
+  if (tid == 0) rowmap[0] = (int32_t)total;
+}
+
+// Greedy verify: grid (chunks, selected rows): one CTA per (row chunk) of the rows listed by greedy_rowmap_kernel (no
+// empty CTAs for the positions beyond a request's window); the last CTA of a request to finish combines the argmaxes.
 template <bool VEC>
 __global__ void __launch_bounds__(kStreamThreads)
     greedy_kernel(const float* __restrict__ p, const int32_t* __restrict__ d, const int32_t* __restrict__ windows,
                   int k, int V, int32_t* __restrict__ accepted, int32_t* __restrict__ out_tok, uint32_t* status,
-                  int* __restrict__ counters, float* __restrict__ arg_val, int32_t* __restrict__ arg_idx) {
-  const int c = blockIdx.x, j = blockIdx.y, b = blockIdx.z, nch = gridDim.x;
+                  int* __restrict__ counters, float* __restrict__ arg_val, int32_t* __restrict__ arg_idx,
+                  const int32_t* __restrict__ rowmap) {
+  const int nch = n_chunks(V);
+  const int y = (int)(blockIdx.x / nch), c = (int)(blockIdx.x - (unsigned)y * nch);
+  if (y >= __ldg(rowmap)) return;
+  const int rm = __ldg(rowmap + 1 + y);
+  const int j = rm & 0xFF, b = rm >> 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float s_v[kChunkWarps];
   __shared__ int s_i[kChunkWarps];
@@ -237,26 +268,38 @@ __global__ void __launch_bounds__(kStreamThreads)
   int w = windows[b];
   const bool bad_w = (w < 0 || w > k);
   w = w < 0 ? 0 : (w > k ? k : w);
-  if (j > w) return;
 
   const float* row = p + ((int64_t)b * (k + 1) + j) * V;
   const int64_t e0 = (int64_t)c * kChunkElems + warp * kWarpElems;
   float v[kWarpSegs][8];
 #pragma unroll
   for (int s = 0; s < kWarpSegs; ++s) load_lane<float, VEC>(row, e0 + s * kSegElems + lane * kLaneElems, V, v[s]);
-  float bv = 0.f;
-  int bi = INT_MAX;
+  // lane argmax in two cheap passes (the per-element numpy-order comparison made this kernel issue-bound): the
+  // NaN-propagating max of the lane's 32 elements, then the first element equal to it (a NaN max matches the first
+  // NaN) — numpy.argmax order.  Elements past V are -inf and lose every tie on index.
+  const float kNegInf = __int_as_float(0xff800000);
+  float bv = kNegInf;
 #pragma unroll
   for (int s = 0; s < kWarpSegs; ++s) {
     const int64_t e = e0 + s * kSegElems + lane * kLaneElems;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (e + i < V && arg_better(v[s][i], (int)(e + i), bv, bi)) {
-        bv = v[s][i];
-        bi = (int)(e + i);
-      }
+      if (e + i >= V) v[s][i] = kNegInf;
+      asm("max.NaN.f32 %0, %0, %1;" : "+f"(bv) : "f"(v[s][i]));
     }
   }
+  const bool bnan = bv != bv;
+  int bi = INT_MAX;
+#pragma unroll
+  for (int s = kWarpSegs - 1; s >= 0; --s) {
+    const int e = (int)(e0 + s * kSegElems + lane * kLaneElems);
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      const bool hit = bnan ? (v[s][i] != v[s][i]) : (v[s][i] == bv);
+      bi = hit ? e + i : bi;
+    }
+  }
+  if (bi >= V) bi = INT_MAX;  // only padding in this lane
 #pragma unroll
   for (int m = 16; m > 0; m >>= 1) {
     const float ov = __shfl_xor_sync(kFull, bv, m);
@@ -563,16 +606,23 @@ extern "C" int tetris_verify_greedy_f32(const float* p, const int32_t* d, const 
   if (!p || !d || !windows || !accepted || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   const bool vec = (V % 8 == 0) && aligned32(p);
-  dim3 grid(n_chunks(V), k + 1, B);
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   float* av = (float*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_VAL);
   int32_t* ai = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_IDX);
+  int32_t* rowmap = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWMAP);
   cudaStream_t st = (cudaStream_t)stream;
+  greedy_rowmap_kernel<<<1, 1024, 0, st>>>(windows, B, k, rowmap);
+  if ((rc = abi::launch_check())) return rc;
+  // one CTA per (selected row, chunk); the selected-row count Σ (w_b + 1) lives on the device, so the grid covers
+  // the bound B * (k + 1) and CTAs past the count exit at once
+  const long long rows_max = (long long)B * (k + 1);
+  dim3 grid((unsigned)(rows_max * n_chunks(V)), 1, 1);
   if (vec)
-    greedy_kernel<true><<<grid, kStreamThreads, 0, st>>>(p, d, windows, k, V, accepted, out_tok, status, cnt, av, ai);
+    greedy_kernel<true><<<grid, kStreamThreads, 0, st>>>(p, d, windows, k, V, accepted, out_tok, status, cnt, av, ai,
+                                                         rowmap);
   else
     greedy_kernel<false><<<grid, kStreamThreads, 0, st>>>(p, d, windows, k, V, accepted, out_tok, status, cnt, av,
-                                                          ai);
+                                                          ai, rowmap);
   return abi::launch_check();
 }
 
