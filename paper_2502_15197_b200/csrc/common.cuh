@@ -70,12 +70,18 @@ __device__ __forceinline__ double w_res(double p, double q) {
   return x > 0.0 ? x : 0.0;
 }
 __device__ __forceinline__ double w_plain(double p) { return p > 0.0 ? p : 0.0; }
+// The same weights from fp32 inputs with the sign test in fp32: (double)p - (double)q > 0 exactly when p > q (both
+// widenings are exact and the fp64 difference of two distinct floats never rounds to zero), NaN compares false.
+// Saves the fp64-pipe compare per element in the streaming consumers.
+__device__ __forceinline__ double w_res32(float p, float q) { return p > q ? (double)p - (double)q : 0.0; }
+__device__ __forceinline__ double w_plain32(float p) { return p > 0.f ? (double)p : 0.0; }
 
-// Left-to-right fold over the 8 lane elements.
+// Left-to-right fold over the 8 lane elements (the contract's ((0 + w0) + w1) + ...; weights are +0.0 or positive,
+// never -0.0, so 0 + w0 == w0 exactly and the fold starts from w0).
 __device__ __forceinline__ double fold8(const double (&w)[8]) {
-  double o = 0.0;
+  double o = w[0];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) o = o + w[i];
+  for (int i = 1; i < 8; ++i) o = o + w[i];
   return o;
 }
 

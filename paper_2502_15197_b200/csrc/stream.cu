@@ -69,10 +69,10 @@ __device__ __forceinline__ double consume_segment(const float* __restrict__ sp, 
       float qv[8];
       lds8_swz(sq + off, lane, qv);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = w_res((double)pv[i], (double)qv[i]);
+      for (int i = 0; i < 8; ++i) w[i] = w_res32(pv[i], qv[i]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = w_plain((double)pv[i]);
+      for (int i = 0; i < 8; ++i) w[i] = w_plain32(pv[i]);
     }
   } else {
 #pragma unroll
