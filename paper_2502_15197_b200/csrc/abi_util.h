@@ -4,6 +4,8 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <mutex>
+
 #include "tetris_b200.h"
 
 namespace tetris {
@@ -43,6 +45,8 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes) {
     size_t max;
   };
   static Entry table[64];
+  static std::mutex mu;  // host threads may launch concurrently (the ABI is reentrant)
+  std::lock_guard<std::mutex> lock(mu);
   const void* fn = reinterpret_cast<const void*>(kernel);
   int slot = -1;
   for (int i = 0; i < 64; ++i) {
