@@ -335,7 +335,9 @@ def run_tetris(args):
             "select_verify_latency_us": 1e3 * statistics.median([a + b for a, b in zip(sel_ms, ver_ms)]),
             "tokens_per_step": total_tokens / args.steps,
             "roofline": {"bound": "hbm", "kernel": "persist_stream_kernel (tetris_resample_f32: streaming + per-"
-                         "request descent in the same launch; CUDA events around the launch, eager pass)" if mode == "stochastic" else "greedy_kernel", "achieved": achieved, "peak": peak,
+                         "request descent in the same launch; CUDA events around the launch, eager pass)" if mode == "stochastic"
+                         else "greedy_rowmap_kernel + persist_greedy_kernel (tetris_verify_greedy_compact_f32: argmax "
+                         "stream + verdicts + compaction in one launch; CUDA events around the call, eager pass)", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "alg_bytes_per_launch": alg_bytes / args.steps,
                          "traffic": _load_traffic(args.config)},

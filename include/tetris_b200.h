@@ -168,6 +168,12 @@ int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B
 int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B, int32_t k,
                              int32_t V, int32_t* accepted, int32_t* out_tok, uint32_t* status, void* ws,
                              size_t ws_bytes, tetris_stream_t stream);
+/* The same verification with the compaction of tetris_compact fused into its launch (offsets[B+1], tokens; cap
+ * nullable): the greedy product path is 2 launches after the selection (row list, persistent argmax stream). */
+int tetris_verify_greedy_compact_f32(const float* p, const int32_t* d, const int32_t* windows, const int32_t* cap,
+                                     int32_t B, int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
+                                     int32_t* offsets, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
+                                     tetris_stream_t stream);
 
 /* Row sampler (the building block of the above, exposed for the token-level adapters):
  * for r < R: weights = max(0, p[p_row[r]] - q[q_row[r]]) if q != NULL and q_row[r] >= 0, else max(0, p[p_row[r]]);

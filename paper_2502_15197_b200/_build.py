@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC",
     "-I", str(INCLUDE),
 ]
-SOURCES = ["abi.cu", "select.cu", "select1.cu", "gselect.cu", "verify.cu", "stream.cu", "compact.cu", "sim.cu"]
+SOURCES = ["abi.cu", "select.cu", "select1.cu", "gselect.cu", "verify.cu", "stream.cu", "greedy.cu", "compact.cu", "sim.cu"]
 
 
 def _nvcc() -> str:

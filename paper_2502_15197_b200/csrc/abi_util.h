@@ -95,7 +95,7 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
     // rows processed by one verify call: B requests (stochastic/greedy) or R sampled rows (sample_rows)
     sizes[WS_CHUNK_SUMS] = (size_t)B * nch * 8;
     sizes[WS_WARP_SUMS] = (size_t)B * nch * TETRIS_CHUNK_WARPS * 8;
-    sizes[WS_ARG_VAL] = (size_t)B * (k + 1) * nch * 4;
+    sizes[WS_ARG_VAL] = (size_t)B * (k + 1) * (nch > 1 ? nch : 2) * 4;  // also the greedy argmax keys (8 B per row)
     sizes[WS_ARG_IDX] = (size_t)B * (k + 1) * nch * 4;
     sizes[WS_SCRATCH] = align_up((size_t)B * 8) * 3 + align_up((size_t)B * 4);  // residual: rows, u, idx
     sizes[WS_ROWINFO] = (size_t)B * 16;  // accept result: row to resample from (p row, q row)

@@ -1,0 +1,404 @@
+// Stage (3) greedy verification as a persistent, warp-specialised TMA stream (sm_100a, fp32 rows, V % 8 == 0),
+// with the compaction of stage (4) fused into the same launch.
+//
+// Greedy verification is verify_token on one-hot distributions (accept_model.py:309-313): position j of request b is
+// accepted iff d[b][j] == argmax_v p[b][j][v] (numpy.argmax order: NaN ranks highest, ties -> lowest index), and the
+// emitted token is the argmax at the first mismatch, or at w_b (the bonus position, sim_engine.py:407-409).  Every
+// selected row 0..w_b is read in full once: HBM-bound, (Σ_b (w_b + 1)) · V · 4 bytes per call.
+//
+// greedy_rowmap_kernel (one CTA) lists those rows in request order and zeroes their argmax keys; then
+// persist_greedy_kernel, one CTA per SM, 18 warps:
+//   warp 16     producer: takes items (listed row, chunk) in order from one global counter and issues 1-D bulk copies
+//               (cp.async.bulk, mbarrier complete_tx) of 8192-element chunks of p into a 6-stage 192 KB ring;
+//   warps 0..15 consumers: the argmax key of 512 staged elements each (two segments), reduced over the warp;
+//   warp 17     publisher: reduces the 16 keys of a chunk, folds it into the row's key with one atomicMax, and counts
+//               the chunk on the request's arrival counter (one release fence per 32 chunks).
+// The argmax travels as one 64-bit key whose unsigned order is numpy's: high word = the value's bits mapped to an
+// unsigned order (NaN above +inf, -0.0 canonicalised to +0.0), low word = ~index (lower index wins a tie).
+// Then, in the same launch, one warp per request (strided over the CTAs) waits for the request's (w_b + 1) · nch
+// chunks, reads the w_b + 1 keys and writes accepted / out_tok; the last CTA out runs the compaction (offsets and
+// tokens, compact_kernel's contract) when asked to.
+#include "common.cuh"
+#include "launch.h"
+
+namespace tetris {
+
+namespace {
+
+constexpr int kGStages = 6;
+constexpr int kGConsumers = 16;
+constexpr int kSegsPerWarp = kChunkElems / kSegElems / kGConsumers;  // staged segments per consumer warp
+constexpr int kGProducer = kGConsumers;
+constexpr int kGPublisher = kGConsumers + 1;
+constexpr int kGThreads = (kGConsumers + 2) * 32;
+constexpr int kGRing = 64;
+constexpr int kClaim = 4;  // work items (row chunks) per claim on the global counter
+constexpr size_t kGStageBytes = (size_t)kChunkElems * sizeof(float);  // 32 KB
+constexpr size_t kGSmem = kGStages * kGStageBytes;                    // 192 KB dynamic
+static_assert(kSegsPerWarp * kGConsumers * kSegElems == kChunkElems, "consumers split a chunk evenly");
+
+struct GMeta {
+  int b, row, c, pad;  // request, row index b*(k+1)+j, chunk
+};
+
+struct GreedyShared {
+  uint64_t full[kGStages];
+  uint64_t empty[kGStages];
+  uint64_t ring_full[kGRing];
+  uint64_t ring_free[kGRing];
+  GMeta meta[kGStages];
+  GMeta ring_meta[kGRing];
+  unsigned long long ring_key[kGRing][kGConsumers];
+};
+
+// numpy.argmax order of a value as an unsigned 32-bit word (larger wins): NaN above +inf, -0.0 equal to +0.0.
+__device__ __forceinline__ uint32_t argmax_order(float v) {
+  if (v != v) return 0xFFFFFFFFu;
+  if (v == 0.f) v = 0.f;
+  const uint32_t bits = __float_as_uint(v);
+  return (bits >> 31) ? ~bits : (bits | 0x80000000u);
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(kFull, x, m);
+    x = y > x ? y : x;
+  }
+  return x;
+}
+
+// The warp's argmax key over its SEGS staged segments (lane l: elements seg*256 + 8l .. +8 of each), as one 64-bit
+// word whose unsigned order is numpy.argmax's: high word argmax_order(value), low word ~index (lower index wins a
+// tie); 0 = no element.  Per element: one NaN-propagating max, then one compare + select for the first index equal
+// to it; NaN rows take a separate (warp-uniform, rare) branch.  Elements at or past V (only in the row's last chunk)
+// are read as -inf: they lose every comparison to a real element of the chunk, which always has one (V % 8 == 0).
+template <int SEGS>
+__device__ __forceinline__ unsigned long long warp_argmax(const float* __restrict__ sp, int chunk_e0, int seg0,
+                                                          bool partial, int V, int lane) {
+  float v[SEGS][8];
+#pragma unroll
+  for (int x = 0; x < SEGS; ++x) lds8_swz(sp + (seg0 + x) * kSegElems + lane * kLaneElems, lane, v[x]);
+  const float kNegInf = __int_as_float(0xff800000);
+  if (partial) {
+#pragma unroll
+    for (int x = 0; x < SEGS; ++x)
+      if (chunk_e0 + (seg0 + x) * kSegElems + lane * kLaneElems >= V) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[x][i] = kNegInf;
+      }
+  }
+  float bv = v[0][0];
+#pragma unroll
+  for (int x = 0; x < SEGS; ++x)
+#pragma unroll
+    for (int i = (x == 0 ? 1 : 0); i < 8; ++i) asm("max.NaN.f32 %0, %0, %1;" : "+f"(bv) : "f"(v[x][i]));
+  int bl = 0;  // local position x * 8 + i of the first element equal to the max
+  if (__any_sync(kFull, bv != bv)) {
+    const bool nan = bv != bv;
+#pragma unroll
+    for (int x = SEGS - 1; x >= 0; --x)
+#pragma unroll
+      for (int i = 7; i >= 0; --i) bl = (nan ? (v[x][i] != v[x][i]) : (v[x][i] == bv)) ? x * 8 + i : bl;
+  } else {
+#pragma unroll
+    for (int x = SEGS - 1; x >= 0; --x)
+#pragma unroll
+      for (int i = 7; i >= 0; --i) bl = (v[x][i] == bv) ? x * 8 + i : bl;
+  }
+  const uint32_t idx = (uint32_t)(chunk_e0 + (seg0 + (bl >> 3)) * kSegElems + lane * kLaneElems + (bl & 7));
+  const uint32_t hi = argmax_order(bv);
+  const uint32_t whi = __reduce_max_sync(kFull, hi);
+  const uint32_t widx = __reduce_min_sync(kFull, hi == whi ? idx : 0xFFFFFFFFu);
+  return ((unsigned long long)whi << 32) | (uint32_t)~widx;
+}
+
+}  // namespace
+
+// Rows read by greedy verification — positions 0..w_b of every request, w_b clamped to [0, k] — in request order:
+// rowmap[1 + r] = b << 8 | j, rowmap[0] = their count; the argmax key of each listed row is zeroed (keys != nullptr).
+// One CTA; each thread a contiguous block of requests.  Launched as a programmatic dependent of the selector.
+__global__ void __launch_bounds__(1024, 1)
+    greedy_rowmap_kernel(const int32_t* __restrict__ windows, int B, int k, int32_t* __restrict__ rowmap,
+                         unsigned long long* __restrict__ keys) {
+  __shared__ long long s_tmp[33];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int tid = threadIdx.x;
+  const int R = (B + blockDim.x - 1) / blockDim.x;
+  const int r0 = min(B, tid * R), r1 = min(B, r0 + R);
+  long long local = 0;
+  for (int b = r0; b < r1; ++b) {
+    const int w = windows[b];
+    local += (w < 0 ? 0 : (w > k ? k : w)) + 1;
+  }
+  long long total;
+  long long off = block_excl_scan<long long>(local, s_tmp, total);
+  for (int b = r0; b < r1; ++b) {
+    int w = windows[b];
+    w = w < 0 ? 0 : (w > k ? k : w);
+    for (int j = 0; j <= w; ++j) {
+      rowmap[1 + off + j] = (b << 8) | j;
+      if (keys) keys[(int64_t)b * (k + 1) + j] = 0ull;
+    }
+    off += w + 1;
+  }
+  if (tid == 0) rowmap[0] = (int32_t)total;
+}
+
+__global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const GreedyArgs a) {
+  extern __shared__ __align__(128) uint8_t stage_mem[];
+  __shared__ GreedyShared sh;
+  __shared__ long long s_tmp[33];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nch = a.nch, V = a.V, k = a.k;
+  const int G = gridDim.x;
+  unsigned long long* work = reinterpret_cast<unsigned long long*>(a.grid_bar + 2);
+
+  if (tid == 0) {
+    for (int s = 0; s < kGStages; ++s) {
+      mbar_init(&sh.full[s], 1);
+      mbar_init(&sh.empty[s], kGConsumers);
+    }
+    for (int r = 0; r < kGRing; ++r) {
+      mbar_init(&sh.ring_full[r], kGConsumers);
+      mbar_init(&sh.ring_free[r], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // programmatic dependent of the row-map kernel: wait for it (and its memory) before reading the row list
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == kGProducer) {
+    if (lane == 0) {
+      const long long total = (long long)__ldcg(a.rowmap) * nch;
+      // Items are claimed kClaim at a time, one claim ahead: the counter's and the row map's round trips (each up to
+      // ~1 us under full HBM load) overlap the copies of a whole claim instead of one 32 KB chunk each.
+      long long c_cur = (long long)atomicAdd(work, (unsigned long long)kClaim);
+      int rm_cur[kClaim], rm_nx[kClaim];
+#pragma unroll
+      for (int x = 0; x < kClaim; ++x) rm_cur[x] = c_cur + x < total ? __ldcg(a.rowmap + 1 + (c_cur + x) / nch) : 0;
+      int t = 0;
+      while (c_cur < total) {
+        const long long c_next = (long long)atomicAdd(work, (unsigned long long)kClaim);
+#pragma unroll
+        for (int x = 0; x < kClaim; ++x) {
+          const long long i = c_cur + x;
+          if (x == 1) {  // one copy issued: fetch the next claim's rows (waits for the counter's reply)
+#pragma unroll
+            for (int y = 0; y < kClaim; ++y)
+              rm_nx[y] = c_next + y < total ? __ldcg(a.rowmap + 1 + (c_next + y) / nch) : 0;
+          }
+          if (i < total) {
+            const int s = t % kGStages;
+            if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
+            const int rm = rm_cur[x];
+            const int b = rm >> 8, j = rm & 0xFF, cc = (int)(i % nch);
+            const int row = b * (k + 1) + j;
+            const int n = min(kChunkElems, V - cc * kChunkElems);
+            const uint32_t bytes = (uint32_t)n * sizeof(float);
+            sh.meta[s] = GMeta{b, row, cc, 0};
+            mbar_arrive_expect_tx(&sh.full[s], bytes);
+            bulk_g2s(stage_mem + s * kGStageBytes, a.p + (int64_t)row * V + (int64_t)cc * kChunkElems, bytes,
+                     &sh.full[s]);
+            ++t;
+          }
+        }
+        c_cur = c_next;
+#pragma unroll
+        for (int x = 0; x < kClaim; ++x) rm_cur[x] = rm_nx[x];
+      }
+      // end of stream: a sentinel stage without data
+      const int s = t % kGStages;
+      if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
+      sh.meta[s] = GMeta{-1, 0, 0, 0};
+      mbar_arrive(&sh.full[s]);
+    }
+    __syncwarp();
+  } else if (warp < kGConsumers) {
+    for (int t = 0;; ++t) {
+      const int s = t % kGStages;
+      mbar_wait(&sh.full[s], (uint32_t)((t / kGStages) & 1));
+      const GMeta m = sh.meta[s];
+      const int slot = t % kGRing;
+      if (t >= kGRing) mbar_wait(&sh.ring_free[slot], (uint32_t)(((t / kGRing) & 1) ^ 1));
+      if (m.b < 0) {  // forward the end of stream to the publisher
+        if (lane == 0) {
+          if (warp == 0) sh.ring_meta[slot] = m;
+          mbar_arrive(&sh.ring_full[slot]);
+        }
+        break;
+      }
+      const float* sp = reinterpret_cast<const float*>(stage_mem + s * kGStageBytes);
+      const int e0 = m.c * kChunkElems;
+      const unsigned long long key =
+          warp_argmax<kSegsPerWarp>(sp, e0, kSegsPerWarp * warp, e0 + kChunkElems > V, V, lane);
+      if (lane == 0) {
+        mbar_arrive(&sh.empty[s]);  // the staged data has been read
+        sh.ring_key[slot][warp] = key;
+        if (warp == 0) sh.ring_meta[slot] = m;
+        mbar_arrive(&sh.ring_full[slot]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // publisher: one chunk per iteration; arrivals on the per-request counters batched behind one release fence
+    int pend_b = 0, npend = 0;
+    auto flush = [&]() {
+      if (npend == 0) return;
+      __syncwarp();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (lane < npend) atomicAdd(a.req_cnt + pend_b, 1);
+      npend = 0;
+    };
+    for (int t = 0;; ++t) {
+      const int slot = t % kGRing;
+      mbar_wait(&sh.ring_full[slot], (uint32_t)((t / kGRing) & 1));
+      const GMeta m = sh.ring_meta[slot];
+      if (m.b < 0) break;
+      unsigned long long key = lane < kGConsumers ? sh.ring_key[slot][lane] : 0ull;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.ring_free[slot]);
+      key = warp_max_u64(key);
+      if (lane == 0) atomicMax(a.keys + m.row, key);
+      if (lane == npend) pend_b = m.b;
+      if (++npend == 32) flush();
+    }
+    flush();
+  }
+
+  // one warp per request as soon as its (w_b + 1) * nch chunks are in
+  __syncthreads();
+  constexpr int kWarps = kGThreads / 32;
+  for (int b = warp * G + blockIdx.x; b < a.B; b += G * kWarps) {
+    int w = a.windows[b];
+    uint32_t bad = (w < 0 || w > k) ? TETRIS_ST_BAD_WINDOW : 0u;
+    w = w < 0 ? 0 : (w > k ? k : w);
+    if (lane == 0) {
+      const int need = (w + 1) * nch;
+      int seen;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.req_cnt + b) : "memory");
+        if (seen >= need) break;
+        __nanosleep(64);
+      }
+      a.req_cnt[b] = 0;  // every arrival is in: ready for the next launch
+    }
+    __syncwarp();
+    const unsigned long long* kb = a.keys + (int64_t)b * (k + 1);
+    int acc = w, tok = -1;
+    for (int j0 = 0; j0 <= w; j0 += 32) {
+      const int j = j0 + lane;
+      const int am = j <= w ? (int)~(uint32_t)__ldcg(kb + j) : -1;
+      const int t = j < w ? a.d[(int64_t)b * k + j] : 0;
+      const unsigned mis = __ballot_sync(kFull, j < w && t != am);
+      if (mis) {
+        const int l = __ffs(mis) - 1;
+        acc = j0 + l;
+        tok = __shfl_sync(kFull, am, l);
+        const int tl = __shfl_sync(kFull, t, l);
+        if (tl < 0 || tl >= V) bad |= TETRIS_ST_BAD_TOKEN;
+        break;
+      }
+      if (w < j0 + 32) tok = __shfl_sync(kFull, am, w - j0);  // all accepted: the bonus position's argmax
+    }
+    if (lane == 0) {
+      a.accepted[b] = acc;
+      a.out_tok[b] = tok;
+      set_status(a.status, bad);
+    }
+  }
+
+  // the last CTA out resets the work counter and, when asked to, compacts the emitted tokens
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* done = a.grid_bar;
+    const bool last = atomicAdd(done, 1u) == (unsigned)G - 1;
+    if (last) {
+      *work = 0ull;
+      *done = 0u;
+      __threadfence();
+    }
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last || a.offsets == nullptr) return;
+  // compact_kernel's contract: n_b = accepted[b] + 1 (capped), offsets = exclusive scan, tokens = d[b][0..a) ++ [x]
+  const int B = a.B;
+  const int R = (B + blockDim.x - 1) / blockDim.x;
+  const int r0 = min(B, tid * R), r1 = min(B, r0 + R);
+  long long local = 0;
+  for (int r = r0; r < r1; ++r) {
+    int n = __ldcg(a.accepted + r) + 1;
+    if (a.cap) n = min(n, max(a.cap[r], 0));
+    local += n;
+  }
+  long long total;
+  long long off = block_excl_scan<long long>(local, s_tmp, total);
+  for (int r = r0; r < r1; ++r) {
+    const int acc = __ldcg(a.accepted + r);
+    int n = acc + 1;
+    if (a.cap) n = min(n, max(a.cap[r], 0));
+    a.offsets[r] = (int32_t)off;
+    const int x = __ldcg(a.out_tok + r);
+    for (int i = 0; i < n; ++i) a.tokens[off + i] = i < acc ? a.d[(int64_t)r * k + i] : x;
+    off += n;
+  }
+  if (tid == 0) a.offsets[B] = (int32_t)total;
+}
+
+}  // namespace tetris
+
+// ---- host side ---------------------------------------------------------------------------------------------------
+#include "abi_util.h"
+
+namespace tetris {
+
+bool persist_greedy_eligible(const float* p, int V) {
+  return (V % kLaneElems == 0) && (((uintptr_t)p & 15u) == 0);
+}
+
+static int launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) return abi::cuda_fail(e);
+  return abi::launch_check();
+}
+
+int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys,
+                         cudaStream_t st) {
+  void* args[] = {(void*)&windows, (void*)&B, (void*)&k, (void*)&rowmap, (void*)&keys};
+  return launch_pdl((const void*)greedy_rowmap_kernel, dim3(1), dim3(1024), 0, st, args);
+}
+
+int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st) {
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    num_sms = n > 0 ? n : 148;
+  }
+  cudaError_t e = abi::ensure_smem((const void*)persist_greedy_kernel, kGSmem);
+  if (e != cudaSuccess) return abi::cuda_fail(e);
+  // the listed-row count lives on the device; the bound B * (k + 1) * nch caps the useful grid
+  const long long items = (long long)a.B * (a.k + 1) * a.nch;
+  const int grid = (int)(items < num_sms ? items : num_sms);
+  GreedyArgs copy = a;
+  void* args[] = {(void*)&copy};
+  return launch_pdl((const void*)persist_greedy_kernel, dim3(grid), dim3(kGThreads), kGSmem, st, args);
+}
+
+}  // namespace tetris

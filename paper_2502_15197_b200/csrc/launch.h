@@ -65,6 +65,24 @@ struct StreamArgs {
                        // launch as each request completes; nullptr -> a separate finalize_kernel launch
 };
 
+// Greedy verification (greedy.cu): the persistent argmax stream over the rows listed by greedy_rowmap_kernel.
+struct GreedyArgs {
+  const float* p;             // [B][k+1][V]
+  const int32_t* d;           // [B][k]
+  const int32_t* windows;     // [B]
+  const int32_t* cap;         // [B] nullable: emitted-token cap of the fused compaction
+  int B, k, V, nch;
+  const int32_t* rowmap;      // [0]: listed-row count, then b << 8 | j
+  unsigned long long* keys;   // [B][k+1] argmax keys of the listed rows (zeroed by the row-map kernel)
+  int* req_cnt;               // [B] per-request published-chunk counters (zero, left at zero)
+  unsigned* grid_bar;         // [0]: CTAs done, [2..3]: 64-bit work counter (zero, left at zero)
+  int32_t* accepted;
+  int32_t* out_tok;
+  int32_t* offsets;           // [B+1] nullable: fused compaction off
+  int32_t* tokens;
+  uint32_t* status;
+};
+
 int launch_select(const SelectArgs& a, cudaStream_t st);
 bool select1_eligible(int B, int k);
 int launch_select1(const SelectArgs& a, cudaStream_t st);  // single-CTA selector (select1.cu)
@@ -72,6 +90,10 @@ int launch_gselect(const SelectArgs& a, void* scratch, cudaStream_t st);  // gri
 size_t gselect_scratch_bytes();
 int launch_persist_stream(const StreamArgs& a, cudaStream_t st);
 bool persist_eligible(const float* p, const float* q, int V);
+bool persist_greedy_eligible(const float* p, int V);
+int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys,
+                         cudaStream_t st);
+int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st);
 int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,
                       int B, int k, int V, uint8_t* acc_bytes, cudaStream_t st);
 int launch_accept(const float* p, const float* q, const int32_t* d, const int32_t* windows, const int32_t* win_off,

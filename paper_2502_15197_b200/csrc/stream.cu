@@ -47,16 +47,6 @@ struct PersistShared {
   double ring_g[kRing][kSegsPerChunk];  // segment sums of each published chunk
 };
 
-// Lane l's 8 elements are two 16-byte halves; lanes with bit 2 set read the upper half first, so each quarter-warp
-// phase of an LDS.128 touches 8 distinct 4-bank groups (no 2-way conflict between lanes l and l+4).
-__device__ __forceinline__ void lds8_swz(const float* p, int lane, float (&v)[8]) {
-  const int sw = (lane >> 2) & 1;
-  const float4 x = *reinterpret_cast<const float4*>(p + 4 * sw);
-  const float4 y = *reinterpret_cast<const float4*>(p + 4 * (1 - sw));
-  const float4 lo = sw ? y : x, hi = sw ? x : y;
-  v[0] = lo.x, v[1] = lo.y, v[2] = lo.z, v[3] = lo.w, v[4] = hi.x, v[5] = hi.y, v[6] = hi.z, v[7] = hi.w;
-}
-
 // Segment sum (lane fold + xor butterfly) of the staged segment at chunk offset `off0` (element e0 of the row).
 __device__ __forceinline__ double consume_segment(const float* __restrict__ sp, const float* __restrict__ sq, bool res,
                                                   int64_t e0, int off0, int V, int lane) {

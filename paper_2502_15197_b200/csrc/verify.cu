@@ -223,31 +223,8 @@ __device__ __forceinline__ bool arg_better(float av, int ai, float bv, int bi) {
   return ai < bi;
 }
 
-// The rows greedy verification reads — positions 0..w_b of every request, w_b clamped to [0, k] — listed in request
-// order: rowmap[1 + r] = b << 8 | j, rowmap[0] = their count (one CTA; each thread a contiguous block of requests).
-__global__ void __launch_bounds__(1024, 1)
-    greedy_rowmap_kernel(const int32_t* __restrict__ windows, int B, int k, int32_t* __restrict__ rowmap) {
-  __shared__ long long s_tmp[33];
-  const int tid = threadIdx.x;
-  const int R = (B + blockDim.x - 1) / blockDim.x;
-  const int r0 = min(B, tid * R), r1 = min(B, r0 + R);
-  long long local = 0;
-  for (int b = r0; b < r1; ++b) {
-    const int w = windows[b];
-    local += (w < 0 ? 0 : (w > k ? k : w)) + 1;
-  }
-  long long total;
-  long long off = block_excl_scan<long long>(local, s_tmp, total);
-  for (int b = r0; b < r1; ++b) {
-    int w = windows[b];
-    w = w < 0 ? 0 : (w > k ? k : w);
-    for (int j = 0; j <= w; ++j) rowmap[1 + off + j] = (b << 8) | j;
-    off += w + 1;
-  }
-  if (tid == 0) rowmap[0] = (int32_t)total;
-}
-
-// Greedy verify: grid (chunks, selected rows): one CTA per (row chunk) of the rows listed by greedy_rowmap_kernel (no
+// Greedy verify fallback (V % 8 != 0 or unaligned p; the product path is persist_greedy_kernel, greedy.cu): grid
+// (chunks, selected rows): one CTA per (row chunk) of the rows listed by greedy_rowmap_kernel (no
 // empty CTAs for the positions beyond a request's window); the last CTA of a request to finish combines the argmaxes.
 template <bool VEC>
 __global__ void __launch_bounds__(kStreamThreads)
@@ -597,33 +574,78 @@ extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len
                              ws_bytes, stream);
 }
 
-extern "C" int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B,
-                                        int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
-                                        uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* windows, const int32_t* cap, int B,
+                              int k, int V, int32_t* accepted, int32_t* out_tok, int32_t* offsets, int32_t* tokens,
+                              uint32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
   int rc = check_shape(B, k, V);
   if (rc) return rc;
-  if (B == 0) return TETRIS_OK;
+  if (B == 0) {
+    if (offsets) {
+      cudaError_t e = cudaMemsetAsync(offsets, 0, sizeof(int32_t), st);
+      if (e != cudaSuccess) return abi::cuda_fail(e);
+    }
+    return TETRIS_OK;
+  }
   if (!p || !d || !windows || !accepted || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (offsets && !tokens) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens is required with offsets");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
-  const bool vec = (V % 8 == 0) && aligned32(p);
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   float* av = (float*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_VAL);
   int32_t* ai = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_IDX);
   int32_t* rowmap = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWMAP);
-  cudaStream_t st = (cudaStream_t)stream;
-  greedy_rowmap_kernel<<<1, 1024, 0, st>>>(windows, B, k, rowmap);
-  if ((rc = abi::launch_check())) return rc;
+  if (persist_greedy_eligible(p, V)) {
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(av);
+    if ((rc = launch_greedy_rowmap(windows, B, k, rowmap, keys, st))) return rc;
+    GreedyArgs a = {};
+    a.p = p;
+    a.d = d;
+    a.windows = windows;
+    a.cap = cap;
+    a.B = B;
+    a.k = k;
+    a.V = V;
+    a.nch = n_chunks(V);
+    a.rowmap = rowmap;
+    a.keys = keys;
+    a.req_cnt = cnt;
+    a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
+    a.accepted = accepted;
+    a.out_tok = out_tok;
+    a.offsets = offsets;
+    a.tokens = tokens;
+    a.status = status;
+    return launch_persist_greedy(a, st);
+  }
+  if ((rc = launch_greedy_rowmap(windows, B, k, rowmap, nullptr, st))) return rc;
   // one CTA per (selected row, chunk); the selected-row count Σ (w_b + 1) lives on the device, so the grid covers
   // the bound B * (k + 1) and CTAs past the count exit at once
   const long long rows_max = (long long)B * (k + 1);
   dim3 grid((unsigned)(rows_max * n_chunks(V)), 1, 1);
-  if (vec)
+  if ((V % 8 == 0) && aligned32(p))
     greedy_kernel<true><<<grid, kStreamThreads, 0, st>>>(p, d, windows, k, V, accepted, out_tok, status, cnt, av, ai,
                                                          rowmap);
   else
     greedy_kernel<false><<<grid, kStreamThreads, 0, st>>>(p, d, windows, k, V, accepted, out_tok, status, cnt, av,
                                                           ai, rowmap);
-  return abi::launch_check();
+  if ((rc = abi::launch_check())) return rc;
+  return offsets ? tetris_compact(accepted, out_tok, d, cap, B, k, offsets, tokens, st) : TETRIS_OK;
+}
+
+extern "C" int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B,
+                                        int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
+                                        uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  return verify_greedy_impl(p, d, windows, nullptr, B, k, V, accepted, out_tok, nullptr, nullptr, status, ws, ws_bytes,
+                            (cudaStream_t)stream);
+}
+
+extern "C" int tetris_verify_greedy_compact_f32(const float* p, const int32_t* d, const int32_t* windows,
+                                                const int32_t* cap, int32_t B, int32_t k, int32_t V,
+                                                int32_t* accepted, int32_t* out_tok, int32_t* offsets,
+                                                int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
+                                                tetris_stream_t stream) {
+  if (!offsets) return abi::fail(TETRIS_INVALID_ARGUMENT, "offsets is required");
+  return verify_greedy_impl(p, d, windows, cap, B, k, V, accepted, out_tok, offsets, tokens, status, ws, ws_bytes,
+                            (cudaStream_t)stream);
 }
 
 extern "C" int tetris_sample_rows_f64(const double* p, const double* q, const int64_t* p_row, const int64_t* q_row,

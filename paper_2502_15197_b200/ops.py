@@ -467,16 +467,14 @@ class TetrisStep:
         self._check(rc)
         if events is not None:
             events[1].record()
-        rc = lib.tetris_verify_greedy_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), B, k, V,
-                                          self.accepted.data_ptr(), self.out_tok.data_ptr(),
-                                          self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        # row list + the persistent argmax stream with the compaction fused into its last CTA
+        rc = lib.tetris_verify_greedy_compact_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), _ptr(cap), B,
+                                                  k, V, self.accepted.data_ptr(), self.out_tok.data_ptr(),
+                                                  self.offsets.data_ptr(), self.tokens.data_ptr(),
+                                                  self.status.data_ptr(), ws.ptr, ws.nbytes, s)
         self._check(rc)
         if events is not None:
             events[2].record()
-        rc = lib.tetris_compact(self.accepted.data_ptr(), self.out_tok.data_ptr(), d.data_ptr(), _ptr(cap), B, k,
-                                self.offsets.data_ptr(), self.tokens.data_ptr(), s)
-        self._check(rc)
-        if events is not None:
             events[3].record()
 
     def _run_fixed(self, lengths, p, q, d, u_acc, u_res, cap, events, window) -> None:
@@ -496,9 +494,14 @@ class TetrisStep:
                 u_res.data_ptr(), B, k, V, self.accepted.data_ptr(), self.out_tok.data_ptr(), self.mass.data_ptr(),
                 self.status.data_ptr(), ws.ptr, ws.nbytes, s))
         else:
-            self._check(lib.tetris_verify_greedy_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), B, k, V,
-                                                     self.accepted.data_ptr(), self.out_tok.data_ptr(),
-                                                     self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+            self._check(lib.tetris_verify_greedy_compact_f32(
+                p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), _ptr(cap), B, k, V, self.accepted.data_ptr(),
+                self.out_tok.data_ptr(), self.offsets.data_ptr(), self.tokens.data_ptr(), self.status.data_ptr(),
+                ws.ptr, ws.nbytes, s))
+            if events is not None:
+                events[2].record()
+                events[3].record()
+            return
         if events is not None:
             events[2].record()
         self._check(lib.tetris_compact(self.accepted.data_ptr(), self.out_tok.data_ptr(), d.data_ptr(), _ptr(cap), B,
@@ -513,9 +516,10 @@ class TetrisStep:
 
     @property
     def launches_per_step(self) -> int:
-        # stochastic: select_kernel (+ accept CTAs), persist_stream_kernel (streaming + grid barrier + descent);
-        # greedy: select_kernel, greedy_kernel, compact_kernel; fixed-window baseline: windows, accept, stream,
-        # compact (stochastic) or windows, greedy, compact
+        # stochastic: select kernel (+ accept CTAs), persist_stream_kernel (streaming + descent + token stream);
+        # greedy: select kernel, greedy_rowmap_kernel, persist_greedy_kernel (argmax stream + verdicts + compaction);
+        # fixed-window baseline: windows, accept, stream, compact (stochastic) or windows, rowmap, greedy stream
+        # (V % 8 == 0 and 16-byte aligned p; otherwise the greedy fallback adds its compact launch)
         if self.policy == "fixed":
             return 4 if self.mode == "stochastic" else 3
         return 2 if self.mode == "stochastic" else 3
