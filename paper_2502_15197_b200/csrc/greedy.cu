@@ -133,15 +133,23 @@ __global__ void __launch_bounds__(1024, 1)
     local += (w < 0 ? 0 : (w > k ? k : w)) + 1;
   }
   long long total;
-  long long off = block_excl_scan<long long>(local, s_tmp, total);
-  for (int b = r0; b < r1; ++b) {
-    int w = windows[b];
-    w = w < 0 ? 0 : (w > k ? k : w);
-    for (int j = 0; j <= w; ++j) {
-      rowmap[1 + off + j] = (b << 8) | j;
-      if (keys) keys[(int64_t)b * (k + 1) + j] = 0ull;
+  const long long off0 = block_excl_scan<long long>(local, s_tmp, total);
+  // the writes, one request at a time per warp with the lanes along the request's rows (coalesced): the owner lane
+  // broadcasts each of its requests' row offset and window
+  const int lane = tid & 31;
+  long long off = off0;
+  for (int src = 0; src < 32; ++src) {
+    const int sb0 = __shfl_sync(kFull, r0, src), sb1 = __shfl_sync(kFull, r1, src);
+    long long so = __shfl_sync(kFull, off, src);
+    for (int b = sb0; b < sb1; ++b) {
+      int w = windows[b];
+      w = w < 0 ? 0 : (w > k ? k : w);
+      for (int j = lane; j <= w; j += 32) {
+        rowmap[1 + so + j] = (b << 8) | j;
+        if (keys) keys[(int64_t)b * (k + 1) + j] = 0ull;
+      }
+      so += w + 1;
     }
-    off += w + 1;
   }
   if (tid == 0) rowmap[0] = (int32_t)total;
 }
@@ -174,24 +182,23 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   if (warp == kGProducer) {
     if (lane == 0) {
       const long long total = (long long)__ldcg(a.rowmap) * nch;
+      const uint64_t pol = l2_evict_first_policy();
       // Items are claimed kClaim at a time, one claim ahead: the counter's and the row map's round trips (each up to
       // ~1 us under full HBM load) overlap the copies of a whole claim instead of one 32 KB chunk each.
-      long long c_cur = (long long)atomicAdd(work, (unsigned long long)kClaim);
+      // small calls (fewer than 16 items per CTA) claim one item at a time, so every SM gets a share
+      const int claim = total >= 16LL * gridDim.x ? kClaim : 1;
+      long long c_cur = (long long)atomicAdd(work, (unsigned long long)claim);
       int rm_cur[kClaim], rm_nx[kClaim];
 #pragma unroll
-      for (int x = 0; x < kClaim; ++x) rm_cur[x] = c_cur + x < total ? __ldcg(a.rowmap + 1 + (c_cur + x) / nch) : 0;
+      for (int x = 0; x < kClaim; ++x)
+        rm_cur[x] = (x < claim && c_cur + x < total) ? __ldcg(a.rowmap + 1 + (c_cur + x) / nch) : 0;
       int t = 0;
       while (c_cur < total) {
-        const long long c_next = (long long)atomicAdd(work, (unsigned long long)kClaim);
+        const long long c_next = (long long)atomicAdd(work, (unsigned long long)claim);
 #pragma unroll
         for (int x = 0; x < kClaim; ++x) {
           const long long i = c_cur + x;
-          if (x == 1) {  // one copy issued: fetch the next claim's rows (waits for the counter's reply)
-#pragma unroll
-            for (int y = 0; y < kClaim; ++y)
-              rm_nx[y] = c_next + y < total ? __ldcg(a.rowmap + 1 + (c_next + y) / nch) : 0;
-          }
-          if (i < total) {
+          if (x < claim && i < total) {
             const int s = t % kGStages;
             if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
             const int rm = rm_cur[x];
@@ -201,9 +208,14 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
             const uint32_t bytes = (uint32_t)n * sizeof(float);
             sh.meta[s] = GMeta{b, row, cc, 0};
             mbar_arrive_expect_tx(&sh.full[s], bytes);
-            bulk_g2s(stage_mem + s * kGStageBytes, a.p + (int64_t)row * V + (int64_t)cc * kChunkElems, bytes,
-                     &sh.full[s]);
+            bulk_g2s_stream(stage_mem + s * kGStageBytes, a.p + (int64_t)row * V + (int64_t)cc * kChunkElems, bytes,
+                     &sh.full[s], pol);
             ++t;
+          }
+          if (x == (claim > 1 ? 1 : 0)) {  // copies issued: fetch the next claim's rows (waits for the counter)
+#pragma unroll
+            for (int y = 0; y < kClaim; ++y)
+              rm_nx[y] = (y < claim && c_next + y < total) ? __ldcg(a.rowmap + 1 + (c_next + y) / nch) : 0;
           }
         }
         c_cur = c_next;

@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
   if (warp == kProducerWarp) {
     // ---------------------------------------------------------------- producer (lane 0)
     if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
       // two items of look-ahead on the counter and the row info, so neither round trip stalls the copies
       long long i_next = (long long)atomicAdd(work, 1ull);
       long long i_next2 = (long long)atomicAdd(work, 1ull);
@@ -262,8 +263,10 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
         sh.meta[s] = StageMeta{b, c, res ? 1 : 0, 0};
         float* sp = reinterpret_cast<float*>(stage_mem + s * kStageBytes);
         mbar_arrive_expect_tx(&sh.full[s], res ? 2 * bytes : bytes);
-        bulk_g2s(sp, a.p + prow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s]);
-        if (res) bulk_g2s(sp + kChunkElems, a.q + qrow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s]);
+        bulk_g2s_stream(sp, a.p + prow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s], pol);
+        if (res)
+          bulk_g2s_stream(sp + kChunkElems, a.q + qrow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s],
+                          pol);
       }
     }
     __syncwarp();
