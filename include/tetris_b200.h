@@ -175,6 +175,17 @@ int tetris_verify_greedy_compact_f32(const float* p, const int32_t* d, const int
                                      int32_t* offsets, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
                                      tetris_stream_t stream);
 
+/* The greedy step in 2 launches (select1 with the row-list epilogue, then the persistent argmax stream with the
+ * verdicts and the compaction; V % 8 == 0 and 16-byte aligned p, else the stage-by-stage fallback): the selection of
+ * tetris_select_f64 over all B_sel rows of conf/len (sharded steps: every shard's scores, gathered) with capacity C,
+ * then tetris_verify_greedy_compact_f32 over the local rows [row0, row0 + B) (p, d, cap, accepted, out_tok, offsets,
+ * tokens are local; windows / win_offsets cover all B_sel rows). */
+int tetris_step_greedy_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C, int32_t row0,
+                           int32_t B, const float* p, const int32_t* d, const int32_t* cap, int32_t V,
+                           int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                           int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
+                           size_t ws_bytes, tetris_stream_t stream);
+
 /* Row sampler (the building block of the above, exposed for the token-level adapters):
  * for r < R: weights = max(0, p[p_row[r]] - q[q_row[r]]) if q != NULL and q_row[r] >= 0, else max(0, p[p_row[r]]);
  * out_idx[r] = sample(weights, u[r]); mass_out[r] = row mass.  Rows are V elements, row index in units of V. */

@@ -75,6 +75,9 @@ _SIGNATURES = {
         C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p,
                   _p, _p, _p, _sz, _p]),
     "tetris_verify_greedy_f32": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
+    "tetris_step_greedy_f32": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz,
+                  _p]),
     "tetris_verify_greedy_compact_f32": (
         C.c_int, [_p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "tetris_sample_rows_f64": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _sz, _p]),

@@ -35,6 +35,10 @@ struct SelectArgs {
   int* acc_counter;    // arrivals of those CTAs (zero between launches)
   long long* dbg;      // diagnostics: per-phase clock64() stamps of CTA 0 (nullptr: off)
   void* gscratch;      // workspace region WS_GSEL (grid selector), zero-initialised
+  // greedy epilogue (select1 only; rowmap == nullptr: off): the row list of greedy verification over the local rows
+  // [ep_row0, ep_row0 + ep_rows) and their zeroed argmax keys (greedy.cu, rowmap_write_warp)
+  int32_t* rowmap;
+  unsigned long long* gkeys;
 };
 
 void set_debug_buffer(long long* p);

@@ -323,6 +323,27 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
   }
   if (stamp) a.dbg[3] = clock64();
 
+  // ---- optional greedy epilogue: the row list of greedy verification over the local rows -------------------------
+  if (a.rowmap != nullptr) {
+    const int ep0 = a.ep_row0, ep1 = a.ep_row0 + a.ep_rows;
+    const int f = max(r0, ep0), l = min(min(r0 + RPT, B), ep1);  // this thread's local rows [f, l)
+    const int nb = l > f ? l - f : 0;
+    int wl[RPT];
+    long long my = 0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      int w = 0;
+#pragma unroll
+      for (int x = 0; x < RPT; ++x) w = (r0 + x == f + i) ? wr[x] : w;
+      wl[i] = i < nb ? w : 0;
+      my += i < nb ? w + 1 : 0;
+    }
+    long long rtot;
+    const long long roff = block_excl_scan<long long>(my, sh.tmp, rtot);
+    rowmap_write_warp<RPT>(wl, f - ep0, nb, roff, k, a.rowmap, a.gkeys, lane);
+    if (tid == 0) a.rowmap[0] = (int32_t)rtot;
+  }
+
   // ---- optional epilogue: first rejection, row to resample from, compaction offsets --------------------------------
   if (a.p != nullptr) {
     uint32_t vbad = 0;

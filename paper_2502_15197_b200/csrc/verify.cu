@@ -631,6 +631,74 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
   return offsets ? tetris_compact(accepted, out_tok, d, cap, B, k, offsets, tokens, st) : TETRIS_OK;
 }
 
+// The greedy step (select -> greedy verification -> compaction) in 2 launches when the selector is the single-CTA one
+// (its epilogue writes the row list) and p qualifies for the persistent stream; otherwise select + row list + stream.
+extern "C" int tetris_step_greedy_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                      int32_t row0, int32_t B, const float* p, const int32_t* d, const int32_t* cap,
+                                      int32_t V, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
+                                      int32_t* out_tok, int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                      uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
+  if (B == 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "empty batch");
+  if (B_sel < B || B_sel > TETRIS_MAX_SELECT_ROWS || row0 < 0 || row0 + B > B_sel)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "local rows [%d, %d) outside the %d selected rows", row0, row0 + B, B_sel);
+  if (!conf || !p || !d || !windows || !accepted || !out_tok || !offsets || !tokens)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!persist_greedy_eligible(p, V)) {
+    if ((rc = tetris_select_f64(conf, len, B_sel, k, C, 0, windows, win_offsets, nullptr, stats4, status, ws, ws_bytes,
+                                stream)))
+      return rc;
+    return verify_greedy_impl(p, d, windows + row0, cap, B, k, V, accepted, out_tok, offsets, tokens, status, ws,
+                              ws_bytes, st);
+  }
+  int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
+  unsigned long long* keys = (unsigned long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_VAL);
+  int32_t* rowmap = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWMAP);
+  SelectArgs sa = {};
+  sa.vals = conf;
+  sa.len = len;
+  sa.B = B_sel;
+  sa.k = k;
+  sa.C = (long long)C;
+  sa.windows = windows;
+  sa.win_offsets = win_offsets;
+  sa.stats = (long long*)stats4;
+  sa.status = status;
+  sa.ep_row0 = row0;
+  sa.ep_rows = B;
+  sa.gscratch = abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_GSEL);
+  const bool fused_rows = select1_eligible(B_sel, k);
+  if (fused_rows) {
+    sa.rowmap = rowmap;
+    sa.gkeys = keys;
+  }
+  if ((rc = launch_select(sa, st))) return rc;
+  if (!fused_rows && (rc = launch_greedy_rowmap(windows + row0, B, k, rowmap, keys, st))) return rc;
+  GreedyArgs a = {};
+  a.p = p;
+  a.d = d;
+  a.windows = windows + row0;
+  a.cap = cap;
+  a.B = B;
+  a.k = k;
+  a.V = V;
+  a.nch = n_chunks(V);
+  a.rowmap = rowmap;
+  a.keys = keys;
+  a.req_cnt = cnt;
+  a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
+  a.accepted = accepted;
+  a.out_tok = out_tok;
+  a.offsets = offsets;
+  a.tokens = tokens;
+  a.status = status;
+  return launch_persist_greedy(a, st);
+}
+
 extern "C" int tetris_verify_greedy_f32(const float* p, const int32_t* d, const int32_t* windows, int32_t B,
                                         int32_t k, int32_t V, int32_t* accepted, int32_t* out_tok,
                                         uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {

@@ -461,21 +461,28 @@ class TetrisStep:
                 events[2].record()
                 events[3].record()
             return
-        rc = lib.tetris_select_f64(sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, 0,
-                                   self.windows_all.data_ptr(), self.win_offsets.data_ptr(), None,
-                                   self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
-        self._check(rc)
         if events is not None:
+            # stage timing (eager): the same results stage by stage, so an event can sit between the selection and
+            # the argmax stream (the product path below fuses the row list into the selector's epilogue)
+            self._check(lib.tetris_select_f64(sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, 0,
+                                              self.windows_all.data_ptr(), self.win_offsets.data_ptr(), None,
+                                              self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s))
             events[1].record()
-        # row list + the persistent argmax stream with the compaction fused into its last CTA
-        rc = lib.tetris_verify_greedy_compact_f32(p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), _ptr(cap), B,
-                                                  k, V, self.accepted.data_ptr(), self.out_tok.data_ptr(),
-                                                  self.offsets.data_ptr(), self.tokens.data_ptr(),
-                                                  self.status.data_ptr(), ws.ptr, ws.nbytes, s)
-        self._check(rc)
-        if events is not None:
+            self._check(lib.tetris_verify_greedy_compact_f32(
+                p.data_ptr(), d.data_ptr(), self.windows.data_ptr(), _ptr(cap), B, k, V, self.accepted.data_ptr(),
+                self.out_tok.data_ptr(), self.offsets.data_ptr(), self.tokens.data_ptr(), self.status.data_ptr(),
+                ws.ptr, ws.nbytes, s))
             events[2].record()
             events[3].record()
+            return
+        # == tetris_step_greedy_f32 (select1 with the row-list epilogue, then the persistent argmax stream with the
+        # verdicts and the compaction)
+        rc = lib.tetris_step_greedy_f32(
+            sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, self.rank * B, B, p.data_ptr(), d.data_ptr(),
+            _ptr(cap), V, self.windows_all.data_ptr(), self.win_offsets.data_ptr(), self.accepted.data_ptr(),
+            self.out_tok.data_ptr(), self.offsets.data_ptr(), self.tokens.data_ptr(), self.stats.data_ptr(),
+            self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        self._check(rc)
 
     def _run_fixed(self, lengths, p, q, d, u_acc, u_res, cap, events, window) -> None:
         """Baseline step (fixed window / sd / dsd common window, clamped to each depth): windows kernel, then the same
@@ -517,12 +524,15 @@ class TetrisStep:
     @property
     def launches_per_step(self) -> int:
         # stochastic: select kernel (+ accept CTAs), persist_stream_kernel (streaming + descent + token stream);
-        # greedy: select kernel, greedy_rowmap_kernel, persist_greedy_kernel (argmax stream + verdicts + compaction);
+        # greedy: select1_kernel (+ row list), persist_greedy_kernel (argmax stream + verdicts + compaction), plus
+        # greedy_rowmap_kernel when the batch is too large for the single-CTA selector (B * k > 16384);
         # fixed-window baseline: windows, accept, stream, compact (stochastic) or windows, rowmap, greedy stream
         # (V % 8 == 0 and 16-byte aligned p; otherwise the greedy fallback adds its compact launch)
         if self.policy == "fixed":
             return 4 if self.mode == "stochastic" else 3
-        return 2 if self.mode == "stochastic" else 3
+        if self.mode == "stochastic":
+            return 2
+        return 2 if self.Bg * self.k <= 16384 and self.Bg <= 4096 else 3
 
 
 class _MappedTensor:

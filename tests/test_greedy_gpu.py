@@ -153,3 +153,49 @@ def test_greedy_persistent_repeat_and_graph():
     assert np.array_equal(_np(step.accepted), acc_ref) and np.array_equal(_np(step.out_tok), tok_ref)
     assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
     ops.raise_for_status(step.status)
+
+
+@pytest.mark.parametrize("W,B,k,V,C,rank", [(1, 16, 5, 32000, 48, 0), (1, 1024, 16, 4096, 8192, 0),
+                                             (2, 512, 16, 8192, 8192, 1), (4, 1024, 16, 2048, 32768, 3),
+                                             (1, 2048, 9, 1024, 9000, 0), (2, 300, 7, 1003, 2000, 1)])
+def test_step_greedy_matches_oracle(W, B, k, V, C, rank):
+    """tetris_step_greedy_f32 for rank r of W (selection over the gathered W*B rows, verification of the local
+    rows): the fused row list (B*W*k <= 16384), the grid selector + row-list kernel (larger), and the stage-by-stage
+    fallback (V % 8 != 0)."""
+    shards = [make_batch(B, k, V, seed=200 + r, mode="greedy") for r in range(W)]
+    conf_all = torch.cat([s.conf for s in shards]).contiguous()
+    len_all = torch.cat([s.lengths for s in shards]).contiguous()
+    bt = shards[rank]
+    Bg = W * B
+    lib = N.load()
+    dev = bt.p.device
+    g = torch.Generator(DEV).manual_seed(rank)
+    cap = torch.randint(0, k + 3, (B,), dtype=torch.int32, device=DEV, generator=g)
+    windows = torch.zeros(Bg, dtype=torch.int32, device=dev)
+    woff = torch.zeros(Bg + 1, dtype=torch.int32, device=dev)
+    acc = torch.full((B,), -5, dtype=torch.int32, device=dev)
+    tok = torch.full((B,), -5, dtype=torch.int32, device=dev)
+    offs = torch.zeros(B + 1, dtype=torch.int32, device=dev)
+    toks = torch.zeros(B * (k + 1), dtype=torch.int32, device=dev)
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    status = ops.new_status(dev)
+    ws = ops.Workspace(dev, N.OP_ALL, Bg, k, V)
+    for _ in range(2):  # the second call checks that every counter was left at zero
+        rc = lib.tetris_step_greedy_f32(
+            conf_all.data_ptr(), len_all.data_ptr(), Bg, k, C, rank * B, B, bt.p.data_ptr(), bt.d.data_ptr(),
+            cap.data_ptr(), V, windows.data_ptr(), woff.data_ptr(), acc.data_ptr(), tok.data_ptr(), offs.data_ptr(),
+            toks.data_ptr(), stats.data_ptr(), status.data_ptr(), ws.ptr, ws.nbytes,
+            torch.cuda.current_stream().cuda_stream)
+        assert rc == N.OK, lib.tetris_last_error()
+        torch.cuda.synchronize()
+        ops.raise_for_status(status)
+        w_ref, _, st_ref = O.select(_np(conf_all), C, _np(len_all))
+        assert np.array_equal(_np(windows), w_ref)
+        assert np.array_equal(_np(woff), np.concatenate([[0], np.cumsum(w_ref)]).astype(np.int32))
+        assert list(_np(stats)[:3]) == list(st_ref[:3])
+        wl = w_ref[rank * B:(rank + 1) * B]
+        acc_ref, tok_ref = O.verify_greedy(_np(bt.p), _np(bt.d), wl, nthreads=8)
+        assert np.array_equal(_np(acc), acc_ref) and np.array_equal(_np(tok), tok_ref)
+        off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), _np(cap))
+        assert np.array_equal(_np(offs), off_ref)
+        assert np.array_equal(_np(toks)[: off_ref[-1]], toks_ref)
