@@ -21,6 +21,10 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 PROF = ROOT / "profiles"
 OURS = ("tetris::",)
+# with an ncu -k filter the names come without their namespace: accept the library's kernel names as such
+OUR_KERNELS = ("select1_kernel", "select_kernel", "gselect_kernel", "persist_stream_kernel", "finalize_kernel",
+               "persist_greedy_kernel", "greedy_rowmap_kernel", "greedy_kernel", "compact_kernel", "pre_accept_kernel",
+               "accept_kernel", "sample_kernel", "uniform_windows_kernel", "sim_step_kernel")
 
 KEYS = [
     ("gpu__time_duration.sum", "duration"),
@@ -61,7 +65,8 @@ def short(name: str) -> str:
 
 
 def launch_table(path: Path, tag: str) -> str:
-    ls = [(short(n), us) for n, us in launches(path) if any(o in n for o in OURS)]
+    ls = [(short(n), us) for n, us in launches(path)
+          if any(o in n for o in OURS) or short(n).split("<")[0] in OUR_KERNELS]
     # drop the first quarter (warm-up / set-up launches) when there are many
     groups: "OrderedDict[str, list]" = OrderedDict()
     for n, us in ls:
