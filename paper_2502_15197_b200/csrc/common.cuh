@@ -15,6 +15,7 @@ constexpr int kChunkWarps = TETRIS_CHUNK_WARPS;
 constexpr int kChunkElems = TETRIS_CHUNK_ELEMS;
 constexpr int kWarpElems = kSegElems * kWarpSegs;  // 1024
 constexpr int kStreamThreads = kChunkWarps * 32;   // 256
+constexpr int kMaxChunks = 64;                      // V <= 524288
 
 static_assert(kLaneElems == 8, "lane = one 256-bit fp32 load");
 

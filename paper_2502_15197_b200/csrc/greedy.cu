@@ -33,6 +33,7 @@ constexpr int kGPublisher = kGConsumers + 1;
 constexpr int kGThreads = (kGConsumers + 2) * 32;
 constexpr int kGRing = 64;
 constexpr int kClaim = 4;  // work items (row chunks) per claim on the global counter
+constexpr int kStaticItems = 8;  // calls with at most this many items per CTA use a static schedule
 constexpr size_t kGStageBytes = (size_t)kChunkElems * sizeof(float);  // 32 KB
 constexpr size_t kGSmem = kGStages * kGStageBytes;                    // 192 KB dynamic
 static_assert(kSegsPerWarp * kGConsumers * kSegElems == kChunkElems, "consumers split a chunk evenly");
@@ -180,8 +181,39 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kGProducer) {
-    if (lane == 0) {
-      const long long total = (long long)__ldcg(a.rowmap) * nch;
+    const long long total = (long long)__ldcg(a.rowmap) * nch;
+    if (lane == 0 && total <= (long long)kStaticItems * gridDim.x) {
+      // small calls: a static schedule (items blockIdx.x + x * G) with every row lookup issued up front
+      const uint64_t pol = l2_evict_first_policy();
+      const int G = gridDim.x;
+      int rm[kStaticItems];
+#pragma unroll
+      for (int x = 0; x < kStaticItems; ++x) {
+        const long long i = blockIdx.x + (long long)x * G;
+        rm[x] = i < total ? __ldcg(a.rowmap + 1 + i / nch) : 0;
+      }
+      int t = 0;
+#pragma unroll
+      for (int x = 0; x < kStaticItems; ++x) {
+        const long long i = blockIdx.x + (long long)x * G;
+        if (i >= total) break;
+        const int s = t % kGStages;
+        if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
+        const int b = rm[x] >> 8, j = rm[x] & 0xFF, cc = (int)(i % nch);
+        const int row = b * (k + 1) + j;
+        const int n = min(kChunkElems, V - cc * kChunkElems);
+        const uint32_t bytes = (uint32_t)n * sizeof(float);
+        sh.meta[s] = GMeta{b, row, cc, 0};
+        mbar_arrive_expect_tx(&sh.full[s], bytes);
+        bulk_g2s_stream(stage_mem + s * kGStageBytes, a.p + (int64_t)row * V + (int64_t)cc * kChunkElems, bytes,
+                        &sh.full[s], pol);
+        ++t;
+      }
+      const int s = t % kGStages;
+      if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
+      sh.meta[s] = GMeta{-1, 0, 0, 0};
+      mbar_arrive(&sh.full[s]);
+    } else if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       // Items are claimed kClaim at a time, one claim ahead: the counter's and the row map's round trips (each up to
       // ~1 us under full HBM load) overlap the copies of a whole claim instead of one 32 KB chunk each.

@@ -67,6 +67,7 @@ struct StreamArgs {
   unsigned* grid_bar;  // [0]: CTAs done, [2..3]: 64-bit work counter (zero-initialised workspace, left at zero)
   int* req_cnt;        // [R] per-request published-chunk counters (zero, left at zero): the descent runs in the same
                        // launch as each request completes; nullptr -> a separate finalize_kernel launch
+  long long* dbg;      // diagnostics: per-CTA %globaltimer stamps at dbg[64 + 8 * cta + slot] (nullptr: off)
 };
 
 // Greedy verification (greedy.cu): the persistent argmax stream over the rows listed by greedy_rowmap_kernel.

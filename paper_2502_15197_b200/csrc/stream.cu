@@ -33,6 +33,15 @@ constexpr size_t kPersistSmem = kStages * kStageBytes;                     // 19
 
 
 
+// diagnostics (tools/dbg_stream.py): per-CTA %globaltimer stamps, a no-op unless a debug buffer is registered
+__device__ __forceinline__ void gstamp(const StreamArgs& a, int slot) {
+  if (a.dbg) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[64 + 8 * blockIdx.x + slot] = t;
+  }
+}
+
 struct StageMeta {
   int b, c, res, pad;
 };
@@ -209,6 +218,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
   unsigned long long* work = reinterpret_cast<unsigned long long*>(a.grid_bar + 2);
 
   if (tid == 0) {
+    gstamp(a, 0);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sh.full[s], 1);
       mbar_init(&sh.empty[s], kConsumerWarps);
@@ -223,6 +233,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
   // launched as a programmatic dependent of the selector: wait for it (and its memory) before the first read of the
   // row info it wrote; no-op for a plain launch
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0) gstamp(a, 1);
 
   if (warp == kProducerWarp) {
     // ---------------------------------------------------------------- producer (lane 0)
@@ -254,8 +265,10 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
         if (i >= total) {  // end of stream: a sentinel stage without data
           sh.meta[s] = StageMeta{-1, 0, 0, 0};
           mbar_arrive(&sh.full[s]);
+          gstamp(a, 3);
           break;
         }
+        if (t == 0) gstamp(a, 2);
         const int b = (int)(i / nch), c = (int)(i % nch);
         const int n = min(kChunkElems, a.V - c * kChunkElems);
         const uint32_t bytes = (uint32_t)n * sizeof(float);
@@ -285,6 +298,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
         }
         break;
       }
+      if (t == 0 && warp == 0 && lane == 0) gstamp(a, 4);
       const float* sp = reinterpret_cast<const float*>(stage_mem + s * kStageBytes);
       double Gs[kSegsPerConsumer];
 #pragma unroll
@@ -339,6 +353,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
       if (++npend == 32) flush();
     }
     flush();
+    if (lane == 0) gstamp(a, 5);
   }
   if (a.req_cnt != nullptr) {
     // Descent, one warp per request (requests strided over the CTAs so the re-reads spread over all SMs), as soon
@@ -362,6 +377,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
     }
     // the last CTA out resets the work counter (every producer is done with it)
     __syncthreads();
+    if (tid == 0) gstamp(a, 6);
     if (tid == 0) {
       unsigned* done = a.grid_bar;
       if (atomicAdd(done, 1u) == (unsigned)G - 1) {
@@ -470,8 +486,10 @@ namespace tetris {
 
 static int g_num_sms = 0;
 
-int launch_persist_stream(const StreamArgs& a, cudaStream_t st) {
-  if (a.R == 0) return TETRIS_OK;
+int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
+  if (a_in.R == 0) return TETRIS_OK;
+  StreamArgs a = a_in;
+  a.dbg = debug_buffer();
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);

@@ -19,7 +19,6 @@
 
 namespace tetris {
 
-constexpr int kMaxChunks = 64;  // V <= 524288
 
 // ---- pass 1: the 4 segment sums of one warp run and its left-to-right total ---------------------------------------
 template <typename T, bool VEC, bool RES>

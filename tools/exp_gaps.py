@@ -9,7 +9,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2502_15197_b200 import ops  # noqa: E402
 from paper_2502_15197_b200.synthetic import make_batch  # noqa: E402
 
-B, k, V, C = 1024, 16, 128256, 8192
+# optional argv: B k V C (default cfg3)
+B, k, V, C = (int(x) for x in sys.argv[1:5]) if len(sys.argv) >= 5 else (1024, 16, 128256, 8192)
 bt = make_batch(B, k, V, seed=0)
 step = ops.TetrisStep(B, k, V, C)
 lib, ws = step._lib, step.ws
