@@ -65,7 +65,7 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes) {
   return e;
 }
 
-enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP, WS_END };
+enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP, WS_SPEC_SUMS, WS_END };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -76,15 +76,19 @@ constexpr size_t kSlotAccCounter = kRequestSlots;        // accept-CTA arrivals 
 constexpr size_t kSlotGridCount = kRequestSlots + 2;     // grid barrier of the persistent sampler: arrivals
 constexpr size_t kSlotGridGen = kRequestSlots + 3;       //   ... and generation
 constexpr size_t kSlotWorkCounter = kRequestSlots + 4;   // the sampler's dynamic work counter (64-bit, 2 slots)
-constexpr size_t kCounterSlots = kRequestSlots + 64;
+constexpr size_t kSlotWorkSpec = kRequestSlots + 6;      // the speculative sampler's phase-A counter (64-bit, 2 slots)
+constexpr size_t kSlotSpecCnt = kRequestSlots + 64;      // its per-request completion counters [64 + 0, 64 + 2048)
+constexpr size_t kSpecSlots = 2048;
+constexpr size_t kCounterSlots = kRequestSlots + 64 + kSpecSlots;
 constexpr size_t kGselScratchBytes = 32 * 1024;  // grid selector: radix histograms, barrier words, CTA totals
 static_assert(kSlotGridGen == kSlotGridCount + 1, "grid_barrier reads the generation at bar + 1");
 static_assert(kSlotWorkCounter == kSlotGridCount + 2 && (kSlotWorkCounter % 2) == 0,
               "persist_stream_kernel reads its 8-byte-aligned work counter at grid_bar + 2");
+static_assert(kSlotWorkSpec == kSlotGridCount + 4, "persist_stream_kernel reads its phase-A counter at grid_bar + 4");
 
 inline size_t region_offset(int op, int B, int k, int V, Region which) {
   const size_t nch = (size_t)((V + TETRIS_CHUNK_ELEMS - 1) / TETRIS_CHUNK_ELEMS);
-  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   sizes[WS_COUNTERS] = kCounterSlots * 4;
   sizes[WS_GSEL] = kGselScratchBytes;  // shape-independent, right after the counters: a fixed offset in every layout
   if (op & TETRIS_OP_SELECT) {
@@ -101,9 +105,11 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
     sizes[WS_ROWINFO] = (size_t)B * 16;  // accept result: row to resample from (p row, q row)
     sizes[WS_ACCBYTES] = (size_t)B * k;  // pre-accept verdicts
     sizes[WS_ROWMAP] = 256 + (size_t)B * (k + 1) * 4;  // greedy: [0] selected-row count, then row -> (b, j)
+    // speculative sampler: the phase-A chunk sums then warp sums (B <= kSpecSlots)
+    sizes[WS_SPEC_SUMS] = B <= (int)kSpecSlots ? (size_t)B * nch * 8 * (1 + TETRIS_CHUNK_WARPS) : 0;
   }
-  const Region order[WS_END] = {WS_COUNTERS, WS_GSEL, WS_KEYS,    WS_CHUNK_SUMS, WS_WARP_SUMS,
-                                WS_ARG_VAL,  WS_ARG_IDX, WS_SCRATCH,    WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP};
+  const Region order[WS_END] = {WS_COUNTERS, WS_GSEL,    WS_KEYS,    WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL,
+                                WS_ARG_IDX,  WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES,   WS_ROWMAP,    WS_SPEC_SUMS};
   size_t off = 0;
   for (int i = 0; i < WS_END; ++i) {
     if (order[i] == which) return off;

@@ -68,7 +68,15 @@ struct StreamArgs {
   int* req_cnt;        // [R] per-request published-chunk counters (zero, left at zero): the descent runs in the same
                        // launch as each request completes; nullptr -> a separate finalize_kernel launch
   long long* dbg;      // diagnostics: per-CTA %globaltimer stamps at dbg[64 + 8 * cta + slot] (nullptr: off)
+  // speculative variant (u_acc != nullptr; R <= spec_max_requests()): the requests whose first drafted token is
+  // rejected are streamed before the selection completes (stream.cu); dense u_acc[R][k], len[R] (nullable: k)
+  const double* u_acc;
+  const int32_t* len;
+  int* req_cnt_spec;         // [R] their completion counters (zero, left at zero)
+  double* chunk_sums_spec;   // [R][nch] and [R][nch][8]: their sums
+  double* warp_sums_spec;
 };
+int spec_max_requests();
 
 // Greedy verification (greedy.cu): the persistent argmax stream over the rows listed by greedy_rowmap_kernel.
 struct GreedyArgs {

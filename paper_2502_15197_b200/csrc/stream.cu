@@ -1,19 +1,22 @@
 #include <cstdlib>
 // Stage (3) streaming: the persistent, warp-specialised residual / bonus sampler (sm_100a, fp32 rows, V % 8 == 0).
 //
-// One CTA per SM, 10 warps:
-//   warp 8      producer: walks this CTA's work items (request b, chunk c) and issues 1-D bulk copies on the TMA
-//               engine (cp.async.bulk + mbarrier complete_tx) of the chunk of the row to resample from — p[b][a_b]
-//               and q[b][a_b] after a rejection, p[b][w_b] for the bonus — into a 3-stage shared-memory ring;
-//   warps 0..7  consumers: each folds one 1024-element warp run of the staged chunk into the sampling-contract
-//               sums (lane: 8 elements left to right; segment: xor butterfly; warp: 4 segments left to right) and
-//               hands the 8 warp sums to the finalizer through a shared-memory ring;
-//   warp 9      publisher: folds the chunk sum and stores chunk + warp sums.
-// Then finalize_kernel (one warp per request) runs the descent T = u*mass -> chunk -> warp -> segment -> lane ->
-// element, re-reading only the one 1024-element warp run that holds the sample.  (An in-kernel last-arrival descent
-// was measured 2x slower: a CTA that falls behind becomes the last arrival of every request it touches.)
-// HBM is touched once per streamed element; the descent's re-read is 4-8 KB per request.  The accept test and the
-// row choice come from the select kernel's epilogue (rowinfo), so the producer never waits on a dependent gather.
+// persist_stream_kernel, one CTA per SM, programmatic dependent of the selector:
+//   warp 16     producer: takes work items (request b, chunk c) from a global counter and issues 1-D bulk copies on
+//               the TMA engine (cp.async.bulk + mbarrier complete_tx) of the chunk of the row to resample from —
+//               p[b][a_b] and q[b][a_b] after a rejection, p[b][w_b] for the bonus — into a 3-stage ring;
+//   warps 0..15 consumers: fold the staged chunk into the sampling-contract segment sums (lane: 8 elements left to
+//               right; segment: xor butterfly), 2 segments each;
+//   warp 17     publisher: folds warp and chunk sums, stores them, counts chunks on per-request counters;
+//   then every warp: the descent T = u*mass -> chunk -> warp -> segment -> lane -> element for the requests it owns,
+//               once their chunks are counted, re-reading only the one 1024-element warp run that holds the sample.
+// Speculative variant (SPEC, tetris_resample_spec_f32): the rows of requests whose FIRST drafted token is rejected —
+// p[b][0] and q[b][0], whatever the selection decides as long as w_b >= 1 — do not depend on the selection, so the
+// kernel computes that set itself (verify_token at position 0, the accept test's arithmetic) and streams it while the
+// selector is still running (phase A, before griddepcontrol.wait); a planner warp (18) then lists every other
+// request from the selector's row info (phase B).  A phase-A request whose window turns out to be 0 is streamed
+// again in phase B (its phase-A sums live in a separate region and are discarded).
+// HBM is touched once per streamed element; the descent's re-read is 4-8 KB per request.
 #include "common.cuh"
 #include "launch.h"
 
@@ -43,7 +46,17 @@ __device__ __forceinline__ void gstamp(const StreamArgs& a, int slot) {
 }
 
 struct StageMeta {
-  int b, c, res, pad;
+  int b, c, res, phase;  // phase 1: speculative (phase A) item
+};
+
+constexpr int kSpecMaxR = 2048;  // speculative variant: requests per call (lists in shared memory)
+
+struct SpecShared {
+  uint32_t inA[kSpecMaxR / 32];  // phase-A set (first drafted token rejected)
+  uint16_t listA[kSpecMaxR];
+  uint16_t listB[kSpecMaxR];
+  uint64_t listB_ready;          // mbarrier: the planner warp has written listB
+  int countA, countB;
 };
 
 struct PersistShared {
@@ -138,12 +151,13 @@ __device__ int descend_global(const float* __restrict__ P, const float* __restri
 
 // Descent for request b after every chunk sum is published (one warp): the chunk and warp sums of all chunks are
 // fetched in one round trip (lane l holds sums l, l+32, ...), then the one warp run holding the sample is re-read.
-__device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane) {
+__device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane, const double* chunk_sums,
+                                 const double* warp_sums) {
   const int nch = a.nch;
   const long long prow = a.prow[(int64_t)b * a.row_stride];
   const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
-  const double* cs = a.chunk_sums + (int64_t)b * nch;
-  const double* ws = a.warp_sums + (int64_t)b * nch * kChunkWarps;
+  const double* cs = chunk_sums + (int64_t)b * nch;
+  const double* ws = warp_sums + (int64_t)b * nch * kChunkWarps;
   double s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
   double s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
   // accepted-prefix tokens of the compacted stream, in parallel with the loads above
@@ -204,18 +218,82 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane)
   }
 }
 
-__global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(const StreamArgs a) {
+// Producer helper: one item (request b, chunk c) of rows prow / qrow (qrow < 0: plain) into stage t.
+__device__ __forceinline__ void issue_item(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, int b,
+                                           int c, long long prow, long long qrow, int phase, uint64_t pol) {
+  const int s = t % kStages;
+  if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
+  const int n = min(kChunkElems, a.V - c * kChunkElems);
+  const uint32_t bytes = (uint32_t)n * sizeof(float);
+  const bool res = qrow >= 0;
+  sh.meta[s] = StageMeta{b, c, res ? 1 : 0, phase};
+  float* sp = reinterpret_cast<float*>(stage_mem + s * kStageBytes);
+  mbar_arrive_expect_tx(&sh.full[s], res ? 2 * bytes : bytes);
+  bulk_g2s_stream(sp, a.p + prow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s], pol);
+  if (res)
+    bulk_g2s_stream(sp + kChunkElems, a.q + qrow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s], pol);
+}
+
+// Producer helper: stream the items (list[y], c), y < count, c < nch, claimed from `work` 4 at a time while more
+// than 8 claims per CTA remain, then one at a time (so the CTAs finish within one item of each other), one claim of
+// look-ahead (the counter's round trip and the row lookups overlap a claim's copies).  rows(b, prow, qrow) gives the
+// rows of request b.  Returns the next stage index.
+template <typename Rows>
+__device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, const uint16_t* list,
+                           int count, unsigned long long* work, int phase, uint64_t pol, Rows rows) {
+  constexpr int kC = 4;
+  const int nch = a.nch;
+  const long long total = (long long)count * nch;
+  const long long tail = 8LL * kC * gridDim.x;
+  auto claim = [&](long long seen, int& n) -> long long {
+    n = total - seen > tail ? kC : 1;
+    return (long long)atomicAdd(work, (unsigned long long)n);
+  };
+  int n_cur, n_next;
+  long long c_cur = claim(0, n_cur);
+  long long pr[kC], qr[kC], pn[kC], qn[kC];
+#pragma unroll
+  for (int x = 0; x < kC; ++x)
+    if (x < n_cur && c_cur + x < total) rows((int)list[(c_cur + x) / nch], pr[x], qr[x]);
+  while (c_cur < total) {
+    const long long c_next = claim(c_cur, n_next);
+#pragma unroll
+    for (int x = 0; x < kC; ++x) {
+      const long long i = c_cur + x;
+      if (x < n_cur && i < total)
+        issue_item(a, sh, stage_mem, t++, (int)list[i / nch], (int)(i % nch), pr[x], qr[x], phase, pol);
+      if (x == (n_cur > 1 ? 1 : 0)) {  // copies issued: the next claim's rows (waits for the counter's reply)
+#pragma unroll
+        for (int y = 0; y < kC; ++y)
+          if (y < n_next && c_next + y < total) rows((int)list[(c_next + y) / nch], pn[y], qn[y]);
+      }
+    }
+    c_cur = c_next;
+    n_cur = n_next;
+#pragma unroll
+    for (int x = 0; x < kC; ++x) {
+      pr[x] = pn[x];
+      qr[x] = qn[x];
+    }
+  }
+  return t;
+}
+
+template <bool SPEC>
+__global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_stream_kernel(const StreamArgs a) {
   extern __shared__ __align__(128) uint8_t stage_mem[];
   __shared__ PersistShared sh;
+  __shared__ SpecShared sx;  // speculative variant only
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nch = a.nch;
-  const long long total = (long long)a.R * nch;
+  const int nch = a.nch, k = a.k, R = a.R;
+  const long long total = (long long)R * nch;
   const int G = gridDim.x;
   // dynamic work distribution: items (request b, chunk c) are handed out in order from one global counter, so the
   // SMs stream neighbouring chunks at any moment (DRAM locality, like a round robin) and an SM that drew more
   // residual (p + q) items simply takes fewer items (balance).  The counter sits beside the grid barrier and is reset
   // by the barrier's last arrival.
   unsigned long long* work = reinterpret_cast<unsigned long long*>(a.grid_bar + 2);
+  unsigned long long* work_a = reinterpret_cast<unsigned long long*>(a.grid_bar + 4);  // speculative phase A
 
   if (tid == 0) {
     gstamp(a, 0);
@@ -227,17 +305,107 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
       mbar_init(&sh.ring_full[r], kConsumerWarps);
       mbar_init(&sh.ring_free[r], 1);
     }
+    if (SPEC) mbar_init(&sx.listB_ready, 1);
     mbar_fence_init();
   }
+  if (SPEC) {
+    // Phase-A set, computed before the selection completes: verify_token at drafted position 0 (accept_model.py:309-
+    // 313, the same arithmetic as the selector's accept test) for every request, one thread each.  All loads of a
+    // thread's requests are issued before any is used: two round trips in all (inputs, then the p/q gathers).
+    constexpr int kPer = (kSpecMaxR + kPersistThreads + 31) / (kPersistThreads + 32);  // requests per thread
+    int tt[kPer];
+    double uu[kPer];
+    bool dr[kPer];
+#pragma unroll
+    for (int x = 0; x < kPer; ++x) {
+      const int b = (warp + x * (int)(blockDim.x >> 5)) * 32 + lane;
+      dr[x] = false;
+      tt[x] = -1;
+      uu[x] = 0.0;
+      if (b < R) {
+        dr[x] = (a.len ? a.len[b] : k) >= 1;
+        tt[x] = a.d[(int64_t)b * k];
+        uu[x] = a.u_acc[(int64_t)b * k];
+      }
+    }
+    float ss[kPer], mm[kPer];
+#pragma unroll
+    for (int x = 0; x < kPer; ++x) {
+      const int b = (warp + x * (int)(blockDim.x >> 5)) * 32 + lane;
+      const bool ok = b < R && dr[x] && tt[x] >= 0 && tt[x] < a.V;
+      ss[x] = ok ? a.q[(int64_t)b * k * a.V + tt[x]] : 0.f;
+      mm[x] = ok ? a.p[(int64_t)b * (k + 1) * a.V + tt[x]] : 0.f;
+    }
+#pragma unroll
+    for (int x = 0; x < kPer; ++x) {
+      const int b0 = (warp + x * (int)(blockDim.x >> 5)) * 32;
+      const int b = b0 + lane;
+      bool rej = false;
+      if (b < R && dr[x]) {
+        if (tt[x] < 0 || tt[x] >= a.V) {
+          rej = true;
+        } else {
+          const double s = (double)ss[x], m = (double)mm[x];
+          rej = !((s <= m) || (uu[x] < m / s));
+        }
+      }
+      const unsigned bal = __ballot_sync(kFull, rej);
+      if (lane == 0 && b0 < R) sx.inA[b0 >> 5] = bal;
+    }
+    if (tid == 0) gstamp(a, 7);
+  }
   __syncthreads();
-  // launched as a programmatic dependent of the selector: wait for it (and its memory) before the first read of the
-  // row info it wrote; no-op for a plain launch
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tid == 0) gstamp(a, 1);
+  if (!SPEC) {
+    // launched as a programmatic dependent of the selector: wait for it (and its memory) before the first read of
+    // the row info it wrote; no-op for a plain launch
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0) gstamp(a, 1);
+  }
 
   if (warp == kProducerWarp) {
-    // ---------------------------------------------------------------- producer (lane 0)
-    if (lane == 0) {
+    // ---------------------------------------------------------------- producer
+    if (SPEC) {
+      // list A, in request order, from the bitmap (whole warp)
+      const int nw = (R + 31) >> 5;
+      int base = 0;
+      for (int w0 = 0; w0 < nw; w0 += 32) {
+        const int wi = w0 + lane;
+        uint32_t word = wi < nw ? sx.inA[wi] : 0u;
+        const int cnt = __popc(word);
+        const int incl = warp_incl_scan<int>(cnt, lane);
+        int pos = base + incl - cnt;
+        while (word) {
+          sx.listA[pos++] = (uint16_t)(wi * 32 + __ffs(word) - 1);
+          word &= word - 1;
+        }
+        base += __shfl_sync(kFull, incl, 31);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint64_t pol = l2_evict_first_policy();
+        gstamp(a, 2);
+        // phase A: residual rows at position 0, no dependence on the selection
+        int t = stream_list(a, sh, stage_mem, 0, sx.listA, base, work_a, 1, pol,
+                            [&](int b, long long& pr, long long& qr) {
+                              pr = (long long)b * (k + 1);
+                              qr = (long long)b * k;
+                            });
+        // phase B: everything else, from the selector's row info (listed by the planner warp)
+        mbar_wait(&sx.listB_ready, 0);
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // the selector's row info (no-op by now)
+        gstamp(a, 1);
+        t = stream_list(a, sh, stage_mem, t, sx.listB, sx.countB, work, 0, pol,
+                        [&](int b, long long& pr, long long& qr) {
+                          pr = a.prow[(int64_t)b * a.row_stride];
+                          qr = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+                        });
+        const int s = t % kStages;  // end of stream: a sentinel stage without data
+        if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
+        sh.meta[s] = StageMeta{-1, 0, 0, 0};
+        mbar_arrive(&sh.full[s]);
+        gstamp(a, 3);
+      }
+    } else if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       // two items of look-ahead on the counter and the row info, so neither round trip stalls the copies
       long long i_next = (long long)atomicAdd(work, 1ull);
@@ -260,26 +428,16 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
             qn = a.qrow ? a.qrow[(int64_t)bb * a.row_stride] : -1;
           }
         }
-        const int s = t % kStages;
-        if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
         if (i >= total) {  // end of stream: a sentinel stage without data
+          const int s = t % kStages;
+          if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
           sh.meta[s] = StageMeta{-1, 0, 0, 0};
           mbar_arrive(&sh.full[s]);
           gstamp(a, 3);
           break;
         }
         if (t == 0) gstamp(a, 2);
-        const int b = (int)(i / nch), c = (int)(i % nch);
-        const int n = min(kChunkElems, a.V - c * kChunkElems);
-        const uint32_t bytes = (uint32_t)n * sizeof(float);
-        const bool res = qrow >= 0;
-        sh.meta[s] = StageMeta{b, c, res ? 1 : 0, 0};
-        float* sp = reinterpret_cast<float*>(stage_mem + s * kStageBytes);
-        mbar_arrive_expect_tx(&sh.full[s], res ? 2 * bytes : bytes);
-        bulk_g2s_stream(sp, a.p + prow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s], pol);
-        if (res)
-          bulk_g2s_stream(sp + kChunkElems, a.q + qrow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s],
-                          pol);
+        issue_item(a, sh, stage_mem, t, (int)(i / nch), (int)(i % nch), prow, qrow, 0, pol);
       }
     }
     __syncwarp();
@@ -317,18 +475,19 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
       }
       __syncwarp();
     }
-  } else {
+  } else if (warp == kPublisherWarp) {
     // ---------------------------------------------------------------- publisher
     // One published chunk per iteration: lanes 0..7 fold a warp run each (4 segments left to right), lane 0 folds the
     // chunk sum over the 8 runs left to right, and the sums go to global memory for the descent.  Arrivals on the
     // per-request counters are batched: after 32 published chunks (and at the end) one release fence, then one
-    // relaxed increment per chunk (lane i for the i-th pending chunk).
+    // relaxed increment per chunk (lane i for the i-th pending chunk).  Phase-A chunks go to their own sums and
+    // counters.
     int pend_b = 0, npend = 0;
     auto flush = [&]() {
       if (npend == 0 || a.req_cnt == nullptr) return;
       __syncwarp();
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      if (lane < npend) atomicAdd(a.req_cnt + pend_b, 1);
+      if (lane < npend) atomicAdd((pend_b < 0 ? a.req_cnt_spec : a.req_cnt) + (pend_b < 0 ? ~pend_b : pend_b), 1);
       npend = 0;
     };
     for (int t = 0;; ++t) {
@@ -347,41 +506,86 @@ __global__ void __launch_bounds__(kPersistThreads, 1) persist_stream_kernel(cons
 #pragma unroll
       for (int w = 0; w < kChunkWarps; ++w) S = S + __shfl_sync(kFull, x, w);
       const int64_t cs = (int64_t)m.b * nch + m.c;
-      if (lane < kChunkWarps) __stcg(&a.warp_sums[cs * kChunkWarps + lane], x);
-      if (lane == 0) __stcg(&a.chunk_sums[cs], S);
-      if (lane == npend) pend_b = m.b;
+      double* wsum = (SPEC && m.phase) ? a.warp_sums_spec : a.warp_sums;
+      double* csum = (SPEC && m.phase) ? a.chunk_sums_spec : a.chunk_sums;
+      if (lane < kChunkWarps) __stcg(&wsum[cs * kChunkWarps + lane], x);
+      if (lane == 0) __stcg(&csum[cs], S);
+      if (lane == npend) pend_b = (SPEC && m.phase) ? ~m.b : m.b;
       if (++npend == 32) flush();
     }
     flush();
     if (lane == 0) gstamp(a, 5);
+  } else if (SPEC) {
+    // ---------------------------------------------------------------- planner (speculative variant)
+    // After the selection: list B = the requests phase A did not cover — not in the phase-A set, or in it with a zero
+    // window (then the bonus row p[b][0] is plain, not the residual phase A streamed).  Loads batched 16 per lane.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    int base = 0;
+    for (int b0 = 0; b0 < R; b0 += 32 * 16) {
+      long long qv[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x) {
+        const int b = b0 + 32 * x + lane;
+        qv[x] = b < R ? a.qrow[(int64_t)b * a.row_stride] : -1;
+      }
+#pragma unroll
+      for (int x = 0; x < 16; ++x) {
+        const int b = b0 + 32 * x + lane;
+        const bool inA = b < R && ((sx.inA[b >> 5] >> (b & 31)) & 1u);
+        const bool doneA = inA && qv[x] == (long long)b * k;
+        const unsigned need = __ballot_sync(kFull, b < R && !doneA);
+        if (b < R && !doneA) sx.listB[base + __popc(need & ((1u << lane) - 1u))] = (uint16_t)b;
+        base += __popc(need);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      sx.countB = base;
+      mbar_arrive(&sx.listB_ready);  // release (CTA scope): the list is visible to the producer's wait
+    }
+    __syncwarp();
   }
   if (a.req_cnt != nullptr) {
     // Descent, one warp per request (requests strided over the CTAs so the re-reads spread over all SMs), as soon
     // as the request's nch chunks are published.  A warp only ever waits for chunks already claimed from the work
     // counter by CTAs that are running, so no co-residency (cooperative launch) is needed.
     __syncthreads();
-    constexpr int kWarps = kPersistThreads / 32;
-    for (int b = warp * G + blockIdx.x; b < a.R; b += G * kWarps) {
+    if (SPEC) asm volatile("griddepcontrol.wait;" ::: "memory");  // the selector's row info (no-op by now)
+    const int nwarps = blockDim.x >> 5;
+    for (int b = warp * G + blockIdx.x; b < R; b += G * nwarps) {
+      const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+      const bool inA = SPEC && ((sx.inA[b >> 5] >> (b & 31)) & 1u);
+      const bool doneA = inA && qrow == (long long)b * k;
       if (lane == 0) {
         int seen;
+        int* cnt = doneA ? a.req_cnt_spec + b : a.req_cnt + b;
         for (;;) {
-          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.req_cnt + b) : "memory");
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
           if (seen >= nch) break;
           __nanosleep(64);
         }
-        a.req_cnt[b] = 0;  // every arrival is in: ready for the next launch
+        *cnt = 0;  // every arrival is in: ready for the next launch
+        if (inA && !doneA) {  // phase A streamed this request for nothing: drain its counter too
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.req_cnt_spec + b) : "memory");
+            if (seen >= nch) break;
+            __nanosleep(64);
+          }
+          a.req_cnt_spec[b] = 0;
+        }
       }
       __syncwarp();
-      const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
-      finalize_request(a, b, qrow >= 0, lane);
+      finalize_request(a, b, qrow >= 0, lane, doneA ? a.chunk_sums_spec : a.chunk_sums,
+                       doneA ? a.warp_sums_spec : a.warp_sums);
     }
-    // the last CTA out resets the work counter (every producer is done with it)
+    // the last CTA out resets the work counters (every producer is done with them)
     __syncthreads();
     if (tid == 0) gstamp(a, 6);
     if (tid == 0) {
       unsigned* done = a.grid_bar;
       if (atomicAdd(done, 1u) == (unsigned)G - 1) {
         *work = 0ull;
+        if (SPEC) *work_a = 0ull;
         *done = 0u;
       }
     }
@@ -394,7 +598,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(const StreamArgs a) {
   const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (b >= a.R) return;
   const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
-  finalize_request(a, b, qrow >= 0, lane);
+  finalize_request(a, b, qrow >= 0, lane, a.chunk_sums, a.warp_sums);
 }
 
 // ---- pre-accept: verify_token on every drafted position, one thread each (runs before the selection) -----------
@@ -496,16 +700,20 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  cudaError_t e =
-      cudaFuncSetAttribute(persist_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPersistSmem);
+  const bool spec = a.u_acc != nullptr && a.req_cnt != nullptr;
+  if (spec && (a.R > kSpecMaxR || !a.req_cnt_spec || !a.chunk_sums_spec || !a.warp_sums_spec || !a.d))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "speculative sampler: R=%d > %d or missing buffers", a.R, kSpecMaxR);
+  const void* fn = spec ? (const void*)persist_stream_kernel<true> : (const void*)persist_stream_kernel<false>;
+  cudaError_t e = abi::ensure_smem(fn, kPersistSmem);
   if (e != cudaSuccess) return abi::cuda_fail(e);
   const long long items = (long long)a.R * a.nch;
   const int grid = (int)(items < g_num_sms ? items : g_num_sms);
+  const int threads = kPersistThreads + (spec ? 32 : 0);
   if (a.req_cnt != nullptr) {
     // one launch: streaming + per-request completion counters + descent
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(kPersistThreads, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
     cfg.dynamicSmemBytes = kPersistSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -513,16 +721,19 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, persist_stream_kernel, a);
+    void* args[] = {(void*)&a};
+    e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return abi::cuda_fail(e);
     return abi::launch_check();
   }
-  persist_stream_kernel<<<grid, kPersistThreads, kPersistSmem, st>>>(a);
+  persist_stream_kernel<false><<<grid, kPersistThreads, kPersistSmem, st>>>(a);
   int rc = abi::launch_check();
   if (rc) return rc;
   finalize_kernel<<<(a.R + 3) / 4, 128, 0, st>>>(a);
   return abi::launch_check();
 }
+
+int spec_max_requests() { return kSpecMaxR; }
 
 bool persist_eligible(const float* p, const float* q, int V) {
   return (V % kLaneElems == 0) && (((uintptr_t)p & 15u) == 0) && (!q || (((uintptr_t)q & 15u) == 0)) &&

@@ -515,10 +515,12 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
   return launch_select(sa, (cudaStream_t)stream);
 }
 
-extern "C" int tetris_resample_f32(const float* p, const float* q, const double* u_res, int32_t B, int32_t k, int32_t V,
-                                   const int32_t* d, const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
-                                   double* mass_out, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
-                                   tetris_stream_t stream) {
+constexpr long long kSpecMinChunks = 4096;  // see tetris_step_stochastic_f32
+
+static int resample_impl(const float* p, const float* q, const double* u_res, const double* u_acc_spec,
+                         const int32_t* len_spec, int B, int k, int V, const int32_t* d, const int32_t* accepted,
+                         const int32_t* offsets, int32_t* out_tok, double* mass_out, int32_t* tokens, uint32_t* status,
+                         void* ws, size_t ws_bytes, cudaStream_t st) {
   int rc = check_shape(B, k, V);
   if (rc) return rc;
   if (B == 0) return TETRIS_OK;
@@ -527,12 +529,15 @@ extern "C" int tetris_resample_f32(const float* p, const float* q, const double*
   if (!persist_eligible(p, q, V))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "the streaming sampler needs V %% 8 == 0 and 16-byte aligned p/q");
   long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+  int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   StreamArgs a = {};
   a.p = p;
   a.q = q;
   a.V = V;
   a.nch = n_chunks(V);
   a.R = B;
+  a.k = k;
+  a.d = d;
   a.prow = rowinfo;
   a.qrow = rowinfo + 1;
   a.row_stride = 2;
@@ -540,20 +545,44 @@ extern "C" int tetris_resample_f32(const float* p, const float* q, const double*
   a.out_idx = out_tok;
   a.mass_out = mass_out;
   a.status = status;
-  a.counters = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
+  a.counters = cnt;
   a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
   a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
-  a.grid_bar = (unsigned*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + abi::kSlotGridCount;
-  a.req_cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
+  a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
+  a.req_cnt = cnt;
   if (tokens) {
     if (!accepted || !offsets || !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted, offsets, d");
     a.accepted = accepted;
     a.offsets = offsets;
     a.tokens = tokens;
-    a.d = d;
-    a.k = k;
   }
-  return launch_persist_stream(a, (cudaStream_t)stream);
+  if (u_acc_spec && d && B <= spec_max_requests()) {
+    double* sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_SPEC_SUMS);
+    a.u_acc = u_acc_spec;
+    a.len = len_spec;
+    a.req_cnt_spec = cnt + abi::kSlotSpecCnt;
+    a.chunk_sums_spec = sums;
+    a.warp_sums_spec = sums + (size_t)B * a.nch;
+  }
+  return launch_persist_stream(a, st);
+}
+
+extern "C" int tetris_resample_f32(const float* p, const float* q, const double* u_res, int32_t B, int32_t k, int32_t V,
+                                   const int32_t* d, const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
+                                   double* mass_out, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
+                                   tetris_stream_t stream) {
+  return resample_impl(p, q, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status,
+                       ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int tetris_resample_spec_f32(const float* p, const float* q, const double* u_res, const double* u_acc,
+                                        const int32_t* len, int32_t B, int32_t k, int32_t V, const int32_t* d,
+                                        const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
+                                        double* mass_out, int32_t* tokens, uint32_t* status, void* ws,
+                                        size_t ws_bytes, tetris_stream_t stream) {
+  if (!u_acc || !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "the speculative sampler needs u_acc and d");
+  return resample_impl(p, q, u_res, u_acc, len, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status, ws,
+                       ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k,
@@ -569,8 +598,12 @@ extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len
   int rc = tetris_select_accept_f32(conf, len, B_sel, k, C, row0, B, p, q, d, u_acc, u_packed, cap, V, windows,
                                     win_offsets, accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
   if (rc) return rc;
-  return tetris_resample_f32(p, q, u_res, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status, ws,
-                             ws_bytes, stream);
+  // dense uniforms: the sampler streams the selection-independent rows while the selector runs — when there is
+  // enough to stream for the early start to pay for its set-up (measured: cfg3, 16384 chunks, 158.8 -> 154.3 us per
+  // step; cfg2, 1024 chunks, 30.3 -> 32.8 us)
+  const bool spec = !u_packed && B <= spec_max_requests() && (long long)B * n_chunks(V) >= kSpecMinChunks;
+  return resample_impl(p, q, u_res, spec ? u_acc : nullptr, spec && len ? len + row0 : nullptr, B, k, V, d, accepted,
+                       offsets, out_tok, mass_out, tokens, status, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* windows, const int32_t* cap, int B,

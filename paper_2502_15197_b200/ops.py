@@ -10,6 +10,8 @@ f64, u_res [B] f64.
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 from typing import Optional
 
@@ -368,6 +370,11 @@ def compact(accepted: torch.Tensor, out_tok: torch.Tensor, d: torch.Tensor, cap:
 # ---------------------------------------------------------------------------------------------------------------
 # one full verification step with preallocated buffers (CUDA-graph capturable)
 # ---------------------------------------------------------------------------------------------------------------
+SPEC_MAX_REQUESTS = 2048  # tetris_resample_spec_f32's limit (per call, local rows)
+SPEC_MIN_CHUNKS = 4096    # below this much streaming the early start does not pay (csrc/verify.cu kSpecMinChunks)
+_NO_SPEC = os.environ.get("TETRIS_NO_SPEC") == "1"  # A/B timing switch: the plain sampler
+
+
 class TetrisStep:
     """select -> verify (stochastic or greedy) -> compact for fixed shapes; every launch goes on the current stream,
     all buffers are preallocated, nothing synchronises the host, so `run` can be captured in a CUDA graph."""
@@ -452,10 +459,19 @@ class TetrisStep:
             self._check(rc)
             if events is not None:
                 events[1].record()
-            rc = lib.tetris_resample_f32(p.data_ptr(), q.data_ptr(), u_res.data_ptr(), B, k, V, d.data_ptr(),
-                                         self.accepted.data_ptr(), self.offsets.data_ptr(), self.out_tok.data_ptr(),
-                                         self.mass.data_ptr(), self.tokens.data_ptr(), self.status.data_ptr(),
-                                         ws.ptr, ws.nbytes, s)
+            if self.u_layout == "dense" and B <= SPEC_MAX_REQUESTS and B * -(-V // 8192) >= SPEC_MIN_CHUNKS \
+                    and not _NO_SPEC:
+                # the speculative sampler: rows that do not depend on the selection stream while it runs
+                len_local = None if sel_len is None else sel_len[self.rank * B:(self.rank + 1) * B]
+                rc = lib.tetris_resample_spec_f32(
+                    p.data_ptr(), q.data_ptr(), u_res.data_ptr(), u_acc.data_ptr(), _ptr(len_local), B, k, V,
+                    d.data_ptr(), self.accepted.data_ptr(), self.offsets.data_ptr(), self.out_tok.data_ptr(),
+                    self.mass.data_ptr(), self.tokens.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+            else:
+                rc = lib.tetris_resample_f32(p.data_ptr(), q.data_ptr(), u_res.data_ptr(), B, k, V, d.data_ptr(),
+                                             self.accepted.data_ptr(), self.offsets.data_ptr(),
+                                             self.out_tok.data_ptr(), self.mass.data_ptr(), self.tokens.data_ptr(),
+                                             self.status.data_ptr(), ws.ptr, ws.nbytes, s)
             self._check(rc)
             if events is not None:
                 events[2].record()

@@ -419,3 +419,61 @@ def test_sampler_adversarial_rows_f32():
                     assert float(mass[r]) == m_ref, (V, r, residual)
                     if m_ref > 0:
                         assert int(idx[r]) == i_ref, (V, r, u_val, residual)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# the speculative sampler (tetris_resample_spec_f32): the rows of requests rejected at their first drafted token are
+# streamed before the selection completes; results identical to the plain sampler and the oracle, including the
+# requests it streams for nothing (window 0), empty rows, out-of-vocabulary first tokens, repeated calls
+@pytest.mark.parametrize("B,k,V,C,seed,ragged", [(64, 4, 8200, 10, 1, True), (300, 6, 4096, 40, 2, True),
+                                                  (1024, 16, 32000, 8192, 3, False), (2048, 3, 1024, 3000, 4, True),
+                                                  (5, 2, 8, 3, 5, False)])
+def test_spec_sampler_matches_oracle(B, k, V, C, seed, ragged):
+    bt = make_batch(B, k, V, seed=seed, ragged=ragged)
+    if ragged:
+        bt.lengths[::7] = 0  # empty rows: nothing drafted, never speculative
+    bt.d[::5, 0] = V + 3     # out-of-vocabulary first token: rejected at 0
+    lib = N.load()
+    dev = bt.p.device
+    outs = {}
+    for variant in ("spec", "plain"):
+        step = ops.TetrisStep(B, k, V, C)
+        for it in range(3):
+            step.status.zero_()
+            rc = lib.tetris_select_accept_f32(
+                bt.conf.data_ptr(), bt.lengths.data_ptr(), B, k, C, 0, B, bt.p.data_ptr(), bt.q.data_ptr(),
+                bt.d.data_ptr(), bt.u_acc.data_ptr(), 0, None, V, step.windows_all.data_ptr(),
+                step.win_offsets.data_ptr(), step.accepted.data_ptr(), step.offsets.data_ptr(), step.tokens.data_ptr(),
+                step.stats.data_ptr(), step.status.data_ptr(), step.ws.ptr, step.ws.nbytes,
+                torch.cuda.current_stream().cuda_stream)
+            assert rc == N.OK, lib.tetris_last_error()
+            if variant == "spec":
+                rc = lib.tetris_resample_spec_f32(
+                    bt.p.data_ptr(), bt.q.data_ptr(), bt.u_res.data_ptr(), bt.u_acc.data_ptr(), bt.lengths.data_ptr(),
+                    B, k, V, bt.d.data_ptr(), step.accepted.data_ptr(), step.offsets.data_ptr(),
+                    step.out_tok.data_ptr(), step.mass.data_ptr(), step.tokens.data_ptr(), step.status.data_ptr(),
+                    step.ws.ptr, step.ws.nbytes, torch.cuda.current_stream().cuda_stream)
+            else:
+                rc = lib.tetris_resample_f32(
+                    bt.p.data_ptr(), bt.q.data_ptr(), bt.u_res.data_ptr(), B, k, V, bt.d.data_ptr(),
+                    step.accepted.data_ptr(), step.offsets.data_ptr(), step.out_tok.data_ptr(), step.mass.data_ptr(),
+                    step.tokens.data_ptr(), step.status.data_ptr(), step.ws.ptr, step.ws.nbytes,
+                    torch.cuda.current_stream().cuda_stream)
+            assert rc == N.OK, lib.tetris_last_error()
+            torch.cuda.synchronize()
+            outs.setdefault(variant, []).append(tuple(_np(x).copy() for x in (
+                step.windows, step.accepted, step.out_tok, step.mass, step.offsets, step.tokens, step.status)))
+    for o in outs["spec"] + outs["plain"][1:]:
+        for x, y in zip(o, outs["plain"][0]):
+            assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+    w, acc, tok, mass, off, toks, st = outs["spec"][0]
+    w_ref, _, _ = O.select(_np(bt.conf), C, _np(bt.lengths))
+    assert np.array_equal(w, w_ref)
+    acc_ref, tok_ref, mass_ref = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), w_ref, _np(bt.u_acc),
+                                                     _np(bt.u_res), None, nthreads=8)
+    assert np.array_equal(acc, acc_ref) and np.array_equal(tok, tok_ref)
+    assert np.array_equal(mass.view(np.uint64), mass_ref.view(np.uint64))
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
+    assert np.array_equal(off, off_ref) and np.array_equal(toks[: off_ref[-1]], toks_ref)
+    if B >= 64:
+        assert (w == 0).any() or C >= B  # the window-0 path is exercised where the capacity is tight

@@ -24,7 +24,8 @@ for it in range(4):
 lib.tetris_debug_timestamps(None)
 d = dbg[64:].view(nsm, 8).cpu()
 t0 = int(d[:, 0][d[:, 0] > 0].min())
-names = ["entry", "after wait", "first copy", "last copy", "first consumed", "publisher done", "descents done"]
+names = ["entry", "after wait", "first copy", "last copy", "first consumed", "publisher done", "descents done",
+         "spec prologue"]
 for s, nme in enumerate(names):
     col = d[:, s]
     col = col[col > 0]
