@@ -79,7 +79,10 @@ constexpr size_t kSlotWorkCounter = kRequestSlots + 4;   // the sampler's dynami
 constexpr size_t kSlotWorkSpec = kRequestSlots + 6;      // the speculative sampler's phase-A counter (64-bit, 2 slots)
 constexpr size_t kSlotSpecCnt = kRequestSlots + 64;      // its per-request completion counters [64 + 0, 64 + 2048)
 constexpr size_t kSpecSlots = 2048;
-constexpr size_t kCounterSlots = kRequestSlots + 64 + kSpecSlots;
+constexpr size_t kSlotSpecCtl = kRequestSlots + 8;       // [2]: phase-A list length, requests processed
+constexpr size_t kSlotSpecBitmap = kSlotSpecCnt + kSpecSlots;   // [64]: the phase-A set
+constexpr size_t kSlotSpecList = kSlotSpecBitmap + 64;          // [2048]: the phase-A list
+constexpr size_t kCounterSlots = kSlotSpecList + kSpecSlots;
 constexpr size_t kGselScratchBytes = 32 * 1024;  // grid selector: radix histograms, barrier words, CTA totals
 static_assert(kSlotGridGen == kSlotGridCount + 1, "grid_barrier reads the generation at bar + 1");
 static_assert(kSlotWorkCounter == kSlotGridCount + 2 && (kSlotWorkCounter % 2) == 0,

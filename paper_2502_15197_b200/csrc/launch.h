@@ -75,6 +75,9 @@ struct StreamArgs {
   int* req_cnt_spec;         // [R] their completion counters (zero, left at zero)
   double* chunk_sums_spec;   // [R][nch] and [R][nch][8]: their sums
   double* warp_sums_spec;
+  int* spec_ctl;             // [2]: phase-A list length, requests processed (zero, left at zero)
+  uint32_t* spec_bitmap;     // [ceil(R / 32)]: the phase-A set (zero, left at zero)
+  int* spec_list;            // [R]: the phase-A list, entry b + 1 (zero, left at zero)
 };
 int spec_max_requests();
 

@@ -52,8 +52,7 @@ struct StageMeta {
 constexpr int kSpecMaxR = 2048;  // speculative variant: requests per call (lists in shared memory)
 
 struct SpecShared {
-  uint32_t inA[kSpecMaxR / 32];  // phase-A set (first drafted token rejected)
-  uint16_t listA[kSpecMaxR];
+  uint32_t inA[kSpecMaxR / 32];  // phase-A set (first drafted token rejected), copied by the planner
   uint16_t listB[kSpecMaxR];
   uint64_t listB_ready;          // mbarrier: the planner warp has written listB
   int countA, countB;
@@ -309,50 +308,39 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
     mbar_fence_init();
   }
   if (SPEC) {
-    // Phase-A set, computed before the selection completes: verify_token at drafted position 0 (accept_model.py:309-
-    // 313, the same arithmetic as the selector's accept test) for every request, one thread each.  All loads of a
-    // thread's requests are issued before any is used: two round trips in all (inputs, then the p/q gathers).
-    constexpr int kPer = (kSpecMaxR + kPersistThreads + 31) / (kPersistThreads + 32);  // requests per thread
-    int tt[kPer];
-    double uu[kPer];
-    bool dr[kPer];
-#pragma unroll
-    for (int x = 0; x < kPer; ++x) {
-      const int b = (warp + x * (int)(blockDim.x >> 5)) * 32 + lane;
-      dr[x] = false;
-      tt[x] = -1;
-      uu[x] = 0.0;
-      if (b < R) {
-        dr[x] = (a.len ? a.len[b] : k) >= 1;
-        tt[x] = a.d[(int64_t)b * k];
-        uu[x] = a.u_acc[(int64_t)b * k];
-      }
-    }
-    float ss[kPer], mm[kPer];
-#pragma unroll
-    for (int x = 0; x < kPer; ++x) {
-      const int b = (warp + x * (int)(blockDim.x >> 5)) * 32 + lane;
-      const bool ok = b < R && dr[x] && tt[x] >= 0 && tt[x] < a.V;
-      ss[x] = ok ? a.q[(int64_t)b * k * a.V + tt[x]] : 0.f;
-      mm[x] = ok ? a.p[(int64_t)b * (k + 1) * a.V + tt[x]] : 0.f;
-    }
-#pragma unroll
-    for (int x = 0; x < kPer; ++x) {
-      const int b0 = (warp + x * (int)(blockDim.x >> 5)) * 32;
-      const int b = b0 + lane;
+    // This CTA's share of the phase-A set (requests b = blockIdx.x + x * G, one thread each): verify_token at drafted
+    // position 0 (accept_model.py:309-313, the same arithmetic as the selector's accept test).  A rejected request
+    // is appended to the global phase-A list (entry b + 1; 0 = not written yet) and its bit set in the global set;
+    // then the CTA counts its requests as processed (release).  Every CTA starts streaming as soon as list entries
+    // appear — no CTA waits for the whole set.
+    const int nmine = blockIdx.x < R ? (R - 1 - (int)blockIdx.x) / G + 1 : 0;
+    if (tid < nmine) {
+      const int b = blockIdx.x + tid * G;
+      const bool drafted = (a.len ? a.len[b] : k) >= 1;
+      const int t = a.d[(int64_t)b * k];
+      const double u = a.u_acc[(int64_t)b * k];
       bool rej = false;
-      if (b < R && dr[x]) {
-        if (tt[x] < 0 || tt[x] >= a.V) {
+      if (drafted) {
+        if (t < 0 || t >= a.V) {
           rej = true;
         } else {
-          const double s = (double)ss[x], m = (double)mm[x];
-          rej = !((s <= m) || (uu[x] < m / s));
+          const double s = (double)a.q[(int64_t)b * k * a.V + t];
+          const double m = (double)a.p[(int64_t)b * (k + 1) * a.V + t];
+          rej = !((s <= m) || (u < m / s));
         }
       }
-      const unsigned bal = __ballot_sync(kFull, rej);
-      if (lane == 0 && b0 < R) sx.inA[b0 >> 5] = bal;
+      if (rej) {
+        const int pos = atomicAdd(a.spec_ctl, 1);
+        atomicOr(a.spec_bitmap + (b >> 5), 1u << (b & 31));
+        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.spec_list + pos), "r"(b + 1) : "memory");
+      }
     }
-    if (tid == 0) gstamp(a, 7);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (nmine) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(a.spec_ctl + 1), "r"(nmine) : "memory");
+      gstamp(a, 7);
+    }
   }
   __syncthreads();
   if (!SPEC) {
@@ -365,31 +353,39 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
   if (warp == kProducerWarp) {
     // ---------------------------------------------------------------- producer
     if (SPEC) {
-      // list A, in request order, from the bitmap (whole warp)
-      const int nw = (R + 31) >> 5;
-      int base = 0;
-      for (int w0 = 0; w0 < nw; w0 += 32) {
-        const int wi = w0 + lane;
-        uint32_t word = wi < nw ? sx.inA[wi] : 0u;
-        const int cnt = __popc(word);
-        const int incl = warp_incl_scan<int>(cnt, lane);
-        int pos = base + incl - cnt;
-        while (word) {
-          sx.listA[pos++] = (uint16_t)(wi * 32 + __ffs(word) - 1);
-          word &= word - 1;
-        }
-        base += __shfl_sync(kFull, incl, 31);
-      }
-      __syncwarp();
       if (lane == 0) {
         const uint64_t pol = l2_evict_first_policy();
-        gstamp(a, 2);
-        // phase A: residual rows at position 0, no dependence on the selection
-        int t = stream_list(a, sh, stage_mem, 0, sx.listA, base, work_a, 1, pol,
-                            [&](int b, long long& pr, long long& qr) {
-                              pr = (long long)b * (k + 1);
-                              qr = (long long)b * k;
-                            });
+        // phase A: residual rows at position 0 of the listed requests, item i = (entry i / nch, chunk i % nch),
+        // claimed one at a time with one claim of look-ahead; an entry not written yet is waited for until every
+        // request has been processed (then the list is complete)
+        int t = 0;
+        long long i = (long long)atomicAdd(work_a, 1ull);
+        for (;;) {
+          const int y = (int)(i / nch);
+          int b = -1;
+          if (y < R) {
+            for (;;) {
+              int e, done;
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
+              if (e) {
+                b = e - 1;
+                break;
+              }
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(done) : "l"(a.spec_ctl + 1) : "memory");
+              if (done >= R) {
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
+                b = e ? e - 1 : -1;
+                break;
+              }
+              __nanosleep(128);
+            }
+          }
+          if (b < 0) break;
+          const long long i_next = (long long)atomicAdd(work_a, 1ull);
+          if (t == 0) gstamp(a, 2);
+          issue_item(a, sh, stage_mem, t++, b, (int)(i % nch), (long long)b * (k + 1), (long long)b * k, 1, pol);
+          i = i_next;
+        }
         // phase B: everything else, from the selector's row info (listed by the planner warp)
         mbar_wait(&sx.listB_ready, 0);
         asm volatile("griddepcontrol.wait;" ::: "memory");  // the selector's row info (no-op by now)
@@ -520,6 +516,17 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
     // After the selection: list B = the requests phase A did not cover — not in the phase-A set, or in it with a zero
     // window (then the bonus row p[b][0] is plain, not the residual phase A streamed).  Loads batched 16 per lane.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (lane == 0) {  // every CTA's share of the phase-A set is in
+      int done;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(done) : "l"(a.spec_ctl + 1) : "memory");
+        if (done >= R) break;
+        __nanosleep(128);
+      }
+    }
+    __syncwarp();
+    for (int w = lane; w < (R + 31) >> 5; w += 32) sx.inA[w] = __ldcg(a.spec_bitmap + w);
+    __syncwarp();
     int base = 0;
     for (int b0 = 0; b0 < R; b0 += 32 * 16) {
       long long qv[16];
@@ -578,15 +585,30 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       finalize_request(a, b, qrow >= 0, lane, doneA ? a.chunk_sums_spec : a.chunk_sums,
                        doneA ? a.warp_sums_spec : a.warp_sums);
     }
-    // the last CTA out resets the work counters (every producer is done with them)
+    // the last CTA out resets the work counters and the phase-A list (every producer is done with them)
     __syncthreads();
-    if (tid == 0) gstamp(a, 6);
+    __shared__ int s_last;
     if (tid == 0) {
+      gstamp(a, 6);
       unsigned* done = a.grid_bar;
-      if (atomicAdd(done, 1u) == (unsigned)G - 1) {
+      s_last = atomicAdd(done, 1u) == (unsigned)G - 1;
+      if (s_last) {
         *work = 0ull;
         if (SPEC) *work_a = 0ull;
         *done = 0u;
+      }
+    }
+    if (SPEC) {
+      __syncthreads();
+      if (s_last) {
+        const int n = __ldcg(a.spec_ctl);
+        for (int y = tid; y < n; y += blockDim.x) a.spec_list[y] = 0;
+        for (int w = tid; w < (R + 31) >> 5; w += blockDim.x) a.spec_bitmap[w] = 0u;
+        __syncthreads();
+        if (tid == 0) {
+          a.spec_ctl[0] = 0;
+          a.spec_ctl[1] = 0;
+        }
       }
     }
   }
@@ -701,7 +723,8 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   const bool spec = a.u_acc != nullptr && a.req_cnt != nullptr;
-  if (spec && (a.R > kSpecMaxR || !a.req_cnt_spec || !a.chunk_sums_spec || !a.warp_sums_spec || !a.d))
+  if (spec && (a.R > kSpecMaxR || !a.req_cnt_spec || !a.chunk_sums_spec || !a.warp_sums_spec || !a.d ||
+               !a.spec_ctl || !a.spec_bitmap || !a.spec_list))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "speculative sampler: R=%d > %d or missing buffers", a.R, kSpecMaxR);
   const void* fn = spec ? (const void*)persist_stream_kernel<true> : (const void*)persist_stream_kernel<false>;
   cudaError_t e = abi::ensure_smem(fn, kPersistSmem);

@@ -563,6 +563,9 @@ static int resample_impl(const float* p, const float* q, const double* u_res, co
     a.req_cnt_spec = cnt + abi::kSlotSpecCnt;
     a.chunk_sums_spec = sums;
     a.warp_sums_spec = sums + (size_t)B * a.nch;
+    a.spec_ctl = cnt + abi::kSlotSpecCtl;
+    a.spec_bitmap = (uint32_t*)(cnt + abi::kSlotSpecBitmap);
+    a.spec_list = cnt + abi::kSlotSpecList;
   }
   return launch_persist_stream(a, st);
 }
