@@ -334,12 +334,18 @@ def run_tetris(args):
                          "compact": 1e3 * statistics.median(cmp_ms)},
             "select_verify_latency_us": 1e3 * statistics.median([a + b for a, b in zip(sel_ms, ver_ms)]),
             "tokens_per_step": total_tokens / args.steps,
-            "roofline": {"bound": "hbm", "kernel": "persist_stream_kernel (tetris_resample_f32: streaming + per-"
-                         "request descent in the same launch; CUDA events around the launch, eager pass)" if mode == "stochastic"
+            "roofline": {"bound": "hbm", "kernel": ("persist_stream_kernel<spec> (tetris_resample_spec_f32: its own "
+                         "phase-A set, streaming, per-request descents in one launch; CUDA events around the launch in "
+                         "an eager pass, where the events keep it from overlapping the selector as it does in the "
+                         "step)" if step.uses_spec else "persist_stream_kernel (tetris_resample_f32: streaming + per-"
+                         "request descent in the same launch; CUDA events around the launch, eager pass)")
+                         if mode == "stochastic"
                          else "greedy_rowmap_kernel + persist_greedy_kernel (tetris_verify_greedy_compact_f32: argmax "
                          "stream + verdicts + compaction in one launch; CUDA events around the call, eager pass)", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "alg_bytes_per_launch": alg_bytes / args.steps,
+                         "step_achieved": alg_bytes / (max_ms / 1e3) / 1e9,
+                         "step_frac": alg_bytes / (max_ms / 1e3) / 1e9 / peak,
                          "traffic": _load_traffic(args.config)},
             "clocks": clk,
             "gpu_launches": step.launches_per_step * args.steps,

@@ -459,8 +459,7 @@ class TetrisStep:
             self._check(rc)
             if events is not None:
                 events[1].record()
-            if self.u_layout == "dense" and B <= SPEC_MAX_REQUESTS and B * -(-V // 8192) >= SPEC_MIN_CHUNKS \
-                    and not _NO_SPEC:
+            if self.uses_spec:
                 # the speculative sampler: rows that do not depend on the selection stream while it runs
                 len_local = None if sel_len is None else sel_len[self.rank * B:(self.rank + 1) * B]
                 rc = lib.tetris_resample_spec_f32(
@@ -536,6 +535,12 @@ class TetrisStep:
         if rc != N.OK:
             msg = self._lib.tetris_last_error().decode(errors="replace")
             raise ValueError(msg) if rc == N.INVALID_ARGUMENT else N.TetrisError(rc, msg)
+
+    @property
+    def uses_spec(self) -> bool:
+        """True when the stochastic step runs the speculative sampler (tetris_resample_spec_f32)."""
+        return (self.mode == "stochastic" and self.policy == "tetris" and self.u_layout == "dense"
+                and self.B <= SPEC_MAX_REQUESTS and self.B * -(-self.V // 8192) >= SPEC_MIN_CHUNKS and not _NO_SPEC)
 
     @property
     def launches_per_step(self) -> int:
