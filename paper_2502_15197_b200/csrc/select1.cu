@@ -83,7 +83,12 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
   uint8_t* hi = lo + B;
   const int r0 = tid * RPT;
   const bool stamp = a.dbg != nullptr && tid == 0;
-  if (stamp) a.dbg[0] = clock64();
+  if (stamp) {
+    a.dbg[0] = clock64();
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    a.dbg[48] = g;
+  }
 
   // ---- phase 0: every global load of the selector in flight at once (row lengths + the [B][k] values, 16-byte
   //      loads where aligned), transposed into keys[j][r]; histogram 0 cleared meanwhile ----------------------------
@@ -428,7 +433,12 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
       if (a.accept_ctas > 0) *a.acc_counter = 0;  // every accept CTA has arrived; ready for the next launch
     }
   }
-  if (stamp) a.dbg[4] = clock64();
+  if (stamp) {
+    a.dbg[4] = clock64();
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    a.dbg[49] = g;
+  }
 }
 
 bool select1_eligible(int B, int k) {
