@@ -233,47 +233,26 @@ __device__ __forceinline__ void issue_item(const StreamArgs& a, PersistShared& s
     bulk_g2s_stream(sp + kChunkElems, a.q + qrow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s], pol);
 }
 
-// Producer helper: stream the items (list[y], c), y < count, c < nch, claimed from `work` 4 at a time while more
-// than 8 claims per CTA remain, then one at a time (so the CTAs finish within one item of each other), one claim of
-// look-ahead (the counter's round trip and the row lookups overlap a claim's copies).  rows(b, prow, qrow) gives the
-// rows of request b.  Returns the next stage index.
+// Producer helper: stream the items (list[y], c), y < count, c < nch, taken one at a time from `work` in order with
+// two items of look-ahead on the counter and one on the row lookup — the plain producer's schedule over a list.
+// rows(b, prow, qrow) gives the rows of request b.  Returns the next stage index.
 template <typename Rows>
 __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, const uint16_t* list,
                            int count, unsigned long long* work, int phase, uint64_t pol, Rows rows) {
-  constexpr int kC = 4;
   const int nch = a.nch;
   const long long total = (long long)count * nch;
-  const long long tail = 8LL * kC * gridDim.x;
-  auto claim = [&](long long seen, int& n) -> long long {
-    n = total - seen > tail ? kC : 1;
-    return (long long)atomicAdd(work, (unsigned long long)n);
-  };
-  int n_cur, n_next;
-  long long c_cur = claim(0, n_cur);
-  long long pr[kC], qr[kC], pn[kC], qn[kC];
-#pragma unroll
-  for (int x = 0; x < kC; ++x)
-    if (x < n_cur && c_cur + x < total) rows((int)list[(c_cur + x) / nch], pr[x], qr[x]);
-  while (c_cur < total) {
-    const long long c_next = claim(c_cur, n_next);
-#pragma unroll
-    for (int x = 0; x < kC; ++x) {
-      const long long i = c_cur + x;
-      if (x < n_cur && i < total)
-        issue_item(a, sh, stage_mem, t++, (int)list[i / nch], (int)(i % nch), pr[x], qr[x], phase, pol);
-      if (x == (n_cur > 1 ? 1 : 0)) {  // copies issued: the next claim's rows (waits for the counter's reply)
-#pragma unroll
-        for (int y = 0; y < kC; ++y)
-          if (y < n_next && c_next + y < total) rows((int)list[(c_next + y) / nch], pn[y], qn[y]);
-      }
-    }
-    c_cur = c_next;
-    n_cur = n_next;
-#pragma unroll
-    for (int x = 0; x < kC; ++x) {
-      pr[x] = pn[x];
-      qr[x] = qn[x];
-    }
+  long long i_next = (long long)atomicAdd(work, 1ull);
+  long long i_next2 = (long long)atomicAdd(work, 1ull);
+  long long pn = 0, qn = -1;
+  if (i_next < total) rows((int)list[i_next / nch], pn, qn);
+  for (;;) {
+    const long long i = i_next;
+    const long long prow = pn, qrow = qn;
+    i_next = i_next2;
+    if (i >= total) break;
+    i_next2 = (long long)atomicAdd(work, 1ull);
+    if (i_next < total) rows((int)list[i_next / nch], pn, qn);
+    issue_item(a, sh, stage_mem, t++, (int)list[i / nch], (int)(i % nch), prow, qrow, phase, pol);
   }
   return t;
 }
@@ -356,35 +335,40 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       if (lane == 0) {
         const uint64_t pol = l2_evict_first_policy();
         // phase A: residual rows at position 0 of the listed requests, item i = (entry i / nch, chunk i % nch),
-        // claimed one at a time with one claim of look-ahead; an entry not written yet is waited for until every
-        // request has been processed (then the list is complete)
-        int t = 0;
-        long long i = (long long)atomicAdd(work_a, 1ull);
-        for (;;) {
+        // taken one at a time with two items of look-ahead on the counter and one on the entry (a relaxed load
+        // issued before the current copy waits for its stage); an entry not written yet is waited for until every
+        // request has been processed (then the list is complete and the phase is over)
+        auto entry = [&](long long i) -> int {  // request of item i, -1: past the end of the list
           const int y = (int)(i / nch);
-          int b = -1;
-          if (y < R) {
-            for (;;) {
-              int e, done;
-              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
-              if (e) {
-                b = e - 1;
-                break;
-              }
-              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(done) : "l"(a.spec_ctl + 1) : "memory");
-              if (done >= R) {
-                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
-                b = e ? e - 1 : -1;
-                break;
-              }
-              __nanosleep(128);
+          if (y >= R) return -1;
+          for (;;) {
+            int e, done;
+            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
+            if (e) return e - 1;
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(done) : "l"(a.spec_ctl + 1) : "memory");
+            if (done >= R) {
+              asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
+              return e ? e - 1 : -1;
             }
+            __nanosleep(128);
           }
-          if (b < 0) break;
-          const long long i_next = (long long)atomicAdd(work_a, 1ull);
+        };
+        int t = 0;
+        long long i_cur = (long long)atomicAdd(work_a, 1ull);
+        long long i_nxt = (long long)atomicAdd(work_a, 1ull);
+        int b_cur = entry(i_cur);
+        while (b_cur >= 0) {
+          const long long i_nxt2 = (long long)atomicAdd(work_a, 1ull);
+          // the next item's entry: its load is in flight while this item waits for a free stage
+          const int y_nxt = (int)(i_nxt / nch);
+          int e_nxt = 0;
+          if (y_nxt < R) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e_nxt) : "l"(a.spec_list + y_nxt));
           if (t == 0) gstamp(a, 2);
-          issue_item(a, sh, stage_mem, t++, b, (int)(i % nch), (long long)b * (k + 1), (long long)b * k, 1, pol);
-          i = i_next;
+          issue_item(a, sh, stage_mem, t++, b_cur, (int)(i_cur % nch), (long long)b_cur * (k + 1),
+                     (long long)b_cur * k, 1, pol);
+          b_cur = e_nxt ? e_nxt - 1 : entry(i_nxt);
+          i_cur = i_nxt;
+          i_nxt = i_nxt2;
         }
         // phase B: everything else, from the selector's row info (listed by the planner warp)
         mbar_wait(&sx.listB_ready, 0);

@@ -3,7 +3,7 @@
 set -u
 T=${1:-rx}
 mkdir -p gpurun_out
-K='regex:select|persist|greedy|compact|finalize|rowmap'
+K="regex:select|persist|greedy|compact|finalize|rowmap"
 timeout -s KILL 600 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
 for c in cfg3g cfg1 cfg2; do
   timeout -s KILL 300 python bench.py --config $c > gpurun_out/${T}_bench_$c.json 2> gpurun_out/${T}_bench_$c.err
