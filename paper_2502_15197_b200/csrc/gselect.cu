@@ -16,6 +16,9 @@
 // The grid barrier is a generation barrier on two words of the workspace (left consistent for the next launch);
 // the launch is cooperative, so all CTAs are co-resident.
 #include <cooperative_groups.h>
+#ifndef GSEL_CELLS_PER_CTA
+#define GSEL_CELLS_PER_CTA 4096
+#endif
 
 #include "abi_util.h"
 #include "common.cuh"
@@ -24,6 +27,7 @@
 namespace tetris {
 
 constexpr int kGThreads = 512;
+constexpr long long kGCellsPerCta = GSEL_CELLS_PER_CTA;
 constexpr int kGBins = 2048;
 constexpr int kGMaxGrid = 256;
 constexpr size_t kGKeyBudget = 150 * 1024;  // keys + verdicts per CTA
@@ -380,7 +384,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
 
 bool gselect_shape(int B, int k, int num_sms, int* grid, int* RB) {
   const long long cells = (long long)B * (k > 0 ? k : 1);
-  long long g = (cells + 1023) / 1024;
+  // cells per CTA: fewer, fuller CTAs leave SMs to the sampler that overlaps the selection (speculative start)
+  long long g = (cells + kGCellsPerCta - 1) / kGCellsPerCta;
   const long long g_rows = (B + kGThreads - 1) / kGThreads;                              // one row per thread
   const long long g_smem = (cells * 9 + (long long)kGKeyBudget - 1) / (long long)kGKeyBudget;  // keys + verdicts
   if (g < g_rows) g = g_rows;
