@@ -82,7 +82,9 @@ constexpr size_t kSpecSlots = 2048;
 constexpr size_t kSlotSpecCtl = kRequestSlots + 8;       // [2]: phase-A list length, requests processed
 constexpr size_t kSlotSpecBitmap = kSlotSpecCnt + kSpecSlots;   // [64]: the phase-A set
 constexpr size_t kSlotSpecList = kSlotSpecBitmap + 64;          // [2048]: the phase-A list
-constexpr size_t kCounterSlots = kSlotSpecList + kSpecSlots;
+constexpr size_t kSlotGreedyKey0 = kSlotSpecList + kSpecSlots;  // [2 * 65536]: greedy row-0 argmax keys (u64)
+constexpr size_t kCounterSlots = kSlotGreedyKey0 + 2 * kRequestSlots;
+static_assert(kSlotGreedyKey0 % 2 == 0, "8-byte aligned greedy row-0 keys");
 constexpr size_t kGselScratchBytes = 32 * 1024;  // grid selector: radix histograms, barrier words, CTA totals
 static_assert(kSlotGridGen == kSlotGridCount + 1, "grid_barrier reads the generation at bar + 1");
 static_assert(kSlotWorkCounter == kSlotGridCount + 2 && (kSlotWorkCounter % 2) == 0,

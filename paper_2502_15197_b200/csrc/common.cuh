@@ -190,11 +190,12 @@ __device__ __forceinline__ void lds8_swz(const float* p, int lane, float (&v)[8]
   v[0] = lo.x, v[1] = lo.y, v[2] = lo.z, v[3] = lo.w, v[4] = hi.x, v[5] = hi.y, v[6] = hi.z, v[7] = hi.w;
 }
 
-// Greedy verification's row list (greedy.cu): rowmap[1 + o_b + j] = b << 8 | j for j = 0..w_b, o_b = Σ_{b' < b}
-// (w_b' + 1), and the argmax key of each listed row zeroed.  Warp-cooperative: every lane passes its own block of
+// Greedy verification's row list (greedy.cu): rowmap[1 + o_b + j - J0] = b << 8 | j for j = J0..w_b, o_b =
+// Σ_{b' < b} (w_b' + 1 - J0), and the argmax key of each listed row zeroed (J0 = 1: row 0 of every request is
+// streamed separately, before the selection completes).  Warp-cooperative: every lane passes its own block of
 // requests [b0, b0 + nb) (nb <= N) with clamped windows w[0..nb) and the row offset of b0; the warp writes each
 // request's rows with the lanes along the rows (coalesced stores).
-template <int N>
+template <int N, int J0 = 1>
 __device__ __forceinline__ void rowmap_write_warp(const int (&w)[N], int b0, int nb, long long off, int k,
                                                   int32_t* __restrict__ rowmap, unsigned long long* __restrict__ keys,
                                                   int lane) {
@@ -206,11 +207,11 @@ __device__ __forceinline__ void rowmap_write_warp(const int (&w)[N], int b0, int
       const int wi = __shfl_sync(kFull, w[i], src);
       if (i < snb) {
         const int b = sb0 + i;
-        for (int j = lane; j <= wi; j += 32) {
-          rowmap[1 + so + j] = (b << 8) | j;
+        for (int j = J0 + lane; j <= wi; j += 32) {
+          rowmap[1 + so + j - J0] = (b << 8) | j;
           if (keys) keys[(int64_t)b * (k + 1) + j] = 0ull;
         }
-        so += wi + 1;
+        so += wi + 1 - J0;
       }
     }
   }

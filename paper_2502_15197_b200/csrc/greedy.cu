@@ -38,8 +38,17 @@ constexpr size_t kGStageBytes = (size_t)kChunkElems * sizeof(float);  // 32 KB
 constexpr size_t kGSmem = kGStages * kGStageBytes;                    // 192 KB dynamic
 static_assert(kSegsPerWarp * kGConsumers * kSegElems == kChunkElems, "consumers split a chunk evenly");
 
+// diagnostics (tools/dbg_greedy.py): per-CTA %globaltimer stamps, a no-op unless a debug buffer is registered
+__device__ __forceinline__ void gtime(const GreedyArgs& a, int slot) {
+  if (a.dbg) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[64 + 8 * blockIdx.x + slot] = t;
+  }
+}
+
 struct GMeta {
-  int b, row, c, pad;  // request, row index b*(k+1)+j, chunk
+  int b, row, c, pad;  // request, row index b*(k+1)+j, chunk; pad 1: a row-0 item (phase A, key in key0)
 };
 
 struct GreedyShared {
@@ -116,12 +125,13 @@ __device__ __forceinline__ unsigned long long warp_argmax(const float* __restric
 
 }  // namespace
 
-// Rows read by greedy verification — positions 0..w_b of every request, w_b clamped to [0, k] — in request order:
+// Rows read by greedy verification — positions j0..w_b of every request, w_b clamped to [0, k] — in request order:
 // rowmap[1 + r] = b << 8 | j, rowmap[0] = their count; the argmax key of each listed row is zeroed (keys != nullptr).
+// j0 = 1 for the persistent stream (it streams row 0 of every request itself, before the selection completes).
 // One CTA; each thread a contiguous block of requests.  Launched as a programmatic dependent of the selector.
 __global__ void __launch_bounds__(1024, 1)
     greedy_rowmap_kernel(const int32_t* __restrict__ windows, int B, int k, int32_t* __restrict__ rowmap,
-                         unsigned long long* __restrict__ keys) {
+                         unsigned long long* __restrict__ keys, int j0) {
   __shared__ long long s_tmp[33];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
@@ -131,7 +141,7 @@ __global__ void __launch_bounds__(1024, 1)
   long long local = 0;
   for (int b = r0; b < r1; ++b) {
     const int w = windows[b];
-    local += (w < 0 ? 0 : (w > k ? k : w)) + 1;
+    local += (w < 0 ? 0 : (w > k ? k : w)) + 1 - j0;
   }
   long long total;
   const long long off0 = block_excl_scan<long long>(local, s_tmp, total);
@@ -145,11 +155,11 @@ __global__ void __launch_bounds__(1024, 1)
     for (int b = sb0; b < sb1; ++b) {
       int w = windows[b];
       w = w < 0 ? 0 : (w > k ? k : w);
-      for (int j = lane; j <= w; j += 32) {
-        rowmap[1 + so + j] = (b << 8) | j;
+      for (int j = j0 + lane; j <= w; j += 32) {
+        rowmap[1 + so + j - j0] = (b << 8) | j;
         if (keys) keys[(int64_t)b * (k + 1) + j] = 0ull;
       }
-      so += w + 1;
+      so += w + 1 - j0;
     }
   }
   if (tid == 0) rowmap[0] = (int32_t)total;
@@ -166,6 +176,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   unsigned long long* work = reinterpret_cast<unsigned long long*>(a.grid_bar + 2);
 
   if (tid == 0) {
+    gtime(a, 0);
     for (int s = 0; s < kGStages; ++s) {
       mbar_init(&sh.full[s], 1);
       mbar_init(&sh.empty[s], kGConsumers);
@@ -177,44 +188,70 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
     mbar_fence_init();
   }
   __syncthreads();
-  // programmatic dependent of the row-map kernel: wait for it (and its memory) before reading the row list
-  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kGProducer) {
+    const uint64_t pol = l2_evict_first_policy();
+    int t = 0;
+    // one item (request b, listed row `row`, chunk c) into the next stage; phase 1: a row-0 item
+    auto issue = [&](int b, int row, int cc, int phase) {
+      const int s = t % kGStages;
+      if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
+      const int n = min(kChunkElems, V - cc * kChunkElems);
+      const uint32_t bytes = (uint32_t)n * sizeof(float);
+      sh.meta[s] = GMeta{b, row, cc, phase};
+      if (t == 0) gtime(a, 1);
+      mbar_arrive_expect_tx(&sh.full[s], bytes);
+      bulk_g2s_stream(stage_mem + s * kGStageBytes, a.p + (int64_t)row * V + (int64_t)cc * kChunkElems, bytes,
+                      &sh.full[s], pol);
+      ++t;
+    };
+    // Phase A, before the selection completes: row 0 of every request — always verified (positions 0..w_b) — as
+    // items i = (b = i / nch, chunk i % nch), claimed 4 at a time (static when there are few)
+    if (lane == 0) {
+      const long long total_a = (long long)a.B * nch;
+      if (total_a <= (long long)kStaticItems * G) {
+        for (long long i = blockIdx.x; i < total_a; i += G) {
+          const int b = (int)(i / nch);
+          issue(b, b * (k + 1), (int)(i % nch), 1);
+        }
+      } else {
+        unsigned long long* work_a = reinterpret_cast<unsigned long long*>(a.grid_bar2);
+        long long c_cur = (long long)atomicAdd(work_a, (unsigned long long)kClaim);
+        while (c_cur < total_a) {
+          const long long c_next = (long long)atomicAdd(work_a, (unsigned long long)kClaim);
+#pragma unroll
+          for (int x = 0; x < kClaim; ++x) {
+            const long long i = c_cur + x;
+            if (i < total_a) {
+              const int b = (int)(i / nch);
+              issue(b, b * (k + 1), (int)(i % nch), 1);
+            }
+          }
+          c_cur = c_next;
+        }
+      }
+    }
+    __syncwarp();
+    // Phase B: the listed rows 1..w_b, once the selection (and its row list) is complete
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (lane == 0) gtime(a, 2);
     const long long total = (long long)__ldcg(a.rowmap) * nch;
     if (lane == 0 && total <= (long long)kStaticItems * gridDim.x) {
       // small calls: a static schedule (items blockIdx.x + x * G) with every row lookup issued up front
-      const uint64_t pol = l2_evict_first_policy();
-      const int G = gridDim.x;
       int rm[kStaticItems];
 #pragma unroll
       for (int x = 0; x < kStaticItems; ++x) {
         const long long i = blockIdx.x + (long long)x * G;
         rm[x] = i < total ? __ldcg(a.rowmap + 1 + i / nch) : 0;
       }
-      int t = 0;
 #pragma unroll
       for (int x = 0; x < kStaticItems; ++x) {
         const long long i = blockIdx.x + (long long)x * G;
         if (i >= total) break;
-        const int s = t % kGStages;
-        if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
-        const int b = rm[x] >> 8, j = rm[x] & 0xFF, cc = (int)(i % nch);
-        const int row = b * (k + 1) + j;
-        const int n = min(kChunkElems, V - cc * kChunkElems);
-        const uint32_t bytes = (uint32_t)n * sizeof(float);
-        sh.meta[s] = GMeta{b, row, cc, 0};
-        mbar_arrive_expect_tx(&sh.full[s], bytes);
-        bulk_g2s_stream(stage_mem + s * kGStageBytes, a.p + (int64_t)row * V + (int64_t)cc * kChunkElems, bytes,
-                        &sh.full[s], pol);
-        ++t;
+        const int b = rm[x] >> 8, j = rm[x] & 0xFF;
+        issue(b, b * (k + 1) + j, (int)(i % nch), 0);
       }
-      const int s = t % kGStages;
-      if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
-      sh.meta[s] = GMeta{-1, 0, 0, 0};
-      mbar_arrive(&sh.full[s]);
     } else if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy();
       // Items are claimed kClaim at a time, one claim ahead: the counter's and the row map's round trips (each up to
       // ~1 us under full HBM load) overlap the copies of a whole claim instead of one 32 KB chunk each.
       // small calls (fewer than 16 items per CTA) claim one item at a time, so every SM gets a share
@@ -224,25 +261,14 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
 #pragma unroll
       for (int x = 0; x < kClaim; ++x)
         rm_cur[x] = (x < claim && c_cur + x < total) ? __ldcg(a.rowmap + 1 + (c_cur + x) / nch) : 0;
-      int t = 0;
       while (c_cur < total) {
         const long long c_next = (long long)atomicAdd(work, (unsigned long long)claim);
 #pragma unroll
         for (int x = 0; x < kClaim; ++x) {
           const long long i = c_cur + x;
           if (x < claim && i < total) {
-            const int s = t % kGStages;
-            if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
-            const int rm = rm_cur[x];
-            const int b = rm >> 8, j = rm & 0xFF, cc = (int)(i % nch);
-            const int row = b * (k + 1) + j;
-            const int n = min(kChunkElems, V - cc * kChunkElems);
-            const uint32_t bytes = (uint32_t)n * sizeof(float);
-            sh.meta[s] = GMeta{b, row, cc, 0};
-            mbar_arrive_expect_tx(&sh.full[s], bytes);
-            bulk_g2s_stream(stage_mem + s * kGStageBytes, a.p + (int64_t)row * V + (int64_t)cc * kChunkElems, bytes,
-                     &sh.full[s], pol);
-            ++t;
+            const int b = rm_cur[x] >> 8, j = rm_cur[x] & 0xFF;
+            issue(b, b * (k + 1) + j, (int)(i % nch), 0);
           }
           if (x == (claim > 1 ? 1 : 0)) {  // copies issued: fetch the next claim's rows (waits for the counter)
 #pragma unroll
@@ -254,11 +280,13 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
 #pragma unroll
         for (int x = 0; x < kClaim; ++x) rm_cur[x] = rm_nx[x];
       }
-      // end of stream: a sentinel stage without data
+    }
+    if (lane == 0) {  // end of stream: a sentinel stage without data
       const int s = t % kGStages;
       if (t >= kGStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kGStages) & 1) ^ 1u));
       sh.meta[s] = GMeta{-1, 0, 0, 0};
       mbar_arrive(&sh.full[s]);
+      gtime(a, 3);
     }
     __syncwarp();
   } else if (warp < kGConsumers) {
@@ -290,6 +318,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   } else {
     // publisher: one chunk per iteration; arrivals on the per-request counters batched behind one release fence
     int pend_b = 0, npend = 0;
+    bool waited = false;
     auto flush = [&]() {
       if (npend == 0) return;
       __syncwarp();
@@ -306,7 +335,11 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.ring_free[slot]);
       key = warp_max_u64(key);
-      if (lane == 0) atomicMax(a.keys + m.row, key);
+      if (m.pad == 0 && !waited) {  // the row list's keys were zeroed by the selection: wait for it once
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+      }
+      if (lane == 0) atomicMax(m.pad ? a.key0 + m.b : a.keys + m.row, key);
       if (lane == npend) pend_b = m.b;
       if (++npend == 32) flush();
     }
@@ -315,6 +348,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
 
   // one warp per request as soon as its (w_b + 1) * nch chunks are in
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // windows (no-op by now)
   constexpr int kWarps = kGThreads / 32;
   for (int b = warp * G + blockIdx.x; b < a.B; b += G * kWarps) {
     int w = a.windows[b];
@@ -335,7 +369,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
     int acc = w, tok = -1;
     for (int j0 = 0; j0 <= w; j0 += 32) {
       const int j = j0 + lane;
-      const int am = j <= w ? (int)~(uint32_t)__ldcg(kb + j) : -1;
+      const int am = j <= w ? (int)~(uint32_t)__ldcg(j == 0 ? a.key0 + b : kb + j) : -1;
       const int t = j < w ? a.d[(int64_t)b * k + j] : 0;
       const unsigned mis = __ballot_sync(kFull, j < w && t != am);
       if (mis) {
@@ -349,6 +383,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       if (w < j0 + 32) tok = __shfl_sync(kFull, am, w - j0);  // all accepted: the bonus position's argmax
     }
     if (lane == 0) {
+      a.key0[b] = 0ull;  // read above (lane 0, j = 0): ready for the next launch
       a.accepted[b] = acc;
       a.out_tok[b] = tok;
       set_status(a.status, bad);
@@ -356,6 +391,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   }
 
   // the last CTA out resets the work counter and, when asked to, compacts the emitted tokens
+  if (tid == 0) gtime(a, 4);
   __threadfence();
   __syncthreads();
   if (tid == 0) {
@@ -363,6 +399,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
     const bool last = atomicAdd(done, 1u) == (unsigned)G - 1;
     if (last) {
       *work = 0ull;
+      *reinterpret_cast<unsigned long long*>(a.grid_bar2) = 0ull;
       *done = 0u;
       __threadfence();
     }
@@ -421,9 +458,9 @@ static int launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaSt
   return abi::launch_check();
 }
 
-int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys,
+int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys, int j0,
                          cudaStream_t st) {
-  void* args[] = {(void*)&windows, (void*)&B, (void*)&k, (void*)&rowmap, (void*)&keys};
+  void* args[] = {(void*)&windows, (void*)&B, (void*)&k, (void*)&rowmap, (void*)&keys, (void*)&j0};
   return launch_pdl((const void*)greedy_rowmap_kernel, dim3(1), dim3(1024), 0, st, args);
 }
 
@@ -441,6 +478,7 @@ int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st) {
   const long long items = (long long)a.B * (a.k + 1) * a.nch;
   const int grid = (int)(items < num_sms ? items : num_sms);
   GreedyArgs copy = a;
+  copy.dbg = debug_buffer();
   void* args[] = {(void*)&copy};
   return launch_pdl((const void*)persist_greedy_kernel, dim3(grid), dim3(kGThreads), kGSmem, st, args);
 }

@@ -90,6 +90,9 @@ struct GreedyArgs {
   int B, k, V, nch;
   const int32_t* rowmap;      // [0]: listed-row count, then b << 8 | j
   unsigned long long* keys;   // [B][k+1] argmax keys of the listed rows (zeroed by the row-map kernel)
+  unsigned long long* key0;   // [B] argmax keys of row 0 (streamed before the selection; zero, left at zero)
+  unsigned* grid_bar2;        // [0..1]: 64-bit counter of the row-0 items (zero, left at zero)
+  long long* dbg;             // diagnostics: per-CTA %globaltimer stamps at dbg[64 + 8 * cta + slot] (nullptr: off)
   int* req_cnt;               // [B] per-request published-chunk counters (zero, left at zero)
   unsigned* grid_bar;         // [0]: CTAs done, [2..3]: 64-bit work counter (zero, left at zero)
   int32_t* accepted;
@@ -107,7 +110,7 @@ size_t gselect_scratch_bytes();
 int launch_persist_stream(const StreamArgs& a, cudaStream_t st);
 bool persist_eligible(const float* p, const float* q, int V);
 bool persist_greedy_eligible(const float* p, int V);
-int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys,
+int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys, int j0,
                          cudaStream_t st);
 int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st);
 int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,

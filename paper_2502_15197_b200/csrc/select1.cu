@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
 #pragma unroll
       for (int x = 0; x < RPT; ++x) w = (r0 + x == f + i) ? wr[x] : w;
       wl[i] = i < nb ? w : 0;
-      my += i < nb ? w + 1 : 0;
+      my += i < nb ? w : 0;  // rows 1..w (row 0 of every request is streamed before the selection completes)
     }
     long long rtot;
     const long long roff = block_excl_scan<long long>(my, sh.tmp, rtot);

@@ -630,7 +630,7 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
   int32_t* rowmap = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWMAP);
   if (persist_greedy_eligible(p, V)) {
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(av);
-    if ((rc = launch_greedy_rowmap(windows, B, k, rowmap, keys, st))) return rc;
+    if ((rc = launch_greedy_rowmap(windows, B, k, rowmap, keys, 1, st))) return rc;
     GreedyArgs a = {};
     a.p = p;
     a.d = d;
@@ -642,6 +642,8 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
     a.nch = n_chunks(V);
     a.rowmap = rowmap;
     a.keys = keys;
+    a.key0 = (unsigned long long*)(cnt + abi::kSlotGreedyKey0);
+    a.grid_bar2 = (unsigned*)cnt + abi::kSlotWorkSpec;
     a.req_cnt = cnt;
     a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
     a.accepted = accepted;
@@ -651,7 +653,7 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
     a.status = status;
     return launch_persist_greedy(a, st);
   }
-  if ((rc = launch_greedy_rowmap(windows, B, k, rowmap, nullptr, st))) return rc;
+  if ((rc = launch_greedy_rowmap(windows, B, k, rowmap, nullptr, 0, st))) return rc;
   // one CTA per (selected row, chunk); the selected-row count Σ (w_b + 1) lives on the device, so the grid covers
   // the bound B * (k + 1) and CTAs past the count exit at once
   const long long rows_max = (long long)B * (k + 1);
@@ -712,7 +714,7 @@ extern "C" int tetris_step_greedy_f32(const double* conf, const int32_t* len, in
     sa.gkeys = keys;
   }
   if ((rc = launch_select(sa, st))) return rc;
-  if (!fused_rows && (rc = launch_greedy_rowmap(windows + row0, B, k, rowmap, keys, st))) return rc;
+  if (!fused_rows && (rc = launch_greedy_rowmap(windows + row0, B, k, rowmap, keys, 1, st))) return rc;
   GreedyArgs a = {};
   a.p = p;
   a.d = d;
@@ -724,6 +726,8 @@ extern "C" int tetris_step_greedy_f32(const double* conf, const int32_t* len, in
   a.nch = n_chunks(V);
   a.rowmap = rowmap;
   a.keys = keys;
+  a.key0 = (unsigned long long*)(cnt + abi::kSlotGreedyKey0);
+  a.grid_bar2 = (unsigned*)cnt + abi::kSlotWorkSpec;
   a.req_cnt = cnt;
   a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
   a.accepted = accepted;
