@@ -9,7 +9,7 @@ from paper_2502_15197_b200 import _native as N  # noqa: E402
 from paper_2502_15197_b200 import ops  # noqa: E402
 from paper_2502_15197_b200.synthetic import make_batch  # noqa: E402
 
-B, k, V, C = 1024, 16, 128256, 8192
+B, k, V, C = (int(x) for x in sys.argv[1:5]) if len(sys.argv) >= 5 else (1024, 16, 128256, 8192)
 bt = make_batch(B, k, V, seed=0)
 step = ops.TetrisStep(B, k, V, C)
 dbg = torch.zeros(32, dtype=torch.int64, device='cuda')
