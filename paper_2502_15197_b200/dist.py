@@ -26,6 +26,29 @@ class ShardSelection:
     status: Optional[torch.Tensor] = None
 
 
+def gather_scores(conf_all: torch.Tensor, len_all: torch.Tensor, conf: torch.Tensor, lengths: torch.Tensor,
+                  group=None) -> None:
+    """All-gather every shard's scores and drafted depths into the [W*B, k] / [W*B] buffers.  NCCL: the two
+    all-gathers go out as ONE coalesced NCCL group (one launch, one latency), the selection's only exchange per step;
+    gloo (CPU / single-device tests): the list form."""
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        try:
+            from torch.distributed.distributed_c10d import _coalescing_manager
+        except ImportError:  # older torch: two collectives
+            _coalescing_manager = None
+        if _coalescing_manager is not None:
+            with _coalescing_manager(group=group, device=conf.device):
+                dist.all_gather_into_tensor(conf_all, conf.contiguous(), group=group)
+                dist.all_gather_into_tensor(len_all, lengths.contiguous(), group=group)
+        else:
+            dist.all_gather_into_tensor(conf_all, conf.contiguous(), group=group)
+            dist.all_gather_into_tensor(len_all, lengths.contiguous(), group=group)
+    else:
+        dist.all_gather(list(conf_all.chunk(world)), conf.contiguous(), group=group)
+        dist.all_gather(list(len_all.chunk(world)), lengths.contiguous(), group=group)
+
+
 def _all_gather_rows(t: torch.Tensor, group=None) -> torch.Tensor:
     world = dist.get_world_size(group)
     out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
@@ -44,10 +67,12 @@ def dist_select(conf_local: torch.Tensor, capacity: int, lengths_local: Optional
     the gloo tests inject the CPU oracle to check the exchange logic without a GPU."""
     B_local, k = conf_local.shape
     rank = dist.get_rank(group)
-    conf_all = _all_gather_rows(conf_local, group)
+    world = dist.get_world_size(group)
     if lengths_local is None:
         lengths_local = torch.full((B_local,), k, dtype=torch.int32, device=conf_local.device)
-    len_all = _all_gather_rows(lengths_local.to(torch.int32), group)
+    conf_all = torch.empty((world * B_local, k), dtype=conf_local.dtype, device=conf_local.device)
+    len_all = torch.empty((world * B_local,), dtype=torch.int32, device=conf_local.device)
+    gather_scores(conf_all, len_all, conf_local, lengths_local.to(torch.int32), group)
     if select_fn is None:
         from . import ops
 

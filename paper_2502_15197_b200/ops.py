@@ -439,12 +439,9 @@ class TetrisStep:
         if self.world > 1 and self.group is not None:
             import torch.distributed as dist
 
-            if dist.get_backend(self.group) == "nccl":
-                dist.all_gather_into_tensor(self.conf_all, conf, group=self.group)
-                dist.all_gather_into_tensor(self.len_all, lengths, group=self.group)
-            else:  # gloo (multi-process tests on one device): list form into views of the gathered buffers
-                dist.all_gather(list(self.conf_all.chunk(self.world)), conf.contiguous(), group=self.group)
-                dist.all_gather(list(self.len_all.chunk(self.world)), lengths.contiguous(), group=self.group)
+            from .dist import gather_scores
+
+            gather_scores(self.conf_all, self.len_all, conf, lengths, self.group)  # one coalesced NCCL exchange
             sel_conf, sel_len = self.conf_all, self.len_all
         else:  # world 1, or a shard given the gathered scores directly
             sel_conf, sel_len = conf, lengths
