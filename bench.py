@@ -374,7 +374,8 @@ def _e2e(args, cfg, step_dev, bt, B, k, V, C, mode, group, world, dev):
         small = [t.cpu().pin_memory() for t in (bt.conf, bt.lengths, bt.d, bt.u_acc, bt.u_res)]
     except RuntimeError as e:
         return {"value": None, "unit": "tokens/s", "error": f"pinned host allocation failed: {e}"[:200]}
-    hs = ops.HostTetrisStep(B, k, V, C, p_h, q_h, mode=mode, device=dev)
+    hs = ops.HostTetrisStep(B, k, V, C, p_h, q_h, mode=mode, device=dev,
+                            transfer="staged" if world == 1 else "zero-copy")
     if world > 1:
         hs.step = ops.TetrisStep(B, k, V, C, mode=mode, device=dev, group=group)
     steps = max(3, min(args.steps, 20))
@@ -399,8 +400,10 @@ def _e2e(args, cfg, step_dev, bt, B, k, V, C, mode, group, world, dev):
     del p_h, q_h
     return {"value": toks / (ms / 1e3), "unit": "tokens/s", "steps": steps, "ms_per_step": ms / steps,
             "h2d_bytes_per_step": hs.h2d_bytes() + zero_copy, "d2h_bytes_per_step": hs.d2h_bytes(),
-            "h2d_mode": "explicit copies of conf/lengths/draft tokens/uniforms (%d B) + zero-copy kernel reads of the "
-                        "needed p/q rows from pinned host memory (%d B)" % (hs.h2d_bytes(), zero_copy)}
+            "h2d_mode": ("explicit copies of conf/lengths/draft tokens/uniforms (%d B) + " % hs.h2d_bytes()) + (
+                "DMA copies of the needed p/q rows from pinned host memory after the selection (%d B; the selector's "
+                "accept test reads its scalars through the mapping)" % zero_copy if hs.transfer == "staged" else
+                "zero-copy kernel reads of the needed p/q rows from pinned host memory (%d B)" % zero_copy)}
 
 
 def _cpu_baseline(cfg, bt, step, B, C, args):

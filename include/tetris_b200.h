@@ -184,6 +184,19 @@ int tetris_verify_greedy_compact_f32(const float* p, const int32_t* d, const int
                                      int32_t* offsets, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
                                      tetris_stream_t stream);
 
+/* The stochastic step for HOST-resident p ([B][k+1][V]) and q ([B][k][V]) in pinned, device-mapped memory (the
+ * end-to-end path): selection + accept test reading the scalars it needs through the mapping, then (host waits for
+ * it) one DMA copy per needed row into the device buffer `staging` (>= 2*B rows of V floats) on the copy engines,
+ * then the sampler on device memory.  rowinfo_host: pinned host scratch of 2*B int64.  Same results as
+ * tetris_step_stochastic_f32 with dense uniforms. */
+int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
+                                      const float* p_host, const float* q_host, const int32_t* d,
+                                      const double* u_acc, const double* u_res, const int32_t* cap, int32_t V,
+                                      float* staging, int64_t* rowinfo_host, int32_t* windows, int32_t* win_offsets,
+                                      int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
+                                      int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                      tetris_stream_t stream);
+
 /* The greedy step in 2 launches (select1 with the row-list epilogue, then the persistent argmax stream with the
  * verdicts and the compaction; V % 8 == 0 and 16-byte aligned p, else the stage-by-stage fallback): the selection of
  * tetris_select_f64 over all B_sel rows of conf/len (sharded steps: every shard's scores, gathered) with capacity C,

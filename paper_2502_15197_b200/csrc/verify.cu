@@ -13,6 +13,7 @@
 // Generator.choice inverse CDF (accept_model.py:364,368), apply_verification's first-rejection cascade
 // (sim_engine.py:388-403), bonus token (sim_engine.py:407-409).
 #include <climits>
+#include <vector>
 
 #include "common.cuh"
 #include "launch.h"
@@ -666,6 +667,97 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
                                                           ai, rowmap);
   if ((rc = abi::launch_check())) return rc;
   return offsets ? tetris_compact(accepted, out_tok, d, cap, B, k, offsets, tokens, st) : TETRIS_OK;
+}
+
+// The stochastic step for HOST-resident p / q (the end-to-end path): the selector's accept test gathers its scalars
+// from the mapped host memory; then the row each request resamples from (rowinfo, 16 B per request) comes back to
+// the host, the host queues one DMA copy per needed row into `staging` on the copy engines (which read host memory
+// at ~55 GB/s on this box, vs ~50 for SM-issued zero-copy reads), rewrites rowinfo as staging rows, and the sampler
+// runs on device memory.  Blocking: the host waits for the selection (one stream synchronize).
+extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k,
+                                                 int64_t C, const float* p_host, const float* q_host,
+                                                 const int32_t* d, const double* u_acc, const double* u_res,
+                                                 const int32_t* cap, int32_t V, float* staging,
+                                                 int64_t* rowinfo_host, int32_t* windows, int32_t* win_offsets,
+                                                 int32_t* accepted, int32_t* out_tok, double* mass_out,
+                                                 int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                                 uint32_t* status, void* ws, size_t ws_bytes,
+                                                 tetris_stream_t stream) {
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (!p_host || !q_host || !staging || !rowinfo_host) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (!persist_eligible(staging, staging, V))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "staged step needs V %% 8 == 0 and a 16-byte aligned staging buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  void* p_map = nullptr;
+  void* q_map = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&p_map, (void*)p_host, 0);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&q_map, (void*)q_host, 0);
+  if (e != cudaSuccess) return abi::cuda_fail(e);
+  if ((rc = tetris_select_accept_f32(conf, len, B, k, C, 0, B, (const float*)p_map, (const float*)q_map, d, u_acc, 0,
+                                     cap, V, windows, win_offsets, accepted, offsets, tokens, stats4, status, ws,
+                                     ws_bytes, stream)))
+    return rc;
+  long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+  const size_t ri_bytes = (size_t)B * 2 * sizeof(long long);
+  if ((e = cudaMemcpyAsync(rowinfo_host, rowinfo, ri_bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return abi::cuda_fail(e);
+  // one copy per needed row, in request order; rowinfo rewritten as staging rows
+  const size_t row_bytes = (size_t)V * sizeof(float);
+  std::vector<void*> dsts, srcs;
+  std::vector<size_t> sizes;
+  dsts.reserve(2 * (size_t)B);
+  srcs.reserve(2 * (size_t)B);
+  long long s = 0;
+  for (int b = 0; b < B; ++b) {
+    const long long pr = rowinfo_host[2 * b], qr = rowinfo_host[2 * b + 1];
+    dsts.push_back(staging + s * V);
+    srcs.push_back((void*)(p_host + pr * V));
+    rowinfo_host[2 * b] = s++;
+    if (qr >= 0) {
+      dsts.push_back(staging + s * V);
+      srcs.push_back((void*)(q_host + qr * V));
+      rowinfo_host[2 * b + 1] = s++;
+    }
+  }
+  sizes.assign(dsts.size(), row_bytes);
+  // the copies are spread over kCopyStreams streams (forked from / joined to the caller's stream with events) so
+  // several copy engines work at once and each copy's set-up overlaps the others' transfers
+  constexpr int kCopyStreams = 8;
+  static thread_local cudaStream_t cs[kCopyStreams] = {};
+  static thread_local cudaEvent_t ev[kCopyStreams + 1] = {};
+  if (!cs[0]) {
+    for (int i = 0; i < kCopyStreams; ++i)
+      if ((e = cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking)) != cudaSuccess) return abi::cuda_fail(e);
+    for (int i = 0; i <= kCopyStreams; ++i)
+      if ((e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming)) != cudaSuccess) return abi::cuda_fail(e);
+  }
+  if ((e = cudaEventRecord(ev[kCopyStreams], st)) != cudaSuccess) return abi::cuda_fail(e);
+  const size_t n = dsts.size();
+  for (int i = 0; i < kCopyStreams; ++i) {
+    if ((e = cudaStreamWaitEvent(cs[i], ev[kCopyStreams], 0)) != cudaSuccess) return abi::cuda_fail(e);
+    const size_t lo = n * i / kCopyStreams, hi = n * (i + 1) / kCopyStreams;
+    if (hi > lo) {
+      cudaMemcpyAttributes attr = {};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      size_t attr_idx = 0, fail_idx = 0;
+      e = cudaMemcpyBatchAsync(dsts.data() + lo, srcs.data() + lo, sizes.data() + lo, hi - lo, &attr, &attr_idx, 1,
+                               &fail_idx, cs[i]);
+      if (e != cudaSuccess) {  // older driver: one copy at a time
+        cudaGetLastError();
+        for (size_t j = lo; j < hi; ++j)
+          if ((e = cudaMemcpyAsync(dsts[j], srcs[j], row_bytes, cudaMemcpyHostToDevice, cs[i])) != cudaSuccess)
+            return abi::cuda_fail(e);
+      }
+    }
+    if ((e = cudaEventRecord(ev[i], cs[i])) != cudaSuccess) return abi::cuda_fail(e);
+    if ((e = cudaStreamWaitEvent(st, ev[i], 0)) != cudaSuccess) return abi::cuda_fail(e);
+  }
+  if ((e = cudaMemcpyAsync(rowinfo, rowinfo_host, ri_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return abi::cuda_fail(e);
+  return resample_impl(staging, staging, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out,
+                       tokens, status, ws, ws_bytes, st);
 }
 
 // The greedy step (select -> greedy verification -> compaction) in 2 launches when the selector is the single-CTA one

@@ -574,11 +574,21 @@ class HostTetrisStep:
     `torch.cuda.current_stream().synchronize()` (or `wait()`) before reading `tokens_host`."""
 
     def __init__(self, B: int, k: int, V: int, capacity: int, p_host: torch.Tensor, q_host: torch.Tensor,
-                 mode: str = "stochastic", device="cuda"):
+                 mode: str = "stochastic", device="cuda", transfer: str = "staged"):
+        """transfer: "staged" (stochastic mode: after the selection, the needed rows are copied host->device by the
+        DMA engines, tetris_step_stochastic_staged_f32; the host waits for the selection) or "zero-copy" (the
+        kernels read the rows from pinned host memory; no host wait)."""
+        if transfer not in ("staged", "zero-copy"):
+            raise ValueError(f"transfer must be 'staged' or 'zero-copy', got {transfer!r}")
         self.step = TetrisStep(B, k, V, capacity, mode=mode, device=device)
         dev = self.step.device
+        self.transfer = transfer if mode == "stochastic" else "zero-copy"
+        self.p_host, self.q_host = p_host, q_host
         self.p = _MappedTensor(p_host)
         self.q = _MappedTensor(q_host) if q_host is not None else None
+        if self.transfer == "staged":
+            self.staging = torch.empty(2 * B, V, dtype=torch.float32, device=dev)
+            self.rowinfo_host = torch.empty(2 * B, dtype=_I64).pin_memory()
         self.conf = torch.empty(B, k, dtype=_F64, device=dev)
         self.lengths = torch.empty(B, dtype=_I32, device=dev)
         self.d = torch.empty(B, k, dtype=_I32, device=dev)
@@ -603,7 +613,17 @@ class HostTetrisStep:
         if u_acc_h is not None:
             self.u_acc.copy_(u_acc_h, non_blocking=True)
             self.u_res.copy_(u_res_h, non_blocking=True)
-        self.step.run(self.conf, self.lengths, self.p, self.q, self.d, self.u_acc, self.u_res)
+        if self.transfer == "staged" and self.step.group is None:
+            st = self.step
+            st._check(st._lib.tetris_step_stochastic_staged_f32(
+                self.conf.data_ptr(), self.lengths.data_ptr(), self.B, self.k, st.C, self.p_host.data_ptr(),
+                self.q_host.data_ptr(), self.d.data_ptr(), self.u_acc.data_ptr(), self.u_res.data_ptr(), None,
+                self.V, self.staging.data_ptr(), self.rowinfo_host.data_ptr(), st.windows_all.data_ptr(),
+                st.win_offsets.data_ptr(), st.accepted.data_ptr(), st.out_tok.data_ptr(), st.mass.data_ptr(),
+                st.offsets.data_ptr(), st.tokens.data_ptr(), st.stats.data_ptr(), st.status.data_ptr(), st.ws.ptr,
+                st.ws.nbytes, torch.cuda.current_stream().cuda_stream))
+        else:
+            self.step.run(self.conf, self.lengths, self.p, self.q, self.d, self.u_acc, self.u_res)
         self.offsets_host.copy_(self.step.offsets, non_blocking=True)
         self.tokens_host.copy_(self.step.tokens, non_blocking=True)
         self.accepted_host.copy_(self.step.accepted, non_blocking=True)
