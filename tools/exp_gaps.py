@@ -25,6 +25,13 @@ def sel():
                                  step.status.data_ptr(), ws.ptr, ws.nbytes, s)
 
 
+def sel_only():
+    s = torch.cuda.current_stream().cuda_stream
+    lib.tetris_select_f64(bt.conf.data_ptr(), bt.lengths.data_ptr(), B, k, C, 0, step.windows_all.data_ptr(),
+                          step.win_offsets.data_ptr(), None, step.stats.data_ptr(), step.status.data_ptr(), ws.ptr,
+                          ws.nbytes, s)
+
+
 def res():
     s = torch.cuda.current_stream().cuda_stream
     lib.tetris_resample_f32(bt.p.data_ptr(), bt.q.data_ptr(), bt.u_res.data_ptr(), B, k, V, bt.d.data_ptr(),
@@ -64,6 +71,7 @@ gs = graph_of(sel)
 gr = graph_of(res)
 g2 = graph_of(lambda: (sel(), res()))
 print("graph select                %.2f us" % timeit(gs.replay))
+print("graph select only (no accept epilogue) %.2f us" % timeit(graph_of(sel_only).replay))
 print("graph resample              %.2f us" % timeit(gr.replay))
 print("graph step                  %.2f us" % timeit(g2.replay))
 x = torch.empty(1 << 20, device="cuda")
