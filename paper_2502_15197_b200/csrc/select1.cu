@@ -63,8 +63,10 @@ __device__ void accept_role(const SelectArgs& a, int acta, int nacta) {
   }
 }
 
-template <int RPT>
-__global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs a) {
+// NT threads per CTA: 1024, or 256 / 128 for batches of at most 256 / 128 rows — every phase costs about
+// (instructions per thread) x (warps per scheduler), so a small batch runs faster on fewer, busier threads.
+template <int RPT, int NT = kS1Threads>
+__global__ void __launch_bounds__(NT, 1) select1_kernel(const SelectArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(16) S1Shared sh;
   // programmatic dependent launch: the sampler that follows may be scheduled onto the SMs this grid leaves idle and
@@ -95,23 +97,23 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
   int Lr[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) Lr[i] = (r0 + i < B) ? (a.len ? a.len[r0 + i] : k) : 0;
-  for (int i = tid; i < kS1Bins; i += kS1Threads) sh.hist[0][i] = 0;
+  for (int i = tid; i < kS1Bins; i += NT) sh.hist[0][i] = 0;
   {
     const int n = B * k;
     const bool vec = ((reinterpret_cast<uintptr_t>(a.vals) & 15) == 0) && (n % 2 == 0);
     if (vec) {
       const double2* v2 = reinterpret_cast<const double2*>(a.vals);
       const int n2 = n / 2;
-      for (int e0 = 0; e0 < n2; e0 += 8 * kS1Threads) {
+      for (int e0 = 0; e0 < n2; e0 += 8 * NT) {
         double2 v[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
-          const int e = e0 + x * kS1Threads + tid;
+          const int e = e0 + x * NT + tid;
           v[x] = e < n2 ? __ldg(v2 + e) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
-          const int e = 2 * (e0 + x * kS1Threads + tid);
+          const int e = 2 * (e0 + x * NT + tid);
           if (e < n) {
             int r = e / k, j = e - r * k;
             keys[(size_t)j * KS + r] = (uint64_t)__double_as_longlong(v[x].x);
@@ -121,16 +123,16 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
         }
       }
     } else {
-      for (int e0 = 0; e0 < n; e0 += 16 * kS1Threads) {
+      for (int e0 = 0; e0 < n; e0 += 16 * NT) {
         double v[16];
 #pragma unroll
         for (int x = 0; x < 16; ++x) {
-          const int e = e0 + x * kS1Threads + tid;
+          const int e = e0 + x * NT + tid;
           v[x] = e < n ? __ldg(a.vals + e) : 0.0;
         }
 #pragma unroll
         for (int x = 0; x < 16; ++x) {
-          const int e = e0 + x * kS1Threads + tid;
+          const int e = e0 + x * NT + tid;
           if (e < n) {
             const int r = e / k, j = e - r * k;
             keys[(size_t)j * KS + r] = (uint64_t)__double_as_longlong(v[x]);
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(kS1Threads, 1) select1_kernel(const SelectArgs
       if (pass == 0 && lane == 0) sh.total = (long long)tot;
     } else {
       uint32_t* Hn = sh.hist[(pass + 1) & 1];
-      for (int i = tid - 32; i < kS1Bins; i += kS1Threads - 32) Hn[i] = 0;
+      for (int i = tid - 32; i < kS1Bins; i += NT - 32) Hn[i] = 0;
     }
     __syncthreads();
     if (stamp) a.dbg[11 + 3 * pass] = clock64();
@@ -449,6 +451,7 @@ int launch_select1(const SelectArgs& args_in, cudaStream_t st) {
   SelectArgs a = args_in;
   a.dbg = debug_buffer();
   const int rpt = (a.B + kS1Threads - 1) / kS1Threads;
+  const int nt = a.B <= 128 ? 128 : (a.B <= 256 ? 256 : kS1Threads);
   const size_t smem = (size_t)a.k * ((a.B | 15) + 2) * 8 + 2 * (size_t)a.B;
   int naccept = 0;
   if (a.acc_bytes && a.accept_ctas > 0) {
@@ -460,7 +463,7 @@ int launch_select1(const SelectArgs& args_in, cudaStream_t st) {
       if (num_sms <= 0) num_sms = 148;
     }
     const long long n = (long long)a.ep_rows * a.k;
-    long long want = (n + kS1Threads - 1) / kS1Threads;  // one drafted position (two gathers) per thread
+    long long want = (n + nt - 1) / nt;  // one drafted position (two gathers) per thread
     if (want > num_sms - 1) want = num_sms - 1;
     if (want < 1) want = 1;
     naccept = (int)want;
@@ -471,9 +474,11 @@ int launch_select1(const SelectArgs& args_in, cudaStream_t st) {
   auto launch = [&](auto kern) -> int {
     cudaError_t e = abi::ensure_smem(kern, smem);
     if (e != cudaSuccess) return abi::cuda_fail(e);
-    kern<<<1 + naccept, kS1Threads, smem, st>>>(a);
+    kern<<<1 + naccept, nt, smem, st>>>(a);
     return abi::launch_check();
   };
+  if (nt == 128) return launch(select1_kernel<1, 128>);
+  if (nt == 256) return launch(select1_kernel<1, 256>);
   switch (rpt) {
     case 1:
       return launch(select1_kernel<1>);
