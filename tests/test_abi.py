@@ -68,3 +68,36 @@ def test_no_cpu_fallback_in_product_path():
         assert "import oracle" not in src and "reference_port" not in src, f
     with pytest.raises(ValueError, match="CUDA"):
         ops.select(torch.zeros(2, 2, dtype=torch.float64), 1)
+
+
+def test_workspace_sizes_cover_every_region():
+    """The workspace grows with the batch in every dimension the kernels index, and the fixed counter region (the
+    only part the kernels rely on being zero between calls) sits at the front at a size independent of the shape."""
+    ws = N.workspace_bytes
+    base = ws(N.OP_VERIFY, 1, 1, 8)
+    assert base > 65536 * 4  # per-request counters + speculative-sampler slots + greedy row-0 keys
+    for op in (N.OP_SELECT, N.OP_VERIFY, N.OP_ALL):
+        prev = 0
+        for B in (1, 16, 1024, 4096, 65535):
+            cur = ws(op, B, 16, 128256)
+            assert cur >= prev
+            prev = cur
+    assert ws(N.OP_VERIFY, 1024, 16, 128256) > ws(N.OP_VERIFY, 1024, 8, 128256) > ws(N.OP_VERIFY, 1024, 8, 32000)
+    # the greedy argmax keys (8 B per listed row) fit even with one chunk per row
+    assert ws(N.OP_VERIFY, 1000, 10, 8) - ws(N.OP_VERIFY, 1, 10, 8) >= 999 * 11 * 8
+
+
+def test_batched_entry_points_reject_bad_arguments_without_gpu():
+    """Host-side validation of the product entry points: shapes, null buffers, workspace size."""
+    for call in (
+        lambda: N.call("tetris_step_greedy_f32", None, None, 4, 2, 3, 0, 4, None, None, None, 128, None, None, None,
+                       None, None, None, None, None, None, 0, None),
+        lambda: N.call("tetris_verify_greedy_compact_f32", 1, 1, 1, None, 4, 2, 128, 1, 1, None, 1, None, None, 0,
+                       None),
+        lambda: N.call("tetris_resample_spec_f32", 1, 1, 1, None, None, 4, 2, 128, None, None, None, 1, None, None,
+                       None, None, 0, None),
+        lambda: N.call("tetris_step_stochastic_staged_f32", None, None, 4, 2, 3, None, None, None, None, None, None,
+                       128, None, None, None, None, None, None, None, None, None, None, None, None, 0, None),
+    ):
+        with pytest.raises(ValueError):
+            call()
