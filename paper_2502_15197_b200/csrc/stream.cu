@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // Stage (3) streaming: the persistent, warp-specialised residual / bonus sampler (sm_100a, fp32 rows, V % 8 == 0).
 //
@@ -56,6 +57,7 @@ struct SpecShared {
   uint16_t listB[kSpecMaxR];
   uint64_t listB_ready;          // mbarrier: the planner warp has written listB
   int countA, countB;
+  int own;                       // the phase-A request this CTA streams itself (-1: none)
 };
 
 struct PersistShared {
@@ -292,26 +294,34 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
     // is appended to the global phase-A list (entry b + 1; 0 = not written yet) and its bit set in the global set;
     // then the CTA counts its requests as processed (release).  Every CTA starts streaming as soon as list entries
     // appear — no CTA waits for the whole set.
-    const int nmine = blockIdx.x < R ? (R - 1 - (int)blockIdx.x) / G + 1 : 0;
-    if (tid < nmine) {
-      const int b = blockIdx.x + tid * G;
-      const bool drafted = (a.len ? a.len[b] : k) >= 1;
-      const int t = a.d[(int64_t)b * k];
-      const double u = a.u_acc[(int64_t)b * k];
+    const int nmine = blockIdx.x < R ? (R - 1 - (int)blockIdx.x) / G + 1 : 0;  // <= 32 (host-checked)
+    if (warp == 0) {
+      const int b = blockIdx.x + lane * G;
       bool rej = false;
-      if (drafted) {
-        if (t < 0 || t >= a.V) {
-          rej = true;
-        } else {
-          const double s = (double)a.q[(int64_t)b * k * a.V + t];
-          const double m = (double)a.p[(int64_t)b * (k + 1) * a.V + t];
-          rej = !((s <= m) || (u < m / s));
+      if (lane < nmine) {
+        const bool drafted = (a.len ? a.len[b] : k) >= 1;
+        const int t = a.d[(int64_t)b * k];
+        const double u = a.u_acc[(int64_t)b * k];
+        if (drafted) {
+          if (t < 0 || t >= a.V) {
+            rej = true;
+          } else {
+            const double s = (double)a.q[(int64_t)b * k * a.V + t];
+            const double m = (double)a.p[(int64_t)b * (k + 1) * a.V + t];
+            rej = !((s <= m) || (u < m / s));
+          }
         }
       }
+      // the first of them the CTA streams itself, straight away (no list round trips before its first copy)
+      const unsigned rj = __ballot_sync(kFull, rej);
+      const int own = rj ? __ffs(rj) - 1 : -1;
+      if (lane == 0) sx.own = own >= 0 ? (int)blockIdx.x + own * G : -1;
       if (rej) {
-        const int pos = atomicAdd(a.spec_ctl, 1);
         atomicOr(a.spec_bitmap + (b >> 5), 1u << (b & 31));
-        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.spec_list + pos), "r"(b + 1) : "memory");
+        if (lane != own) {
+          const int pos = atomicAdd(a.spec_ctl, 1);
+          asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.spec_list + pos), "r"(b + 1) : "memory");
+        }
       }
     }
     __syncthreads();
@@ -354,6 +364,13 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           }
         };
         int t = 0;
+        if (sx.own >= 0) {
+          const int b = sx.own;
+          for (int cc = 0; cc < nch; ++cc) {
+            if (t == 0) gstamp(a, 2);
+            issue_item(a, sh, stage_mem, t++, b, cc, (long long)b * (k + 1), (long long)b * k, 1, pol);
+          }
+        }
         long long i_cur = (long long)atomicAdd(work_a, 1ull);
         long long i_nxt = (long long)atomicAdd(work_a, 1ull);
         int b_cur = entry(i_cur);
@@ -708,7 +725,9 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
   }
   const bool spec = a.u_acc != nullptr && a.req_cnt != nullptr;
   if (spec && (a.R > kSpecMaxR || !a.req_cnt_spec || !a.chunk_sums_spec || !a.warp_sums_spec || !a.d ||
-               !a.spec_ctl || !a.spec_bitmap || !a.spec_list))
+               !a.spec_ctl || !a.spec_bitmap || !a.spec_list ||
+               (a.R + (int)std::min<long long>((long long)a.R * a.nch, g_num_sms) - 1) /
+                       (int)std::min<long long>((long long)a.R * a.nch, g_num_sms) > 32))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "speculative sampler: R=%d > %d or missing buffers", a.R, kSpecMaxR);
   const void* fn = spec ? (const void*)persist_stream_kernel<true> : (const void*)persist_stream_kernel<false>;
   cudaError_t e = abi::ensure_smem(fn, kPersistSmem);
