@@ -241,8 +241,13 @@ def run_tetris(args):
         a = step.accepted.cpu().numpy().astype(np.int64)
         bytes_per_set.append(_verify_bytes(cfg, w, a))
 
-    # CUDA graphs: one captured step per input set (single GPU; the NCCL exchange of N>1 stays eager)
+    # CUDA graphs (single GPU; the NCCL exchange of N>1 stays eager): one captured step per input set, plus one graph
+    # of M consecutive steps over the rotating sets (M a multiple of the set count, >= --graph-steps) so that the
+    # per-replay launch cost is paid once per M steps; the timed loop replays the M-step graph while >= M steps remain
+    # (aligned with the rotation) and single-step graphs for the rest, so exactly K steps run
     graphs = []
+    multi = None
+    M = 1
     use_graph = args.graph and world == 1
     if use_graph:
         cs = torch.cuda.Stream()
@@ -257,6 +262,12 @@ def run_tetris(args):
             with torch.cuda.graph(g):
                 run(s)
             graphs.append(g)
+        M = nsets * max(1, -(-args.graph_steps // nsets))
+        if M > 1:
+            multi = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(multi):
+                for j in range(M):
+                    run(j)
         torch.cuda.synchronize()
 
     def step_i(i):
@@ -264,6 +275,17 @@ def run_tetris(args):
             graphs[i % nsets].replay()
         else:
             run(i)
+
+    def steps_from(i0, n):
+        """run steps i0 .. i0+n-1 (multi-step graph replays where the rotation allows)"""
+        i = i0
+        while i < i0 + n:
+            if multi is not None and i % M == 0 and i + M <= i0 + n:
+                multi.replay()
+                i += M
+            else:
+                step_i(i)
+                i += 1
 
     for i in range(args.warmup):
         step_i(i)
@@ -274,8 +296,7 @@ def run_tetris(args):
     t1 = torch.cuda.Event(enable_timing=True)
     w0 = time.time()
     t0.record()
-    for i in range(args.steps):
-        step_i(i)
+    steps_from(0, args.steps)
     t1.record()
     torch.cuda.synchronize()
     w1 = time.time()
@@ -328,7 +349,8 @@ def run_tetris(args):
                        "l2": "rotated input sets larger than L2 together (%.3f GB per set, %d sets)" % (
                            set_bytes / 1e9, nsets),
                        "parallelism": f"request-sharded dp{world}" + (" + NCCL all-gather select" if world > 1 else ""),
-                       "launch": "CUDA graph replay" if use_graph else "eager", "policy": args.policy,
+                       "launch": (f"CUDA graph replay ({M} steps per graph)" if use_graph else "eager"),
+                       "policy": args.policy,
                        "simulated_shard": f"rank 0 of {sim_w} on one GPU (no exchange timed)" if sim_w else None},
             "stage_us": {"select": 1e3 * statistics.median(sel_ms), "verify": 1e3 * statistics.median(ver_ms),
                          "compact": 1e3 * statistics.median(cmp_ms)},
@@ -623,6 +645,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="time eager launches instead of CUDA graphs")
+    ap.add_argument("--graph-steps", type=int, default=8, help="steps captured per CUDA graph (rounded up to a "
+                    "multiple of the input-set count)")
     ap.add_argument("--simulate-world", type=int, default=0,
                     help="on 1 GPU: time rank 0's share of a step sharded over this many ranks (the other ranks' "
                          "gathered scores are this rank's rows reshuffled; no NCCL exchange in the timed region)")
