@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   // one warp per request as soon as its (w_b + 1) * nch chunks are in
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");  // windows (no-op by now)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's selector may be scheduled
   constexpr int kWarps = kGThreads / 32;
   for (int b = warp * G + blockIdx.x; b < a.B; b += G * kWarps) {
     int w = a.windows[b];

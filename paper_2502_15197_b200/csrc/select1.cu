@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(NT, 1) select1_kernel(const SelectArgs a) {
   __shared__ __align__(16) S1Shared sh;
   // programmatic dependent launch: the sampler that follows may be scheduled onto the SMs this grid leaves idle and
   // run its prologue; it reads nothing of ours before its griddepcontrol.wait (= this grid complete and flushed)
+  // launched itself as a programmatic dependent of whatever precedes it (the previous step's sampler lets it be
+  // scheduled early, during its descents): nothing is read or written before that grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (blockIdx.x > 0) {
     accept_role(a, blockIdx.x - 1, gridDim.x - 1);
@@ -474,7 +477,18 @@ int launch_select1(const SelectArgs& args_in, cudaStream_t st) {
   auto launch = [&](auto kern) -> int {
     cudaError_t e = abi::ensure_smem(kern, smem);
     if (e != cudaSuccess) return abi::cuda_fail(e);
-    kern<<<1 + naccept, nt, smem, st>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1 + naccept, 1, 1);
+    cfg.blockDim = dim3(nt, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+    if (e != cudaSuccess) return abi::cuda_fail(e);
     return abi::launch_check();
   };
   if (nt == 128) return launch(select1_kernel<1, 128>);
