@@ -345,7 +345,10 @@ def test_fused_step_full_cfg3_bit_exact():
 # simulated on one GPU: the selection runs over the gathered W*B rows with the global capacity, the verification
 # tensors cover only this rank's rows
 @pytest.mark.parametrize("W,B,k,V,C,rank", [(2, 512, 16, 8192, 8192, 1), (4, 1024, 16, 4096, 32768, 3),
-                                             (8, 1024, 16, 2048, 65536, 5), (2, 300, 7, 4096, 2000, 0)])
+                                             (8, 1024, 16, 2048, 65536, 5), (2, 300, 7, 4096, 2000, 0),
+                                             # >= 4096 streamed chunks: the speculative sampler behind the single-CTA
+                                             # selector (W=2) and behind the grid selector (W=8)
+                                             (2, 512, 16, 65536, 8192, 1), (8, 1024, 4, 32768, 16384, 6)])
 def test_sharded_step_matches_global_selection(W, B, k, V, C, rank):
     shards = [make_batch(B, k, V, seed=100 + r) for r in range(W)]
     conf_all = torch.cat([s.conf for s in shards]).contiguous()
@@ -477,3 +480,38 @@ def test_spec_sampler_matches_oracle(B, k, V, C, seed, ragged):
     assert np.array_equal(off, off_ref) and np.array_equal(toks[: off_ref[-1]], toks_ref)
     if B >= 64:
         assert (w == 0).any() or C >= B  # the window-0 path is exercised where the capacity is tight
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_spec_sampler_random_shapes(seed):
+    """Seeded random shapes through the speculative sampler explicitly (tight and loose capacities, ragged depths,
+    V with a partial last chunk), against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 700))
+    k = int(rng.integers(1, 12))
+    V = int(rng.choice([8, 1000, 8192, 8200, 20000]))
+    V -= V % 8
+    C = int(rng.integers(0, B * k + 2))
+    bt = make_batch(B, k, V, seed=seed, ragged=bool(seed % 2))
+    step = ops.TetrisStep(B, k, V, C)
+    lib = N.load()
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.tetris_select_accept_f32(
+        bt.conf.data_ptr(), bt.lengths.data_ptr(), B, k, C, 0, B, bt.p.data_ptr(), bt.q.data_ptr(), bt.d.data_ptr(),
+        bt.u_acc.data_ptr(), 0, None, V, step.windows_all.data_ptr(), step.win_offsets.data_ptr(),
+        step.accepted.data_ptr(), step.offsets.data_ptr(), step.tokens.data_ptr(), step.stats.data_ptr(),
+        step.status.data_ptr(), step.ws.ptr, step.ws.nbytes, s) == N.OK
+    assert lib.tetris_resample_spec_f32(
+        bt.p.data_ptr(), bt.q.data_ptr(), bt.u_res.data_ptr(), bt.u_acc.data_ptr(), bt.lengths.data_ptr(), B, k, V,
+        bt.d.data_ptr(), step.accepted.data_ptr(), step.offsets.data_ptr(), step.out_tok.data_ptr(),
+        step.mass.data_ptr(), step.tokens.data_ptr(), step.status.data_ptr(), step.ws.ptr, step.ws.nbytes, s) == N.OK
+    torch.cuda.synchronize()
+    w_ref, _, _ = O.select(_np(bt.conf), C, _np(bt.lengths))
+    assert np.array_equal(_np(step.windows), w_ref)
+    acc_ref, tok_ref, mass_ref = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), w_ref, _np(bt.u_acc),
+                                                     _np(bt.u_res), None, nthreads=8)
+    assert np.array_equal(_np(step.accepted), acc_ref) and np.array_equal(_np(step.out_tok), tok_ref)
+    assert np.array_equal(_np(step.mass).view(np.uint64), mass_ref.view(np.uint64))
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
+    assert np.array_equal(_np(step.offsets), off_ref)
+    assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)

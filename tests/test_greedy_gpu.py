@@ -199,3 +199,27 @@ def test_step_greedy_matches_oracle(W, B, k, V, C, rank):
         off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), _np(cap))
         assert np.array_equal(_np(offs), off_ref)
         assert np.array_equal(_np(toks)[: off_ref[-1]], toks_ref)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_step_greedy_random_shapes(seed):
+    """Seeded random shapes through the fused greedy step (row 0 streamed early, rows 1..w from the selector's row
+    list), against the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    B = int(rng.integers(1, 600))
+    k = int(rng.integers(1, 20))
+    V = int(rng.choice([8, 1000, 8192, 8200, 20000]))
+    V -= V % 8
+    C = int(rng.integers(0, B * k + 2))
+    bt = make_batch(B, k, V, seed=seed, mode="greedy", ragged=bool(seed % 2))
+    step = ops.TetrisStep(B, k, V, C, mode="greedy")
+    step.run(bt.conf, bt.lengths, bt.p, None, bt.d)
+    torch.cuda.synchronize()
+    ops.raise_for_status(step.status)
+    w_ref, _, _ = O.select(_np(bt.conf), C, _np(bt.lengths))
+    assert np.array_equal(_np(step.windows), w_ref)
+    acc_ref, tok_ref = O.verify_greedy(_np(bt.p), _np(bt.d), w_ref, nthreads=8)
+    assert np.array_equal(_np(step.accepted), acc_ref) and np.array_equal(_np(step.out_tok), tok_ref)
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
+    assert np.array_equal(_np(step.offsets), off_ref)
+    assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
