@@ -300,8 +300,8 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       bool rej = false;
       if (lane < nmine) {
         const bool drafted = (a.len ? a.len[b] : k) >= 1;
-        const int t = a.d[(int64_t)b * k];
-        const double u = a.u_acc[(int64_t)b * k];
+        const int t = drafted ? a.d[(int64_t)b * k] : 0;
+        const double u = drafted ? a.u_acc[(int64_t)b * k] : 0.0;
         if (drafted) {
           if (t < 0 || t >= a.V) {
             rej = true;

@@ -422,7 +422,8 @@ extern "C" int tetris_verify_stochastic_f32(const float* p, const float* q, cons
   int rc = check_shape(B, k, V);
   if (rc) return rc;
   if (B == 0) return TETRIS_OK;
-  if (!p || !q || !d || !windows || !u_acc || !u_res || !accepted || !out_tok)
+  // with k == 0 nothing is drafted: the [B][0] tensors (d, u_acc) may be null
+  if (!p || (k > 0 && (!d || !u_acc || !q)) || !windows || !u_res || !accepted || !out_tok)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
@@ -479,7 +480,7 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
   if (B_sel < B || B_sel > TETRIS_MAX_SELECT_ROWS || row0 < 0 || row0 + B > B_sel)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "local rows [%d, %d) outside the %d selected rows", row0, row0 + B, B_sel);
   if (u_packed && B != B_sel) return abi::fail(TETRIS_INVALID_ARGUMENT, "packed uniforms need the whole batch");
-  if (!conf || !p || !q || !d || !u_acc || !windows || !win_offsets || !accepted || !offsets || !tokens)
+  if ((k > 0 && (!conf || !d || !u_acc || !q)) || !p || !windows || !win_offsets || !accepted || !offsets || !tokens)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   SelectArgs sa = {};
@@ -525,7 +526,7 @@ static int resample_impl(const float* p, const float* q, const double* u_res, co
   int rc = check_shape(B, k, V);
   if (rc) return rc;
   if (B == 0) return TETRIS_OK;
-  if (!p || !q || !u_res || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (!p || (k > 0 && !q) || !u_res || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   if (!persist_eligible(p, q, V))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "the streaming sampler needs V %% 8 == 0 and 16-byte aligned p/q");
@@ -552,7 +553,8 @@ static int resample_impl(const float* p, const float* q, const double* u_res, co
   a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
   a.req_cnt = cnt;
   if (tokens) {
-    if (!accepted || !offsets || !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted, offsets, d");
+    if (!accepted || !offsets || (k > 0 && !d))
+      return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens needs accepted, offsets, d");
     a.accepted = accepted;
     a.offsets = offsets;
     a.tokens = tokens;
@@ -584,7 +586,7 @@ extern "C" int tetris_resample_spec_f32(const float* p, const float* q, const do
                                         const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
                                         double* mass_out, int32_t* tokens, uint32_t* status, void* ws,
                                         size_t ws_bytes, tetris_stream_t stream) {
-  if (!u_acc || !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "the speculative sampler needs u_acc and d");
+  if (k > 0 && (!u_acc || !d)) return abi::fail(TETRIS_INVALID_ARGUMENT, "the speculative sampler needs u_acc and d");
   return resample_impl(p, q, u_res, u_acc, len, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status, ws,
                        ws_bytes, (cudaStream_t)stream);
 }
@@ -622,7 +624,8 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
     }
     return TETRIS_OK;
   }
-  if (!p || !d || !windows || !accepted || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (!p || (k > 0 && !d) || !windows || !accepted || !out_tok)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if (offsets && !tokens) return abi::fail(TETRIS_INVALID_ARGUMENT, "tokens is required with offsets");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
@@ -773,7 +776,7 @@ extern "C" int tetris_step_greedy_f32(const double* conf, const int32_t* len, in
   if (B == 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "empty batch");
   if (B_sel < B || B_sel > TETRIS_MAX_SELECT_ROWS || row0 < 0 || row0 + B > B_sel)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "local rows [%d, %d) outside the %d selected rows", row0, row0 + B, B_sel);
-  if (!conf || !p || !d || !windows || !accepted || !out_tok || !offsets || !tokens)
+  if ((k > 0 && (!conf || !d)) || !p || !windows || !accepted || !out_tok || !offsets || !tokens)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   cudaStream_t st = (cudaStream_t)stream;

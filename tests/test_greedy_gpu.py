@@ -223,3 +223,23 @@ def test_step_greedy_random_shapes(seed):
     off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
     assert np.array_equal(_np(step.offsets), off_ref)
     assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
+
+
+@pytest.mark.parametrize("mode", ["greedy", "stochastic"])
+def test_step_zero_draft_depth(mode):
+    """k = 0 (nothing drafted): every window is 0, the emitted token comes from position 0 (the bonus row)."""
+    B, k, V, C = 37, 0, 8192, 5
+    bt = make_batch(B, k, V, seed=3, mode=mode)
+    step = ops.TetrisStep(B, k, V, C, mode=mode)
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    ops.raise_for_status(step.status)
+    assert int(step.windows.abs().sum()) == 0 and int(step.accepted.abs().sum()) == 0
+    if mode == "greedy":
+        _, tok_ref = O.verify_greedy(_np(bt.p), _np(bt.d), np.zeros(B, np.int32), nthreads=8)
+    else:
+        _, tok_ref, _ = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), np.zeros(B, np.int32), _np(bt.u_acc),
+                                            _np(bt.u_res), None, nthreads=8)
+    assert np.array_equal(_np(step.out_tok), tok_ref)
+    assert np.array_equal(_np(step.offsets), np.arange(B + 1, dtype=np.int32))
+    assert np.array_equal(_np(step.tokens)[:B], tok_ref)
