@@ -446,6 +446,26 @@ class TetrisStep:
             sel_conf, sel_len = self.conf_all, self.len_all
         else:  # world 1, or a shard given the gathered scores directly
             sel_conf, sel_len = conf, lengths
+        if self.mode == "stochastic" and V % 8 != 0:
+            # the TMA sampler needs 32-byte rows (V % 8 == 0): the stage-by-stage kernels serve any V
+            self._check(lib.tetris_select_f64(sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, 0,
+                                              self.windows_all.data_ptr(), self.win_offsets.data_ptr(), None,
+                                              self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+            if events is not None:
+                events[1].record()
+            packed = self.u_layout == "packed"
+            self._check(lib.tetris_verify_stochastic_f32(
+                p.data_ptr(), q.data_ptr(), _ptr(d), self.windows.data_ptr(),
+                self.win_offsets.data_ptr() if packed else None, _ptr(u_acc), u_res.data_ptr(), B, k, V,
+                self.accepted.data_ptr(), self.out_tok.data_ptr(), self.mass.data_ptr(), self.status.data_ptr(),
+                ws.ptr, ws.nbytes, s))
+            if events is not None:
+                events[2].record()
+            self._check(lib.tetris_compact(self.accepted.data_ptr(), self.out_tok.data_ptr(), _ptr(d), _ptr(cap), B,
+                                           k, self.offsets.data_ptr(), self.tokens.data_ptr(), s))
+            if events is not None:
+                events[3].record()
+            return
         if self.mode == "stochastic":
             # == tetris_step_stochastic_f32, called as its two halves so an event can sit between the kernels
             rc = lib.tetris_select_accept_f32(
@@ -550,7 +570,7 @@ class TetrisStep:
         if self.policy == "fixed":
             return 4 if self.mode == "stochastic" else 3
         if self.mode == "stochastic":
-            return 2
+            return 2 if self.V % 8 == 0 else 3  # V % 8 != 0: select, verify (one sample_kernel), compact
         return 2 if self.Bg * self.k <= 16384 and self.Bg <= 4096 else 3
 
 

@@ -515,3 +515,23 @@ def test_spec_sampler_random_shapes(seed):
     off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
     assert np.array_equal(_np(step.offsets), off_ref)
     assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
+
+
+@pytest.mark.parametrize("V", [1003, 13, 8191])
+def test_step_stochastic_any_vocabulary(V):
+    """V % 8 != 0: TetrisStep runs the stage-by-stage kernels (the TMA sampler needs 32-byte rows); same results as
+    the oracle."""
+    B, k, C = 90, 5, 200
+    bt = make_batch(B, k, V, seed=V, ragged=True)
+    step = ops.TetrisStep(B, k, V, C)
+    assert step.launches_per_step == 3
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    ops.raise_for_status(step.status)
+    w_ref, _, _ = O.select(_np(bt.conf), C, _np(bt.lengths))
+    acc_ref, tok_ref, mass_ref = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), w_ref, _np(bt.u_acc),
+                                                     _np(bt.u_res), None, nthreads=8)
+    assert np.array_equal(_np(step.accepted), acc_ref) and np.array_equal(_np(step.out_tok), tok_ref)
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
+    assert np.array_equal(_np(step.offsets), off_ref)
+    assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
