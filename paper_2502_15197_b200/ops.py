@@ -603,7 +603,8 @@ class HostTetrisStep:
             raise ValueError(f"transfer must be 'staged' or 'zero-copy', got {transfer!r}")
         self.step = TetrisStep(B, k, V, capacity, mode=mode, device=device)
         dev = self.step.device
-        self.transfer = transfer if mode == "stochastic" else "zero-copy"
+        # the staged path feeds the TMA sampler (32-byte rows): other vocabulary sizes read through the mapping
+        self.transfer = transfer if (mode == "stochastic" and V % 8 == 0) else "zero-copy"
         self.p_host, self.q_host = p_host, q_host
         self.p = _MappedTensor(p_host)
         self.q = _MappedTensor(q_host) if q_host is not None else None

@@ -18,7 +18,7 @@ def _np(t):
 
 @pytest.mark.parametrize("mode,transfer", [("stochastic", "staged"), ("stochastic", "zero-copy"),
                                            ("greedy", "zero-copy")])
-@pytest.mark.parametrize("B,k,V,C", [(64, 8, 16384, 200), (200, 5, 8200, 500)])
+@pytest.mark.parametrize("B,k,V,C", [(64, 8, 16384, 200), (200, 5, 8200, 500), (40, 3, 1003, 60)])
 def test_host_step_matches_device_step(mode, transfer, B, k, V, C):
     bt = make_batch(B, k, V, seed=B + k, mode=mode, ragged=True)
     dev_step = ops.TetrisStep(B, k, V, C, mode=mode)
