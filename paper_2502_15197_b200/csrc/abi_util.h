@@ -42,15 +42,18 @@ template <typename K>
 inline cudaError_t ensure_smem(K kernel, size_t bytes) {
   struct Entry {
     const void* fn;
+    int dev;  // the attribute is per device
     size_t max;
   };
   static Entry table[64];
   static std::mutex mu;  // host threads may launch concurrently (the ABI is reentrant)
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   const void* fn = reinterpret_cast<const void*>(kernel);
   int slot = -1;
   for (int i = 0; i < 64; ++i) {
-    if (table[i].fn == fn) {
+    if (table[i].fn == fn && table[i].dev == dev) {
       if (table[i].max >= bytes) return cudaSuccess;
       slot = i;
       break;
@@ -61,7 +64,7 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes) {
     }
   }
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess && slot >= 0) table[slot] = Entry{fn, bytes};
+  if (e == cudaSuccess && slot >= 0) table[slot] = Entry{fn, dev, bytes};
   return e;
 }
 
