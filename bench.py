@@ -314,9 +314,9 @@ def run_tetris(args):
     # events around each whole step, eager, median over the steps
     lat = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(min(args.steps, 200))]
-    for i, (ea, eb) in enumerate(lat):
+    for j, (ea, eb) in enumerate(lat):  # the last K steps' sets, so the run ends on step K-1's set (checked below)
         ea.record()
-        run(i)
+        run(args.steps - len(lat) + j)
         eb.record()
     torch.cuda.synchronize()
     step_lat_ms = [ea.elapsed_time(eb) for ea, eb in lat]
