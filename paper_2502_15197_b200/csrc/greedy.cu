@@ -6,10 +6,14 @@
 // emitted token is the argmax at the first mismatch, or at w_b (the bonus position, sim_engine.py:407-409).  Every
 // selected row 0..w_b is read in full once: HBM-bound, (Σ_b (w_b + 1)) · V · 4 bytes per call.
 //
-// greedy_rowmap_kernel (one CTA) lists those rows in request order and zeroes their argmax keys; then
-// persist_greedy_kernel, one CTA per SM, 18 warps:
-//   warp 16     producer: takes items (listed row, chunk) in order from one global counter and issues 1-D bulk copies
-//               (cp.async.bulk, mbarrier complete_tx) of 8192-element chunks of p into a 6-stage 192 KB ring;
+// The row list (rows 1..w_b of every request, in request order, their argmax keys zeroed) comes from the selector's
+// epilogue (select1.cu) or from greedy_rowmap_kernel (one CTA); then persist_greedy_kernel, a programmatic dependent
+// of the selector, one CTA per SM, 18 warps:
+//   warp 16     producer: first row 0 of every request — always verified, so it streams before the selection
+//               completes (its keys live in a fixed workspace region, left at zero) — then, after griddepcontrol.wait,
+//               the listed rows; items (row, chunk) claimed 4 at a time from global counters, 1-D bulk copies
+//               (cp.async.bulk, mbarrier complete_tx, L2 evict-first) of 8192-element chunks of p into a 6-stage
+//               192 KB ring;
 //   warps 0..15 consumers: the argmax key of 512 staged elements each (two segments), reduced over the warp;
 //   warp 17     publisher: reduces the 16 keys of a chunk, folds it into the row's key with one atomicMax, and counts
 //               the chunk on the request's arrival counter (one release fence per 32 chunks).
