@@ -482,14 +482,15 @@ def _reference_step_inputs(bt, n):
             "u_res": bt.u_res.cpu().numpy()}
 
 
-def _time_reference(h, C, n, mode, threads):
+def _time_reference(h, C, n, mode, threads, rows=None):
     """One reference step: select_tetris(cumulative_products(conf)) then verify requests [0, n) on `threads`
     threads.  Returns (select seconds, verify seconds, emitted tokens in the sample, None)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import reference_port as RP
 
-    rows = [list(map(float, h["conf"][b, : h["lengths"][b]])) for b in range(h["conf"].shape[0])]
+    if rows is None:
+        rows = [list(map(float, h["conf"][b, : h["lengths"][b]])) for b in range(h["conf"].shape[0])]
     t0 = time.perf_counter()
     windows, _ = RP.select_tetris(RP.cumulative_products(rows), C)
     t1 = time.perf_counter()
@@ -538,12 +539,22 @@ def run_reference(args):
     for key in ("d", "conf", "lengths", "u_acc", "u_res"):
         h[key] = np.concatenate([pt[key] for pt in parts])
     threads = os.cpu_count() or 1
-    for _ in range(max(0, min(args.warmup, 1))):
-        _time_reference(h, C, n, mode, threads)
+    rows = [list(map(float, h["conf"][b, : h["lengths"][b]])) for b in range(h["conf"].shape[0])]
+    ws, wv = 0.0, 0.0
+    for _ in range(max(1, min(args.warmup, 1))):
+        ws, wv, _, _ = _time_reference(h, C, n, mode, threads, rows)
+    # each step's verification sample is sized so the K timed steps take about --ref-budget-s seconds (the full
+    # selection over all requests runs every step; the sample shrinks, not below 8 requests, as K grows)
+    per_req = wv / max(n, 1)
+    n_eff = n
+    if per_req > 0:
+        n_eff = int((args.ref_budget_s / max(args.steps, 1) - ws) / per_req)
+        n_eff = max(min(8, n), min(n, n_eff))
     sel, ver, toks = 0.0, 0.0, 0
     for _ in range(args.steps):
-        a, b, t, _ = _time_reference(h, C, n, mode, threads)
+        a, b, t, _ = _time_reference(h, C, n_eff, mode, threads, rows)
         sel, ver, toks = sel + a, ver + b, toks + t
+    n = n_eff
     scale = Bg / n
     step_s = (sel + ver * scale) / args.steps
     value = (toks / args.steps) * scale / step_s
@@ -657,6 +668,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="time eager launches instead of CUDA graphs")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: about this many seconds for the K timed steps (sets the per-step sample)")
     ap.add_argument("--graph-steps", type=int, default=8, help="steps captured per CUDA graph (rounded up to a "
                     "multiple of the input-set count)")
     ap.add_argument("--simulate-world", type=int, default=0,
