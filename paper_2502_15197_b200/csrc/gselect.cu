@@ -384,8 +384,10 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
 
 bool gselect_shape(int B, int k, int num_sms, int* grid, int* RB) {
   const long long cells = (long long)B * (k > 0 ? k : 1);
-  // cells per CTA: fewer, fuller CTAs leave SMs to the sampler that overlaps the selection (speculative start)
-  long long g = (cells + kGCellsPerCta - 1) / kGCellsPerCta;
+  // cells per CTA: 1024 while that needs at most 64 CTAs (the selection's own latency is lowest with many CTAs),
+  // else 4096 — fewer, fuller CTAs leave SMs to the sampler that overlaps a large gathered selection
+  long long g = (cells + 1023) / 1024;
+  if (g > 64) g = (cells + kGCellsPerCta - 1) / kGCellsPerCta;
   const long long g_rows = (B + kGThreads - 1) / kGThreads;                              // one row per thread
   const long long g_smem = (cells * 9 + (long long)kGKeyBudget - 1) / (long long)kGKeyBudget;  // keys + verdicts
   if (g < g_rows) g = g_rows;
