@@ -158,7 +158,7 @@ int tetris_resample_f32(const float* p, const float* q, const double* u_res, int
 /* tetris_resample_f32 with the speculative start (same results): the rows of requests whose first drafted token is
  * rejected do not depend on the selection, so the kernel finds them itself (verify_token at position 0 with the
  * dense uniforms u_acc[b][0] of the local rows; len: their drafted depths, nullable) and streams them while the
- * preceding tetris_select_accept_f32 is still running; the rest follows the selection.  B <= 2048 (larger batches:
+ * preceding tetris_select_accept_f32 is still running; the rest follows the selection.  B <= 4096 (larger batches:
  * TETRIS_INVALID_ARGUMENT).  tetris_step_stochastic_f32 uses it for dense uniforms. */
 int tetris_resample_spec_f32(const float* p, const float* q, const double* u_res, const double* u_acc,
                              const int32_t* len, int32_t B, int32_t k, int32_t V, const int32_t* d,

@@ -80,11 +80,11 @@ constexpr size_t kSlotGridCount = kRequestSlots + 2;     // grid barrier of the 
 constexpr size_t kSlotGridGen = kRequestSlots + 3;       //   ... and generation
 constexpr size_t kSlotWorkCounter = kRequestSlots + 4;   // the sampler's dynamic work counter (64-bit, 2 slots)
 constexpr size_t kSlotWorkSpec = kRequestSlots + 6;      // the speculative sampler's phase-A counter (64-bit, 2 slots)
-constexpr size_t kSlotSpecCnt = kRequestSlots + 64;      // its per-request completion counters [64 + 0, 64 + 2048)
-constexpr size_t kSpecSlots = 2048;
+constexpr size_t kSlotSpecCnt = kRequestSlots + 64;      // its per-request completion counters [64 + 0, 64 + 4096)
+constexpr size_t kSpecSlots = 4096;
 constexpr size_t kSlotSpecCtl = kRequestSlots + 8;       // [2]: phase-A list length, requests processed
-constexpr size_t kSlotSpecBitmap = kSlotSpecCnt + kSpecSlots;   // [64]: the phase-A set
-constexpr size_t kSlotSpecList = kSlotSpecBitmap + 64;          // [2048]: the phase-A list
+constexpr size_t kSlotSpecBitmap = kSlotSpecCnt + kSpecSlots;   // [kSpecSlots / 32]: the phase-A set
+constexpr size_t kSlotSpecList = kSlotSpecBitmap + kSpecSlots / 32;  // [kSpecSlots]: the phase-A list
 constexpr size_t kSlotGreedyKey0 = kSlotSpecList + kSpecSlots;  // [2 * 65536]: greedy row-0 argmax keys (u64)
 constexpr size_t kCounterSlots = kSlotGreedyKey0 + 2 * kRequestSlots;
 static_assert(kSlotGreedyKey0 % 2 == 0, "8-byte aligned greedy row-0 keys");

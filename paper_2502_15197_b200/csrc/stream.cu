@@ -53,7 +53,7 @@ struct StageMeta {
   int b, c, res, phase;  // phase 1: speculative (phase A) item
 };
 
-constexpr int kSpecMaxR = 2048;  // speculative variant: requests per call (lists in shared memory)
+constexpr int kSpecMaxR = 4096;  // speculative variant: requests per call (lists in shared memory)
 
 struct SpecShared {
   uint32_t inA[kSpecMaxR / 32];  // phase-A set (first drafted token rejected), copied by the planner

@@ -370,7 +370,7 @@ def compact(accepted: torch.Tensor, out_tok: torch.Tensor, d: torch.Tensor, cap:
 # ---------------------------------------------------------------------------------------------------------------
 # one full verification step with preallocated buffers (CUDA-graph capturable)
 # ---------------------------------------------------------------------------------------------------------------
-SPEC_MAX_REQUESTS = 2048  # tetris_resample_spec_f32's limit (per call, local rows)
+SPEC_MAX_REQUESTS = 4096  # tetris_resample_spec_f32's limit (per call, local rows)
 # below this much streaming the early start does not pay (csrc/verify.cu kSpecMinChunks); env override for A/B runs
 SPEC_MIN_CHUNKS = int(os.environ.get("TETRIS_SPEC_MIN_CHUNKS", "4096"))
 _NO_SPEC = os.environ.get("TETRIS_NO_SPEC") == "1"  # A/B timing switch: the plain sampler

@@ -430,6 +430,7 @@ def test_sampler_adversarial_rows_f32():
 # requests it streams for nothing (window 0), empty rows, out-of-vocabulary first tokens, repeated calls
 @pytest.mark.parametrize("B,k,V,C,seed,ragged", [(64, 4, 8200, 10, 1, True), (300, 6, 4096, 40, 2, True),
                                                   (1024, 16, 32000, 8192, 3, False), (2048, 3, 1024, 3000, 4, True),
+                                                  (4096, 2, 1024, 5000, 6, True),
                                                   (5, 2, 8, 3, 5, False)])
 def test_spec_sampler_matches_oracle(B, k, V, C, seed, ragged):
     bt = make_batch(B, k, V, seed=seed, ragged=ragged)
