@@ -1,4 +1,4 @@
-"""CPU: the committed bench lines (profiles/r1j_bench*.json, produced by bench.py on a B200) carry every key of the
+"""CPU: the committed bench lines (profiles/r1k_bench*.json, produced by bench.py on a B200) carry every key of the
 benchmark contract, with consistent values; and bench.py's reference arm prints its line here (the oracle port on
 the host cores, no GPU needed)."""
 import json
@@ -9,7 +9,7 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
-LINES = sorted((ROOT / "profiles").glob("r1j_bench*.json"))
+LINES = sorted((ROOT / "profiles").glob("r1k_bench*.json"))
 
 
 def _load(p):
