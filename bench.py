@@ -311,13 +311,15 @@ def run_tetris(args):
         run(i, ev[i])
     torch.cuda.synchronize()
     # per-step latency as the product runs it (no event between the launches, so the sampler overlaps the selector):
-    # events around each whole step, eager, median over the steps
+    # events around each whole step, one step in flight at a time, median over the steps
     lat = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(min(args.steps, 200))]
     for j, (ea, eb) in enumerate(lat):  # the last K steps' sets, so the run ends on step K-1's set (checked below)
+        i = args.steps - len(lat) + j
         ea.record()
-        run(args.steps - len(lat) + j)
+        step_i(i)  # one step, as the timed loop launches it (a one-step graph replay when graphs are on)
         eb.record()
+        eb.synchronize()  # one step at a time: its latency, not the throughput of a queue of steps
     torch.cuda.synchronize()
     step_lat_ms = [ea.elapsed_time(eb) for ea, eb in lat]
     sel_ms = [e[0].elapsed_time(e[1]) for e in ev]
