@@ -9,17 +9,19 @@ draws the same index as numpy's Generator.choice for the same uniform up to last
 from __future__ import annotations
 
 import math
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
 import numpy as np
 import torch
 
-from . import ops
+from . import _types, ops
 from .errors import DegenerateResidualError
 
 __all__ = ["AcceptanceMatrix", "TokenDistribution", "DegenerateResidualError", "verify_token",
-           "residual_distribution", "sample_emitted_token", "verify_tokens_batch"]
+           "residual_distribution", "sample_emitted_token", "verify_tokens_batch", "matrix_to_device"]
 
 
 def _device():
@@ -57,13 +59,20 @@ class AcceptanceMatrix:
 
     def to_device(self, device=None):
         """Dense [B, k] f64 (zero padded) + lengths [B] i32 on the GPU."""
-        dev = device or _device()
-        k = max((len(r) for r in self.rows), default=0)
-        a = np.zeros((len(self.rows), max(k, 1)), np.float64)
-        for i, r in enumerate(self.rows):
-            a[i, : len(r)] = r
-        ln = np.array([len(r) for r in self.rows], np.int32)
-        return torch.from_numpy(a).to(dev), torch.from_numpy(ln).to(dev)
+        return matrix_to_device(self, device)
+
+
+def matrix_to_device(matrix, device=None):
+    """Any object with `.rows` (this package's AcceptanceMatrix or tetris_sched's) -> dense [B, k] f64 (zero padded)
+    + lengths [B] i32 on the GPU."""
+    rows = matrix.rows
+    dev = device or _device()
+    k = max((len(r) for r in rows), default=0)
+    a = np.zeros((len(rows), max(k, 1)), np.float64)
+    for i, r in enumerate(rows):
+        a[i, : len(r)] = r
+    ln = np.array([len(r) for r in rows], np.int32)
+    return torch.from_numpy(a).to(dev), torch.from_numpy(ln).to(dev)
 
 
 class TokenDistribution:
@@ -88,15 +97,41 @@ class TokenDistribution:
         return int(self.probs.size)
 
 
+for _name, _cls in (("AcceptanceMatrix", AcceptanceMatrix), ("TokenDistribution", TokenDistribution),
+                   ("DegenerateResidualError", DegenerateResidualError)):
+    _types.set_default(_name, _cls)
+
+
 def _check_pair(p_draft: TokenDistribution, p_target: TokenDistribution) -> None:
     if p_draft.vocab_size != p_target.vocab_size:
         raise ValueError(
             f"vocabulary mismatch: draft {p_draft.vocab_size} vs target {p_target.vocab_size}")
 
 
+_row_cache: "OrderedDict[int, tuple]" = OrderedDict()
+_ROW_CACHE_MAX = 64
+
+
+def _device_row(arr, dev) -> torch.Tensor:
+    """[1, V] f64 device copy of a distribution's probability vector.  Read-only vectors (TokenDistribution marks
+    them so, accept_model.py:276) are immutable, so their device copy is cached by identity (a weak reference
+    guards against id reuse): Monte Carlo callers that verify 10^6 tokens against one pair copy it once."""
+    if isinstance(arr, np.ndarray) and not arr.flags.writeable:
+        hit = _row_cache.get(id(arr))
+        if hit is not None and hit[0]() is arr and hit[1].device == dev:
+            _row_cache.move_to_end(id(arr))
+            return hit[1]
+        t = torch.from_numpy(np.array(arr, np.float64)).view(1, -1).to(dev)
+        _row_cache[id(arr)] = (weakref.ref(arr), t)
+        if len(_row_cache) > _ROW_CACHE_MAX:
+            _row_cache.popitem(last=False)
+        return t
+    return torch.from_numpy(np.array(arr, np.float64)).view(1, -1).to(dev)
+
+
 def _rows(*dists: TokenDistribution):
     dev = _device()
-    return [torch.from_numpy(np.array(d.probs)).view(1, -1).to(dev) for d in dists]
+    return [_device_row(d.probs, dev) for d in dists]
 
 
 def verify_token(p_draft: TokenDistribution, p_target: TokenDistribution, token: int, u: float) -> bool:
@@ -124,8 +159,11 @@ def residual_distribution(p_draft: TokenDistribution, p_target: TokenDistributio
     _check_pair(p_draft, p_target)
     ps, pt = _rows(p_draft, p_target)
     out, mass, st = ops.residual(ps, pt)
-    ops.raise_for_status(st, "residual_distribution")  # DegenerateResidualError when the mass is 0
-    return TokenDistribution(out[0].cpu().numpy())
+    try:
+        ops.raise_for_status(st, "residual_distribution")  # DegenerateResidualError when the mass is 0
+    except DegenerateResidualError as e:
+        raise _types.get("DegenerateResidualError")(str(e)) from None
+    return _types.get("TokenDistribution")(out[0].cpu().numpy())
 
 
 def _sample(dist_row: torch.Tensor, u: float, q_row: torch.Tensor = None) -> int:

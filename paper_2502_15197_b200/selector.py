@@ -13,8 +13,8 @@ from typing import Sequence
 import numpy as np
 import torch
 
-from . import ops
-from .accept_model import AcceptanceMatrix, _device
+from . import _types, ops
+from .accept_model import AcceptanceMatrix, _device, matrix_to_device
 from .errors import CapacityExceededError, OracleSizeExceededError  # noqa: F401  (re-exported names)
 
 __all__ = ["Candidate", "Selection", "PolicyStats", "cumulative_products", "select_tetris", "expected_accepted",
@@ -75,13 +75,19 @@ class PolicyStats:
     comparisons: int
 
 
+for _name, _cls in (("Candidate", Candidate), ("Selection", Selection), ("PolicyStats", PolicyStats)):
+    _types.set_default(_name, _cls)
+
+
 def cumulative_products(probs: AcceptanceMatrix) -> list:
-    """Per-row candidates scored by the running product of acceptance rates (selector.py:95-110)."""
-    a, ln = probs.to_device()
+    """Per-row candidates scored by the running product of acceptance rates (selector.py:95-110).  `probs` is any
+    object with `.rows` (this package's AcceptanceMatrix or the reference's)."""
+    a, ln = matrix_to_device(probs)
     res = ops.select(a, 0, ln, want_cum=True)
     ops.raise_for_status(res.status, "cumulative_products")
-    cum = res.cum.cpu().numpy()
-    return [[Candidate(row=i, depth=j + 1, cum=float(cum[i, j])) for j in range(len(row))]
+    cum = res.cum.cpu().numpy().tolist()
+    cand = _types.get("Candidate")
+    return [[cand(row=i, depth=j + 1, cum=cum[i][j]) for j in range(len(row))]
             for i, row in enumerate(probs.rows)]
 
 
@@ -103,8 +109,9 @@ def select_tetris(candidates: Sequence, capacity: int, *, exact_stats: bool = Tr
     if capacity < 0:
         raise ValueError(f"capacity must be >= 0, got {capacity}")
     B = len(candidates)
+    sel_t, stats_t = _types.get("Selection"), _types.get("PolicyStats")
     if B == 0:
-        return Selection(()), PolicyStats(0, 0, 0, 0)
+        return sel_t(()), stats_t(0, 0, 0, 0)
     vals, ln = _pack_candidates(candidates)
     if vals.shape[1] > ops.N.MAX_K:
         raise ValueError(f"rows deeper than {ops.N.MAX_K} candidates are not supported")
@@ -118,7 +125,7 @@ def select_tetris(candidates: Sequence, capacity: int, *, exact_stats: bool = Tr
         st = res.stats.cpu().numpy()
     ops.raise_for_status(res.status, "select_tetris")
     windows = tuple(int(x) for x in res.windows.cpu().numpy())
-    return Selection(windows), PolicyStats(int(st[0]), int(st[1]), int(st[2]), int(st[3]))
+    return sel_t(windows), stats_t(int(st[0]), int(st[1]), int(st[2]), int(st[3]))
 
 
 def select_fixed_window(n_rows: int, window: int, capacity: int) -> Selection:
@@ -130,22 +137,22 @@ def select_fixed_window(n_rows: int, window: int, capacity: int) -> Selection:
     if n_rows * window > capacity:
         raise CapacityExceededError(
             f"{n_rows} rows x window {window} = {n_rows * window} tokens exceeds capacity {capacity}")
-    return Selection((window,) * n_rows)
+    return _types.get("Selection")((window,) * n_rows)
 
 
 def select_dsd(alpha_estimate: float, n_rows: int, capacity: int, depth_limit: int) -> Selection:
     """Adaptive common window from a scalar acceptance-rate estimate (selector.py:193-222)."""
-    return Selection((ops.dsd_window(alpha_estimate, n_rows, capacity, depth_limit),) * n_rows)
+    return _types.get("Selection")((ops.dsd_window(alpha_estimate, n_rows, capacity, depth_limit),) * n_rows)
 
 
 def expected_accepted(selection: Selection, probs: AcceptanceMatrix) -> float:
     """Expected accepted draft tokens under `selection` (selector.py:286-306)."""
-    if len(selection.windows) != probs.n_rows:
-        raise ValueError(f"selection covers {len(selection.windows)} rows, matrix has {probs.n_rows}")
+    if len(selection.windows) != len(probs.rows):
+        raise ValueError(f"selection covers {len(selection.windows)} rows, matrix has {len(probs.rows)}")
     for window, row in zip(selection.windows, probs.rows):
         if window > len(row):
             raise ValueError(f"selection window {window} deeper than row of depth {len(row)}")
-    a, ln = probs.to_device()
+    a, ln = matrix_to_device(probs)
     w = torch.tensor(selection.windows, dtype=torch.int32, device=a.device)
     return float(ops.expected_accepted(a, w, ln).item())
 

@@ -11,7 +11,7 @@ import torch
 
 from . import _native as N
 from . import ops
-from .accept_model import AcceptanceMatrix, _device
+from .accept_model import AcceptanceMatrix, _device, matrix_to_device
 from .selector import Selection
 
 __all__ = ["apply_verification", "bonus_tokens", "credit", "GpuSimulator", "GpuStepOutcome"]
@@ -20,14 +20,14 @@ __all__ = ["apply_verification", "bonus_tokens", "credit", "GpuSimulator", "GpuS
 def apply_verification(selection: Selection, truth: AcceptanceMatrix, rng: np.random.Generator) -> tuple:
     """Cascading accept/reject per row.  Consumes exactly windows[i] uniforms for row i, in row order, as
     `rng.random(sum(windows))` (identical stream to the reference's per-row `rng.random(w_i)` calls)."""
-    if len(selection.windows) != truth.n_rows:
-        raise ValueError(f"selection covers {len(selection.windows)} rows, truth has {truth.n_rows}")
+    if len(selection.windows) != len(truth.rows):
+        raise ValueError(f"selection covers {len(selection.windows)} rows, truth has {len(truth.rows)}")
     for window, row in zip(selection.windows, truth.rows):
         if window > len(row):
             raise ValueError(f"selection window {window} deeper than drafted depth {len(row)}")
     n = sum(selection.windows)
     draws = rng.random(n) if n else np.zeros(0)
-    a, ln = truth.to_device()
+    a, ln = matrix_to_device(truth)
     dev = a.device
     w = torch.tensor(selection.windows, dtype=torch.int32, device=dev)
     off = torch.zeros(len(selection.windows) + 1, dtype=torch.int32, device=dev)
