@@ -1,4 +1,4 @@
-"""pytest plugin (`-p tests.ref_suite.dropin_plugin`) for running the REFERENCE's own test suite with its hot path
+"""pytest plugin (`-p dropin_plugin` with tests/ref_suite on PYTHONPATH) for running the REFERENCE's own test suite with its hot path
 rebound to the CUDA adapters, the way an integrator would switch an existing tetris_sched deployment over
 (SURVEY.md §4 "How to reuse the suite against the new path").
 

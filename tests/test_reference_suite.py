@@ -109,9 +109,10 @@ def _run_ref_file(name: str, tmp_path: Path):
     report = tmp_path / "dropin.json"
     junit = tmp_path / "junit.xml"
     env = dict(os.environ)
-    env["PYTHONPATH"] = os.pathsep.join([str(REF), str(ROOT), env.get("PYTHONPATH", "")])
+    env["PYTHONPATH"] = os.pathsep.join([str(REF), str(ROOT), str(ROOT / "tests" / "ref_suite"),
+                                         env.get("PYTHONPATH", "")])
     env["TETRIS_DROPIN_REPORT"] = str(report)
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "tests.ref_suite.dropin_plugin",
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "dropin_plugin",
                         "--rootdir", str(REF_TESTS), "-c", str(REF_TESTS / "pytest.ini"), f"--junitxml={junit}",
                         str(REF_TESTS / name)], cwd=str(ROOT), env=env, capture_output=True, text=True,
                        timeout=1500)
