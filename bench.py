@@ -443,27 +443,73 @@ def _e2e(args, cfg, step_dev, bt, B, k, V, C, mode, group, world, dev):
 
 
 def _cpu_baseline(cfg, bt, step, B, C, args):
-    """The reference algorithm (oracle/reference_port.py: heapq select + numpy verify/residual/choice) on the host
-    cores, on a bounded sample: the full selection plus verification of the first `n` requests, scaled to the
-    whole batch (requests are independent).  Also reports how many sampled requests emit the same token as the GPU."""
+    """The reference CPU path (oracle/ref_arm.py: tetris_sched itself from baseline/_ref when staged, else the port)
+    on the host cores, on a bounded sample: the full selection plus verification of the first `n` requests, scaled to
+    the whole batch (requests are independent) -- once on one thread, once fanned out over a process pool on all
+    cores.  Also checks the GPU against it: (accepted, token) on the sample, accepted lengths on all B requests
+    (scalar gathers), and the emitted token against numpy's Generator.choice arithmetic on all B requests' sampled
+    rows (`numpy_mismatch`)."""
+    import numpy as np
+    import torch
+
     sys.path.insert(0, str(ROOT / "oracle"))
+    import ref_arm
+
+    mode = cfg["mode"]
     n = min(B, args.cpu_sample)
     h = _reference_step_inputs(bt, n)
-    threads = os.cpu_count() or 1
-    t_sel, t_ver, toks, out = _time_reference(h, C, n, cfg["mode"], threads)
-    scale = B / n
+    cores = os.cpu_count() or 1
+    rs = ref_arm.ReferenceStep(h, C, mode).start_pool()
+    try:
+        rs.run(min(n, 8), parallel=True)  # warm the workers
+        t_sel, t_ver, toks, out = rs.run(n, parallel=True)
+        n1 = min(n, 32)
+        s_sel, s_ver, s_toks, _ = rs.run(n1, parallel=False)
+    finally:
+        rs.close()
+    scale, scale1 = B / n, B / n1
     step_s = t_sel + t_ver * scale
-    agree = None
-    if args.sets >= 1:
-        # step currently holds the results of the last timed step; recompute set 0 for the comparison
-        step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
-        acc = step.accepted.cpu().numpy()[:n]
-        tok = step.out_tok.cpu().numpy()[:n]
-        agree = int(sum(1 for b, (a, x) in enumerate(out) if a == acc[b] and x == tok[b]))
-    return {"value": toks * scale / step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"full selection over B={B} + verification of {n}/{B} requests, scaled x{scale:.1f} "
-                      f"(select {t_sel * 1e3:.1f} ms, verify {t_ver * 1e3:.1f} ms for the sample)",
-            "cpu_model": _cpu_model(), "gpu_agreement": f"{agree}/{n} requests identical (accepted, token)"}
+    step1_s = s_sel + s_ver * scale1
+    # the GPU against the reference: re-run input set 0 (step holds the last timed step's results)
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    acc = step.accepted.cpu().numpy()
+    tok = step.out_tok.cpu().numpy()
+    agree = int(sum(1 for b, (a, x) in enumerate(out) if a == acc[b] and x == tok[b]))
+    res = {"value": toks * scale / step_s, "unit": "tokens/s", "cores": cores, "kind": ref_arm.kind(),
+           "sample": f"full selection over B={B} + verification of {n}/{B} requests on a {cores}-process pool, "
+                     f"scaled x{scale:.1f} (select {t_sel * 1e3:.1f} ms, verify {t_ver * 1e3:.1f} ms for the sample)",
+           "single_thread": {"value": s_toks * scale1 / step1_s, "unit": "tokens/s", "cores": 1,
+                             "ms_per_step": step1_s * 1e3,
+                             "sample": f"verification of {n1}/{B} requests on one thread, scaled x{scale1:.1f}"},
+           "os_cpu_count": cores, "cpu_model": _cpu_model(),
+           "gpu_agreement": f"{agree}/{n} requests identical (accepted, token)"}
+    if mode == "stochastic":
+        # all B requests: the reference accept cascade on gathered scalars, then numpy's choice arithmetic on the rows
+        windows = np.asarray(ref_arm.select(rs.rows, C), np.int64)
+        d = bt.d.long()
+        pd = bt.p[:, : cfg["k"]].gather(2, d.unsqueeze(-1)).squeeze(-1).double().cpu().numpy()
+        qd = bt.q.gather(2, d.unsqueeze(-1)).squeeze(-1).double().cpu().numpy()
+        ua = bt.u_acc.cpu().numpy()
+        a_ref = windows.copy()
+        for b in range(B):
+            for j in range(windows[b]):
+                s_, m_ = qd[b, j], pd[b, j]
+                if not (s_ <= m_ or ua[b, j] < m_ / s_):
+                    a_ref[b] = j
+                    break
+        resid = a_ref < windows
+        ar = torch.arange(B, device=bt.p.device)
+        at = torch.from_numpy(a_ref).to(bt.p.device)
+        wt = torch.from_numpy(windows).to(bt.p.device)
+        P = bt.p[ar, torch.where(torch.from_numpy(resid).to(bt.p.device), at, wt)].cpu().numpy()
+        Q = bt.q[ar, at.clamp(max=cfg["k"] - 1)].cpu().numpy()
+        mism, _ = ref_arm.numpy_agreement(P, Q, resid, bt.u_res.cpu().numpy(), tok)
+        res["accepted_mismatch"] = int(np.count_nonzero(a_ref != acc))
+        res["numpy_mismatch"] = f"{mism}/{B} requests emit a different token than numpy's Generator.choice " \
+                                f"arithmetic on the same row and uniform ({int(resid.sum())} residual, " \
+                                f"{int((~resid).sum())} bonus rows)"
+    return res
 
 
 def _cpu_model():
@@ -484,33 +530,10 @@ def _reference_step_inputs(bt, n):
             "u_res": bt.u_res.cpu().numpy()}
 
 
-def _time_reference(h, C, n, mode, threads, rows=None):
-    """One reference step: select_tetris(cumulative_products(conf)) then verify requests [0, n) on `threads`
-    threads.  Returns (select seconds, verify seconds, emitted tokens in the sample, None)."""
-    from concurrent.futures import ThreadPoolExecutor
-
-    import reference_port as RP
-
-    if rows is None:
-        rows = [list(map(float, h["conf"][b, : h["lengths"][b]])) for b in range(h["conf"].shape[0])]
-    t0 = time.perf_counter()
-    windows, _ = RP.select_tetris(RP.cumulative_products(rows), C)
-    t1 = time.perf_counter()
-
-    def one(b):
-        if mode == "greedy":
-            return RP.verify_request_greedy(h["p"][b], h["d"][b], windows[b])
-        return RP.verify_request(h["p"][b], h["q"][b], h["d"][b], windows[b], h["u_acc"][b], h["u_res"][b])
-
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        out = list(ex.map(one, range(n)))
-    t2 = time.perf_counter()
-    toks = sum(a + 1 for a, _ in out)
-    return t1 - t0, t2 - t1, toks, out
-
-
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port) timed on the host cores, same metric/config."""
+    """--impl reference: the reference's CPU path (oracle/ref_arm.py: tetris_sched itself from baseline/_ref, else the
+    port) timed on the host cores, same metric/config; verification fanned out over a process pool on all cores, plus
+    a single-thread figure."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -519,6 +542,8 @@ def run_reference(args):
     from paper_2502_15197_b200.synthetic import make_batch
 
     sys.path.insert(0, str(ROOT / "oracle"))
+    import ref_arm
+
     cfg = dict(CONFIGS[args.config])
     world = args.gpus
     B = cfg["B"] // world if cfg.get("strong") else cfg["B"]
@@ -540,35 +565,49 @@ def run_reference(args):
     h = dict(parts[0])
     for key in ("d", "conf", "lengths", "u_acc", "u_res"):
         h[key] = np.concatenate([pt[key] for pt in parts])
-    threads = os.cpu_count() or 1
-    rows = [list(map(float, h["conf"][b, : h["lengths"][b]])) for b in range(h["conf"].shape[0])]
-    ws, wv = 0.0, 0.0
-    for _ in range(max(1, min(args.warmup, 1))):
-        ws, wv, _, _ = _time_reference(h, C, n, mode, threads, rows)
-    # each step's verification sample is sized so the K timed steps take about --ref-budget-s seconds (the full
-    # selection over all requests runs every step; the sample shrinks, not below 8 requests, as K grows)
-    per_req = wv / max(n, 1)
-    n_eff = n
-    if per_req > 0:
-        n_eff = int((args.ref_budget_s / max(args.steps, 1) - ws) / per_req)
-        n_eff = max(min(8, n), min(n, n_eff))
-    sel, ver, toks = 0.0, 0.0, 0
-    for _ in range(args.steps):
-        a, b, t, _ = _time_reference(h, C, n_eff, mode, threads, rows)
-        sel, ver, toks = sel + a, ver + b, toks + t
-    n = n_eff
-    scale = Bg / n
+    cores = os.cpu_count() or 1
+    rs = ref_arm.ReferenceStep(h, C, mode).start_pool()
+    try:
+        n1 = min(n, 16)
+        s_sel, s_ver, s_toks, _ = rs.run(n1, parallel=False)
+        ws, wv = 0.0, 0.0
+        for _ in range(max(1, min(args.warmup, 2))):
+            ws, wv, _, _ = rs.run(n, parallel=True)
+        # the faster fan-out is timed: the process pool, or one thread when the batch is too small to pay for it
+        parallel = wv / max(n, 1) < s_ver / max(n1, 1)
+        per_req = wv / max(n, 1) if parallel else s_ver / max(n1, 1)
+        # each step's verification sample is sized so the K timed steps take about --ref-budget-s seconds (the full
+        # selection over all requests runs every step; the sample shrinks, not below one request per process)
+        n_eff = n
+        if per_req > 0:
+            n_eff = int((args.ref_budget_s / max(args.steps, 1) - ws) / per_req)
+            n_eff = max(min(cores, n), min(n, n_eff))
+        sel, ver, toks = 0.0, 0.0, 0
+        for _ in range(args.steps):
+            a, b, t, _ = rs.run(n_eff, parallel=parallel)
+            sel, ver, toks = sel + a, ver + b, toks + t
+    finally:
+        rs.close()
+    scale = Bg / n_eff
     step_s = (sel + ver * scale) / args.steps
     value = (toks / args.steps) * scale / step_s
+    scale1 = Bg / n1
+    step1_s = s_sel + s_ver * scale1
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None, "impl": "reference",
             "dtype": "f32 probabilities, f64 accumulation (numpy)", "data": "synthetic",
             "config": {"workload": f"{args.config}: B={Bg} k={k} C={C} V={V} {mode}", "B_per_gpu": B, "k": k,
                        "C": C, "V": V, "verify": mode},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
-                             "sample": f"per step: full selection over B={Bg} + verification of {n} requests "
-                                       f"(scaled x{scale:.1f})", "cpu_model": _cpu_model()},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores if parallel else 1,
+                             "kind": ref_arm.kind(),
+                             "sample": f"per step: full selection over B={Bg} + verification of {n_eff} requests "
+                                       + (f"on a {cores}-process pool" if parallel else "on one thread (faster than "
+                                          f"the {cores}-process pool at this size)") + f" (scaled x{scale:.1f})",
+                             "single_thread": {"value": s_toks * scale1 / step1_s, "unit": "tokens/s", "cores": 1,
+                                               "ms_per_step": step1_s * 1e3,
+                                               "sample": f"verification of {n1} requests, scaled x{scale1:.1f}"},
+                             "os_cpu_count": cores, "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -627,12 +666,12 @@ def run_select_sweep(args):
             sweep[str(C)] = {"us_per_select": us, "selections_per_s": 1e6 / us, "cells_per_s": B * k * 1e6 / us}
     if not args.no_cpu_baseline or args.impl == "reference":
         sys.path.insert(0, str(ROOT / "oracle"))
-        import reference_port as RP
+        import ref_arm
 
         rows = [list(map(float, r)) for r in host_sets[0].numpy()]
         for C in cfg["sweep"]:
             t = time.perf_counter()
-            RP.select_tetris(RP.cumulative_products(rows), C)
+            ref_arm.select(rows, C)  # AcceptanceMatrix.from_rows + cumulative_products + select_tetris
             cpu[str(C)] = (time.perf_counter() - t) * 1e6
     main_C = "8192"
     if args.impl == "reference":
@@ -640,8 +679,9 @@ def run_select_sweep(args):
         line = {"metric": "selection-only top-C latency", "value": v, "unit": "us", "n_gpus": args.gpus,
                 "steps": 1, "warmup": 0, "higher_is_better": False, "impl": "reference", "vs_baseline": None,
                 "config": {"workload": f"cfg4: B={B} k={k} C=sweep, selection only", "sweep_us": cpu},
-                "cpu_baseline": {"value": v, "unit": "us", "cores": 1, "kind": "port",
-                                 "sample": "cumulative_products + heapq select_tetris over the full batch, 1 thread"},
+                "cpu_baseline": {"value": v, "unit": "us", "cores": 1, "kind": ref_arm.kind(),
+                                 "sample": "AcceptanceMatrix.from_rows + cumulative_products + heapq select_tetris "
+                                           "over the full batch, 1 thread"},
                 "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     else:
         v = sweep[main_C]["us_per_select"]
@@ -652,7 +692,7 @@ def run_select_sweep(args):
                            "l2": f"{nsets} rotated conf sets ({nsets * B * k * 8 / 1e6:.0f} MB > L2)",
                            "launch": "CUDA graph replay"},
                 "sweep": sweep,
-                "cpu_baseline": {"sweep_us": cpu, "unit": "us", "cores": 1, "kind": "port"} if cpu else None,
+                "cpu_baseline": {"sweep_us": cpu, "unit": "us", "cores": 1, "kind": ref_arm.kind()} if cpu else None,
                 "gpu_launches": nsets * reps * len(cfg["sweep"])}
     print(json.dumps(line), flush=True)
 

@@ -96,8 +96,29 @@ def verify_request(p_rows, q_rows, d, w, u_acc, u_res):
         if mass <= 0.0:
             raise ValueError("degenerate residual")
         return a, choice_index(diff / mass, float(u_res))
-    pb = np.asarray(p_rows[w], np.float64)
-    return a, choice_index(pb / pb.sum(), float(u_res))
+    # bonus: Generator.choice(V, p=p[w]) on the fp64-upcast target row (choice normalises by its own cdf[-1])
+    return a, choice_index(np.asarray(p_rows[w], np.float64), float(u_res))
+
+
+def numpy_cdf(p_row, q_row=None) -> np.ndarray:
+    """The CDF numpy's Generator.choice searches (accept_model.py:364,368): for a residual (q_row given) the
+    probabilities are residual_distribution's `clip(p - q, 0) / pairwise-sum` (accept_model.py:316-327); for a bonus
+    row the fp64-upcast target row itself.  cdf = cumsum(p); cdf /= cdf[-1]."""
+    p64 = np.asarray(p_row, np.float64)
+    if q_row is not None:
+        diff = np.clip(p64 - np.asarray(q_row, np.float64), 0.0, None)
+        mass = float(diff.sum())
+        if mass <= 0.0:
+            raise ValueError("degenerate residual")
+        p64 = diff / mass
+    cdf = np.cumsum(p64)
+    cdf /= cdf[-1]
+    return cdf
+
+
+def numpy_choice(cdf: np.ndarray, u) -> np.ndarray:
+    """searchsorted(cdf, u, 'right') for one or many uniforms (Generator.choice's inverse CDF)."""
+    return np.searchsorted(cdf, u, side="right")
 
 
 def verify_request_greedy(p_rows, d, w):
