@@ -11,8 +11,10 @@
  *   - All pointers are DEVICE pointers (or host pointers registered/mapped for device access) owned by the caller;
  *     the library allocates nothing persistent.  Scratch space comes from a caller-provided workspace that must be
  *     zeroed once with tetris_workspace_init() (kernels leave their arrival counters at zero after every call).
- *   - Everything is stream-ordered on the caller's `stream`; no entry point synchronises the host.  The ABI is
- *     reentrant: no mutable globals besides the thread-local last-error string.
+ *   - Everything is stream-ordered on the caller's `stream`; no entry point synchronises the host, except the two
+ *     host-buffer steps (tetris_step_*_staged_f32), which wait for the selection mid-call to learn which host rows to
+ *     copy.  The ABI is reentrant: no mutable globals besides the thread-local last-error string and write-once
+ *     per-device caches (SM count, kernel shared-memory attributes, the staged steps' per-thread copy streams).
  *   - Host-checkable argument errors return TETRIS_INVALID_ARGUMENT immediately.  Data-dependent errors found on the
  *     device are OR-ed into the caller's device word `status` (TETRIS_ST_* bits); the host adapter reads it when it
  *     materialises results and raises the reference's exception.
@@ -79,7 +81,12 @@ const char* tetris_last_error(void);
  * [host_ptr, host_ptr+bytes) (registering it as mapped/portable when it is not pinned yet), so the streaming kernels
  * can read p/q rows straight from host RAM over PCIe/C2C and only the touched rows cross the link. */
 int tetris_map_host(void* host_ptr, size_t bytes, void** dev_ptr);
+/* Releases a registration tetris_map_host made itself (no-op for memory the caller pinned or never mapped). */
+int tetris_unmap_host(void* host_ptr);
 int tetris_abi_version(void);
+/* Largest B the speculative sampler (tetris_resample_spec_f32) takes on the current device: min(4096, 32 x SMs).
+ * tetris_step_stochastic_f32 falls back to the plain sampler above it. */
+int tetris_spec_max_requests(void);
 
 /* Diagnostics: when dev_buf != NULL the selector writes clock64() stamps of its phases (CTA 0) into dev_buf[0..9]. */
 int tetris_debug_timestamps(void* dev_buf);
@@ -134,7 +141,9 @@ int tetris_verify_stochastic_f32(const float* p, const float* q, const int32_t* 
                                  tetris_stream_t stream);
 
 /* The whole stochastic step in two launches (the product hot path), also callable as its two halves:
- *   tetris_select_accept_f32 — select_kernel (cluster) with its epilogue: prefix products, global top-C windows +
+ *   tetris_select_accept_f32 — the selector (select1_kernel, one CTA, for B_sel*k <= 16384; else the grid selector
+ *      gselect_kernel in the workspace's scratch; the cluster/DSMEM select_kernel only when no workspace is given)
+ *      with its epilogue: prefix products, global top-C windows +
  *      win_offsets + stats, the accept test of every selected position, accepted[b], the row to resample from
  *      (kept in the workspace) and the compaction offsets (n_b = accepted[b]+1, capped by cap[b] when cap != NULL);
  *      with dense uniforms the accept test of every drafted position runs first in a full-grid pre_accept_kernel;
@@ -158,8 +167,8 @@ int tetris_resample_f32(const float* p, const float* q, const double* u_res, int
 /* tetris_resample_f32 with the speculative start (same results): the rows of requests whose first drafted token is
  * rejected do not depend on the selection, so the kernel finds them itself (verify_token at position 0 with the
  * dense uniforms u_acc[b][0] of the local rows; len: their drafted depths, nullable) and streams them while the
- * preceding tetris_select_accept_f32 is still running; the rest follows the selection.  B <= 4096 (larger batches:
- * TETRIS_INVALID_ARGUMENT).  tetris_step_stochastic_f32 uses it for dense uniforms. */
+ * preceding tetris_select_accept_f32 is still running; the rest follows the selection.  B <= tetris_spec_max_requests()
+ * (larger batches: TETRIS_INVALID_ARGUMENT).  tetris_step_stochastic_f32 uses it for dense uniforms. */
 int tetris_resample_spec_f32(const float* p, const float* q, const double* u_res, const double* u_acc,
                              const int32_t* len, int32_t B, int32_t k, int32_t V, const int32_t* d,
                              const int32_t* accepted, const int32_t* offsets, int32_t* out_tok, double* mass_out,
@@ -196,6 +205,16 @@ int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, in
                                       int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
                                       int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
                                       tetris_stream_t stream);
+
+/* The greedy step for HOST-resident p ([B][k+1][V], pinned and device-mapped): the selection, then (host waits for it)
+ * one DMA copy per request of its verified rows p[b][0 .. windows[b]] (contiguous in host memory) into the same
+ * place of the device buffer p_dev ([B][k+1][V]; rows not needed are left untouched), then the greedy verification +
+ * compaction on p_dev.  windows_host: pinned host scratch of B int32.  Same results as tetris_step_greedy_f32. */
+int tetris_step_greedy_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
+                                  const float* p_host, const int32_t* d, const int32_t* cap, int32_t V, float* p_dev,
+                                  int32_t* windows_host, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
+                                  int32_t* out_tok, int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                  uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
 
 /* The greedy step in 2 launches (select1 with the row-list epilogue, then the persistent argmax stream with the
  * verdicts and the compaction; V % 8 == 0 and 16-byte aligned p, else the stage-by-stage fallback): the selection of

@@ -58,6 +58,8 @@ _SIGNATURES = {
     "tetris_abi_version": (C.c_int, []),
     "tetris_debug_timestamps": (C.c_int, [_p]),
     "tetris_map_host": (C.c_int, [_p, _sz, C.POINTER(C.c_void_p)]),
+    "tetris_unmap_host": (C.c_int, [_p]),
+    "tetris_spec_max_requests": (C.c_int, []),
     "tetris_workspace_bytes": (_sz, [C.c_int, _i32, _i32, _i32]),
     "tetris_workspace_init": (C.c_int, [_p, _sz, _p]),
     "tetris_select_f64": (C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _p, _p, _p, _p, _p, _p, _sz, _p]),
@@ -80,6 +82,8 @@ _SIGNATURES = {
     "tetris_step_stochastic_staged_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
                   _p, _sz, _p]),
+    "tetris_step_greedy_staged_f32": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "tetris_step_greedy_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz,
                   _p]),
@@ -138,6 +142,16 @@ def map_host(ptr: int, nbytes: int) -> int:
     out = C.c_void_p()
     call("tetris_map_host", ptr, nbytes, C.byref(out))
     return int(out.value)
+
+
+def unmap_host(ptr: int) -> None:
+    """Release a registration map_host made (no-op for caller-pinned memory)."""
+    call("tetris_unmap_host", ptr)
+
+
+def spec_max_requests() -> int:
+    """Largest batch the speculative sampler takes on the current device (min(4096, 32 x SMs))."""
+    return int(load().tetris_spec_max_requests())
 
 
 def workspace_bytes(op: int, B: int, k: int, V: int) -> int:

@@ -2,6 +2,9 @@
 #include "abi_util.h"
 #include "launch.h"
 
+#include <mutex>
+#include <set>
+
 namespace tetris {
 namespace abi {
 char* err_buf() {
@@ -28,6 +31,11 @@ extern "C" int tetris_workspace_init(void* ws, size_t ws_bytes, tetris_stream_t 
   return TETRIS_OK;
 }
 
+// host ranges this library registered itself (tetris_unmap_host releases only those; caller-pinned memory is the
+// caller's)
+static std::mutex g_reg_mu;
+static std::set<void*> g_registered;
+
 extern "C" int tetris_map_host(void* host_ptr, size_t bytes, void** dev_ptr) {
   if (!host_ptr || !dev_ptr) return tetris::abi::fail(TETRIS_INVALID_ARGUMENT, "null pointer");
   cudaError_t e = cudaHostGetDevicePointer(dev_ptr, host_ptr, 0);
@@ -35,10 +43,29 @@ extern "C" int tetris_map_host(void* host_ptr, size_t bytes, void** dev_ptr) {
   cudaGetLastError();  // not pinned yet: register it
   e = cudaHostRegister(host_ptr, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
   if (e != cudaSuccess) return tetris::abi::cuda_fail(e);
+  {
+    std::lock_guard<std::mutex> lock(g_reg_mu);
+    g_registered.insert(host_ptr);
+  }
   e = cudaHostGetDevicePointer(dev_ptr, host_ptr, 0);
   if (e != cudaSuccess) return tetris::abi::cuda_fail(e);
   return TETRIS_OK;
 }
+
+extern "C" int tetris_unmap_host(void* host_ptr) {
+  if (!host_ptr) return TETRIS_OK;
+  {
+    std::lock_guard<std::mutex> lock(g_reg_mu);
+    auto it = g_registered.find(host_ptr);
+    if (it == g_registered.end()) return TETRIS_OK;  // pinned by the caller, or never mapped: nothing to release
+    g_registered.erase(it);
+  }
+  cudaError_t e = cudaHostUnregister(host_ptr);
+  if (e != cudaSuccess) return tetris::abi::cuda_fail(e);
+  return TETRIS_OK;
+}
+
+extern "C" int tetris_spec_max_requests(void) { return tetris::spec_max_requests(); }
 
 extern "C" int tetris_debug_timestamps(void* dev_buf) {
   tetris::set_debug_buffer((long long*)dev_buf);

@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "tetris_b200.h"
@@ -66,6 +67,25 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e == cudaSuccess && slot >= 0) table[slot] = Entry{fn, dev, bytes};
   return e;
+}
+
+// SM count of the CURRENT device, cached per device (a process may drive GPUs / MIG slices of different sizes;
+// grids sized from another device's count would break the cooperative launches' co-residency).  Lock-free: racing
+// first calls write the same value.
+inline int device_sm_count() {
+  static std::atomic<int> cache[128];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 128) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
 }
 
 enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP, WS_SPEC_SUMS, WS_END };

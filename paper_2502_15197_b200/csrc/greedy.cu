@@ -470,13 +470,7 @@ int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, 
 }
 
 int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    num_sms = n > 0 ? n : 148;
-  }
+  const int num_sms = abi::device_sm_count();
   cudaError_t e = abi::ensure_smem((const void*)persist_greedy_kernel, kGSmem);
   if (e != cudaSuccess) return abi::cuda_fail(e);
   // the listed-row count lives on the device; the bound B * (k + 1) * nch caps the useful grid

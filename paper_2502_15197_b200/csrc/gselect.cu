@@ -404,13 +404,7 @@ bool gselect_shape(int B, int k, int num_sms, int* grid, int* RB) {
 }
 
 int launch_gselect(const SelectArgs& args_in, void* scratch, cudaStream_t st) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (num_sms <= 0) num_sms = 148;
-  }
+  const int num_sms = abi::device_sm_count();
   GArgs ga;
   ga.a = args_in;
   ga.a.dbg = debug_buffer();

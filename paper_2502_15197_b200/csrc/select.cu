@@ -684,12 +684,7 @@ int launch_select(const SelectArgs& args_in, cudaStream_t st) {
   // accept CTAs (whole clusters after cluster 0): one thread per drafted position, within the co-resident limit
   int extra_clusters = 0;
   if (a.acc_bytes && a.accept_ctas > 0) {
-    static int num_sms = 0;
-    if (num_sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int num_sms = abi::device_sm_count();
     const long long n = (long long)a.ep_rows * a.k;
     long long want = (n + sh.T - 1) / sh.T;
     const long long cap = (long long)(num_sms - G) / G * G;

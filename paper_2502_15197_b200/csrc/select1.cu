@@ -458,13 +458,7 @@ int launch_select1(const SelectArgs& args_in, cudaStream_t st) {
   const size_t smem = (size_t)a.k * ((a.B | 15) + 2) * 8 + 2 * (size_t)a.B;
   int naccept = 0;
   if (a.acc_bytes && a.accept_ctas > 0) {
-    static int num_sms = 0;
-    if (num_sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-      if (num_sms <= 0) num_sms = 148;
-    }
+    const int num_sms = abi::device_sm_count();
     const long long n = (long long)a.ep_rows * a.k;
     long long want = (n + nt - 1) / nt;  // one drafted position (two gathers) per thread
     if (want > num_sms - 1) want = num_sms - 1;

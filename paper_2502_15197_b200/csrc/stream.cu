@@ -714,18 +714,11 @@ __global__ void accept_kernel(const float* __restrict__ p, const float* __restri
 
 namespace tetris {
 
-static int g_num_sms = 0;
-
 int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
   if (a_in.R == 0) return TETRIS_OK;
   StreamArgs a = a_in;
   a.dbg = debug_buffer();
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
+  const int g_num_sms = abi::device_sm_count();
   const bool spec = a.u_acc != nullptr && a.req_cnt != nullptr;
   if (spec && (a.R > kSpecMaxR || !a.req_cnt_spec || !a.chunk_sums_spec || !a.warp_sums_spec || !a.d ||
                !a.spec_ctl || !a.spec_bitmap || !a.spec_list ||
@@ -762,7 +755,9 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
   return abi::launch_check();
 }
 
-int spec_max_requests() { return kSpecMaxR; }
+// requests one speculative call can take on the current device: its shared-memory lists hold kSpecMaxR, and each CTA
+// evaluates at most 32 requests' position-0 verdicts in the prologue (ceil(R / grid) <= 32)
+int spec_max_requests() { return std::min(kSpecMaxR, 32 * abi::device_sm_count()); }
 
 bool persist_eligible(const float* p, const float* q, int V) {
   return (V % kLaneElems == 0) && (((uintptr_t)p & 15u) == 0) && (!q || (((uintptr_t)q & 15u) == 0)) &&

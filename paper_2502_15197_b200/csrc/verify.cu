@@ -677,6 +677,66 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
 // the host, the host queues one DMA copy per needed row into `staging` on the copy engines (which read host memory
 // at ~55 GB/s on this box, vs ~50 for SM-issued zero-copy reads), rewrites rowinfo as staging rows, and the sampler
 // runs on device memory.  Blocking: the host waits for the selection (one stream synchronize).
+// ---- host-buffer steps: the needed host rows are copied by the DMA engines --------------------------------------
+// The copies are spread over kCopyStreams streams (forked from / joined to the caller's stream with events) so several
+// copy engines work at once and each copy's set-up overlaps the others' transfers.  The streams and events are created
+// once per (host thread, device): a thread that later drives another GPU gets that device's own set.
+constexpr int kCopyStreams = 8;
+constexpr int kMaxDevices = 64;
+struct CopyLanes {
+  cudaStream_t cs[kCopyStreams];
+  cudaEvent_t ev[kCopyStreams + 1];
+  bool ready;
+};
+
+static int copy_lanes(CopyLanes** out) {
+  static thread_local CopyLanes lanes[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return abi::cuda_fail(e);
+  if (dev < 0 || dev >= kMaxDevices) return abi::fail(TETRIS_INVALID_ARGUMENT, "device %d >= %d", dev, kMaxDevices);
+  CopyLanes& L = lanes[dev];
+  if (!L.ready) {
+    for (int i = 0; i < kCopyStreams; ++i)
+      if ((e = cudaStreamCreateWithFlags(&L.cs[i], cudaStreamNonBlocking)) != cudaSuccess) return abi::cuda_fail(e);
+    for (int i = 0; i <= kCopyStreams; ++i)
+      if ((e = cudaEventCreateWithFlags(&L.ev[i], cudaEventDisableTiming)) != cudaSuccess) return abi::cuda_fail(e);
+    L.ready = true;
+  }
+  *out = &L;
+  return TETRIS_OK;
+}
+
+static int copy_h2d_batched(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<size_t>& sizes,
+                            cudaStream_t st) {
+  CopyLanes* L = nullptr;
+  int rc = copy_lanes(&L);
+  if (rc) return rc;
+  cudaError_t e;
+  if ((e = cudaEventRecord(L->ev[kCopyStreams], st)) != cudaSuccess) return abi::cuda_fail(e);
+  const size_t n = dsts.size();
+  for (int i = 0; i < kCopyStreams; ++i) {
+    if ((e = cudaStreamWaitEvent(L->cs[i], L->ev[kCopyStreams], 0)) != cudaSuccess) return abi::cuda_fail(e);
+    const size_t lo = n * i / kCopyStreams, hi = n * (i + 1) / kCopyStreams;
+    if (hi > lo) {
+      cudaMemcpyAttributes attr = {};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      size_t attr_idx = 0, fail_idx = 0;
+      e = cudaMemcpyBatchAsync(dsts.data() + lo, srcs.data() + lo, sizes.data() + lo, hi - lo, &attr, &attr_idx, 1,
+                               &fail_idx, L->cs[i]);
+      if (e != cudaSuccess) {  // older driver: one copy at a time
+        cudaGetLastError();
+        for (size_t j = lo; j < hi; ++j)
+          if ((e = cudaMemcpyAsync(dsts[j], srcs[j], sizes[j], cudaMemcpyHostToDevice, L->cs[i])) != cudaSuccess)
+            return abi::cuda_fail(e);
+      }
+    }
+    if ((e = cudaEventRecord(L->ev[i], L->cs[i])) != cudaSuccess) return abi::cuda_fail(e);
+    if ((e = cudaStreamWaitEvent(st, L->ev[i], 0)) != cudaSuccess) return abi::cuda_fail(e);
+  }
+  return TETRIS_OK;
+}
+
 extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k,
                                                  int64_t C, const float* p_host, const float* q_host,
                                                  const int32_t* d, const double* u_acc, const double* u_res,
@@ -688,14 +748,15 @@ extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32
                                                  tetris_stream_t stream) {
   int rc = check_shape(B, k, V);
   if (rc) return rc;
-  if (!p_host || !q_host || !staging || !rowinfo_host) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (!p_host || (k > 0 && !q_host) || !staging || !rowinfo_host)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if (!persist_eligible(staging, staging, V))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "staged step needs V %% 8 == 0 and a 16-byte aligned staging buffer");
   cudaStream_t st = (cudaStream_t)stream;
   void* p_map = nullptr;
   void* q_map = nullptr;
   cudaError_t e = cudaHostGetDevicePointer(&p_map, (void*)p_host, 0);
-  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&q_map, (void*)q_host, 0);
+  if (e == cudaSuccess && q_host) e = cudaHostGetDevicePointer(&q_map, (void*)q_host, 0);
   if (e != cudaSuccess) return abi::cuda_fail(e);
   if ((rc = tetris_select_accept_f32(conf, len, B, k, C, 0, B, (const float*)p_map, (const float*)q_map, d, u_acc, 0,
                                      cap, V, windows, win_offsets, accepted, offsets, tokens, stats4, status, ws,
@@ -725,38 +786,7 @@ extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32
     }
   }
   sizes.assign(dsts.size(), row_bytes);
-  // the copies are spread over kCopyStreams streams (forked from / joined to the caller's stream with events) so
-  // several copy engines work at once and each copy's set-up overlaps the others' transfers
-  constexpr int kCopyStreams = 8;
-  static thread_local cudaStream_t cs[kCopyStreams] = {};
-  static thread_local cudaEvent_t ev[kCopyStreams + 1] = {};
-  if (!cs[0]) {
-    for (int i = 0; i < kCopyStreams; ++i)
-      if ((e = cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking)) != cudaSuccess) return abi::cuda_fail(e);
-    for (int i = 0; i <= kCopyStreams; ++i)
-      if ((e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming)) != cudaSuccess) return abi::cuda_fail(e);
-  }
-  if ((e = cudaEventRecord(ev[kCopyStreams], st)) != cudaSuccess) return abi::cuda_fail(e);
-  const size_t n = dsts.size();
-  for (int i = 0; i < kCopyStreams; ++i) {
-    if ((e = cudaStreamWaitEvent(cs[i], ev[kCopyStreams], 0)) != cudaSuccess) return abi::cuda_fail(e);
-    const size_t lo = n * i / kCopyStreams, hi = n * (i + 1) / kCopyStreams;
-    if (hi > lo) {
-      cudaMemcpyAttributes attr = {};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t attr_idx = 0, fail_idx = 0;
-      e = cudaMemcpyBatchAsync(dsts.data() + lo, srcs.data() + lo, sizes.data() + lo, hi - lo, &attr, &attr_idx, 1,
-                               &fail_idx, cs[i]);
-      if (e != cudaSuccess) {  // older driver: one copy at a time
-        cudaGetLastError();
-        for (size_t j = lo; j < hi; ++j)
-          if ((e = cudaMemcpyAsync(dsts[j], srcs[j], row_bytes, cudaMemcpyHostToDevice, cs[i])) != cudaSuccess)
-            return abi::cuda_fail(e);
-      }
-    }
-    if ((e = cudaEventRecord(ev[i], cs[i])) != cudaSuccess) return abi::cuda_fail(e);
-    if ((e = cudaStreamWaitEvent(st, ev[i], 0)) != cudaSuccess) return abi::cuda_fail(e);
-  }
+  if ((rc = copy_h2d_batched(dsts, srcs, sizes, st))) return rc;
   if ((e = cudaMemcpyAsync(rowinfo, rowinfo_host, ri_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return abi::cuda_fail(e);
   return resample_impl(staging, staging, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out,
@@ -909,4 +939,48 @@ extern "C" int tetris_residual_f64(const double* p_draft, const double* p_target
   dim3 grid((V + 255) / 256 < 1024 ? (V + 255) / 256 : 1024, R);
   residual_norm_kernel<<<grid, 256, 0, st>>>(p_draft, p_target, V, mass_out, out);
   return abi::launch_check();
+}
+
+// The greedy step for host-resident p: selection, then one DMA copy per request of its verified rows p[b][0..w_b]
+// (contiguous in host memory) into the same place of p_dev, then the greedy verification + compaction on p_dev.
+extern "C" int tetris_step_greedy_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
+                                             const float* p_host, const int32_t* d, const int32_t* cap, int32_t V,
+                                             float* p_dev, int32_t* windows_host, int32_t* windows,
+                                             int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                                             int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status,
+                                             void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  using namespace tetris;
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
+  if (B == 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "empty batch");
+  if ((k > 0 && (!conf || !d)) || !p_host || !p_dev || !windows_host || !windows || !accepted || !out_tok ||
+      !offsets || !tokens)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = tetris_select_f64(conf, len, B, k, C, 0, windows, win_offsets, nullptr, stats4, status, ws, ws_bytes,
+                              stream)))
+    return rc;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(windows_host, windows, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToHost, st)) !=
+          cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return abi::cuda_fail(e);
+  const size_t req_elems = (size_t)(k + 1) * V;
+  std::vector<void*> dsts, srcs;
+  std::vector<size_t> sizes;
+  dsts.reserve(B);
+  srcs.reserve(B);
+  sizes.reserve(B);
+  for (int b = 0; b < B; ++b) {
+    int w = windows_host[b];
+    w = w < 0 ? 0 : (w > k ? k : w);
+    dsts.push_back(p_dev + (size_t)b * req_elems);
+    srcs.push_back((void*)(p_host + (size_t)b * req_elems));
+    sizes.push_back((size_t)(w + 1) * V * sizeof(float));
+  }
+  if ((rc = copy_h2d_batched(dsts, srcs, sizes, st))) return rc;
+  return verify_greedy_impl(p_dev, d, windows, cap, B, k, V, accepted, out_tok, offsets, tokens, status, ws, ws_bytes,
+                            st);
 }

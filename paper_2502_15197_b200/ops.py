@@ -370,7 +370,8 @@ def compact(accepted: torch.Tensor, out_tok: torch.Tensor, d: torch.Tensor, cap:
 # ---------------------------------------------------------------------------------------------------------------
 # one full verification step with preallocated buffers (CUDA-graph capturable)
 # ---------------------------------------------------------------------------------------------------------------
-SPEC_MAX_REQUESTS = 4096  # tetris_resample_spec_f32's limit (per call, local rows)
+SPEC_MAX_REQUESTS = 4096  # tetris_resample_spec_f32's limit (per call, local rows) on a full B200; a device with
+# fewer SMs takes min(4096, 32 x SMs) (tetris_spec_max_requests, queried per TetrisStep)
 # below this much streaming the early start does not pay (csrc/verify.cu kSpecMinChunks); env override for A/B runs
 SPEC_MIN_CHUNKS = int(os.environ.get("TETRIS_SPEC_MIN_CHUNKS", "4096"))
 _NO_SPEC = os.environ.get("TETRIS_NO_SPEC") == "1"  # A/B timing switch: the plain sampler
@@ -425,6 +426,8 @@ class TetrisStep:
         self.tokens = torch.zeros(B * (k + 1), dtype=_I32, device=dev)
         self.ws = Workspace(dev, N.OP_ALL, Bg, k, V)
         self._lib = N.load()
+        with torch.cuda.device(dev):
+            self.spec_max = min(SPEC_MAX_REQUESTS, N.spec_max_requests())
 
     def run(self, conf, lengths, p, q, d, u_acc=None, u_res=None, cap=None, events=None, window=None) -> None:
         """events: optional 4 torch.cuda.Events recorded around select / verify / compact (kernel timing).  The
@@ -446,8 +449,9 @@ class TetrisStep:
             sel_conf, sel_len = self.conf_all, self.len_all
         else:  # world 1, or a shard given the gathered scores directly
             sel_conf, sel_len = conf, lengths
-        if self.mode == "stochastic" and V % 8 != 0:
-            # the TMA sampler needs 32-byte rows (V % 8 == 0): the stage-by-stage kernels serve any V
+        if self.mode == "stochastic" and (V % 8 != 0 or p.data_ptr() % 16 or (q is not None and q.data_ptr() % 16)):
+            # the TMA sampler needs 32-byte rows (V % 8 == 0) and 16-byte aligned p / q (persist_eligible,
+            # csrc/stream.cu): the stage-by-stage kernels serve any V and alignment
             self._check(lib.tetris_select_f64(sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, 0,
                                               self.windows_all.data_ptr(), self.win_offsets.data_ptr(), None,
                                               self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s))
@@ -558,7 +562,7 @@ class TetrisStep:
     def uses_spec(self) -> bool:
         """True when the stochastic step runs the speculative sampler (tetris_resample_spec_f32)."""
         return (self.mode == "stochastic" and self.policy == "tetris" and self.u_layout == "dense"
-                and self.B <= SPEC_MAX_REQUESTS and self.B * -(-self.V // 8192) >= SPEC_MIN_CHUNKS and not _NO_SPEC)
+                and self.B <= self.spec_max and self.B * -(-self.V // 8192) >= SPEC_MIN_CHUNKS and not _NO_SPEC)
 
     @property
     def launches_per_step(self) -> int:
@@ -575,42 +579,62 @@ class TetrisStep:
 
 
 class _MappedTensor:
-    """Stand-in exposing a device address for a pinned host tensor (zero-copy reads by the kernels)."""
+    """Stand-in exposing a device address for a pinned host tensor (zero-copy reads by the kernels).  Memory that the
+    library had to register (pageable input) is unregistered when this object goes away."""
 
     def __init__(self, host: torch.Tensor):
         if host.is_cuda or not host.is_contiguous():
             raise ValueError("expected a contiguous host tensor")
         self.host = host
-        self._dev = N.map_host(host.data_ptr(), host.numel() * host.element_size())
+        self._ptr = host.data_ptr()
+        self._dev = N.map_host(self._ptr, host.numel() * host.element_size())
 
     def data_ptr(self) -> int:
         return self._dev
+
+    def __del__(self):
+        try:
+            N.unmap_host(self._ptr)
+        except Exception:
+            pass
 
 
 class HostTetrisStep:
     """The same step for HOST-resident inputs (the end-to-end API): small per-request inputs (conf, lengths, draft
     tokens, uniforms) are copied host->device; the large target/draft probability tensors stay in pinned host memory
-    and the streaming kernel reads only the rows it needs over the host link (zero-copy); the compacted token stream
-    and per-request results are copied back into pinned host buffers.  `run` is stream-ordered; call
-    `torch.cuda.current_stream().synchronize()` (or `wait()`) before reading `tokens_host`."""
+    and only the rows the step needs cross the host link; the compacted token stream and per-request results are
+    copied back into pinned host buffers.  `run` is stream-ordered; call `torch.cuda.current_stream().synchronize()`
+    (or `wait()`) before reading `tokens_host`."""
 
-    def __init__(self, B: int, k: int, V: int, capacity: int, p_host: torch.Tensor, q_host: torch.Tensor,
+    def __init__(self, B: int, k: int, V: int, capacity: int, p_host: torch.Tensor, q_host: Optional[torch.Tensor],
                  mode: str = "stochastic", device="cuda", transfer: str = "staged"):
-        """transfer: "staged" (stochastic mode: after the selection, the needed rows are copied host->device by the
-        DMA engines, tetris_step_stochastic_staged_f32; the host waits for the selection) or "zero-copy" (the
-        kernels read the rows from pinned host memory; no host wait)."""
+        """transfer: "staged" (after the selection the needed rows are copied host->device by the DMA engines --
+        tetris_step_stochastic_staged_f32: the residual / bonus row of each request into a [2B, V] staging buffer;
+        tetris_step_greedy_staged_f32: rows 0..w_b of each request into their place of a [B, k+1, V] device copy;
+        the host waits for the selection) or "zero-copy" (the kernels read the rows from pinned host memory; no host
+        wait).  q_host may be None (or empty) when k == 0 or mode == "greedy"."""
         if transfer not in ("staged", "zero-copy"):
             raise ValueError(f"transfer must be 'staged' or 'zero-copy', got {transfer!r}")
         self.step = TetrisStep(B, k, V, capacity, mode=mode, device=device)
         dev = self.step.device
-        # the staged path feeds the TMA sampler (32-byte rows): other vocabulary sizes read through the mapping
-        self.transfer = transfer if (mode == "stochastic" and V % 8 == 0) else "zero-copy"
+        self.mode = mode
+        # the staged stochastic path feeds the TMA sampler (32-byte rows): other vocabulary sizes read through the
+        # mapping
+        self.transfer = transfer if (mode == "greedy" or V % 8 == 0) else "zero-copy"
+        if q_host is not None and q_host.numel() == 0:
+            q_host = None
+        if mode == "stochastic" and k > 0 and q_host is None:
+            raise ValueError("q_host is required for stochastic verification with k > 0")
         self.p_host, self.q_host = p_host, q_host
         self.p = _MappedTensor(p_host)
-        self.q = _MappedTensor(q_host) if q_host is not None else None
-        if self.transfer == "staged":
+        # k == 0 (nothing drafted): no draft rows exist; an empty device tensor stands in (null pointer in the ABI)
+        self.q = _MappedTensor(q_host) if q_host is not None else torch.empty(B, 0, V, dtype=_F32, device=dev)
+        if self.transfer == "staged" and mode == "stochastic":
             self.staging = torch.empty(2 * B, V, dtype=torch.float32, device=dev)
             self.rowinfo_host = torch.empty(2 * B, dtype=_I64).pin_memory()
+        elif self.transfer == "staged":
+            self.p_dev = torch.empty(B, k + 1, V, dtype=torch.float32, device=dev)
+            self.windows_host = torch.empty(B, dtype=_I32).pin_memory()
         self.conf = torch.empty(B, k, dtype=_F64, device=dev)
         self.lengths = torch.empty(B, dtype=_I32, device=dev)
         self.d = torch.empty(B, k, dtype=_I32, device=dev)
@@ -622,8 +646,10 @@ class HostTetrisStep:
         self.B, self.k, self.V = B, k, V
 
     def h2d_bytes(self) -> int:
+        """Bytes of the explicit per-request input copies (the probability rows come on top, see the bench)."""
         B, k = self.B, self.k
-        return B * k * 8 + B * 4 + B * k * 4 + B * k * 8 + B * 8
+        n = B * k * 8 + B * 4 + B * k * 4
+        return n + (B * k * 8 + B * 8 if self.mode == "stochastic" else 0)
 
     def d2h_bytes(self) -> int:
         return (self.B + 1) * 4 + self.B * (self.k + 1) * 4 + self.B * 4
@@ -635,17 +661,25 @@ class HostTetrisStep:
         if u_acc_h is not None:
             self.u_acc.copy_(u_acc_h, non_blocking=True)
             self.u_res.copy_(u_res_h, non_blocking=True)
-        if self.transfer == "staged" and self.step.group is None:
-            st = self.step
+        st = self.step
+        s = torch.cuda.current_stream().cuda_stream
+        if self.transfer == "staged" and st.group is None and self.mode == "stochastic":
             st._check(st._lib.tetris_step_stochastic_staged_f32(
                 self.conf.data_ptr(), self.lengths.data_ptr(), self.B, self.k, st.C, self.p_host.data_ptr(),
-                self.q_host.data_ptr(), self.d.data_ptr(), self.u_acc.data_ptr(), self.u_res.data_ptr(), None,
+                _ptr(self.q_host), self.d.data_ptr(), self.u_acc.data_ptr(), self.u_res.data_ptr(), None,
                 self.V, self.staging.data_ptr(), self.rowinfo_host.data_ptr(), st.windows_all.data_ptr(),
                 st.win_offsets.data_ptr(), st.accepted.data_ptr(), st.out_tok.data_ptr(), st.mass.data_ptr(),
                 st.offsets.data_ptr(), st.tokens.data_ptr(), st.stats.data_ptr(), st.status.data_ptr(), st.ws.ptr,
-                st.ws.nbytes, torch.cuda.current_stream().cuda_stream))
+                st.ws.nbytes, s))
+        elif self.transfer == "staged" and st.group is None:
+            st._check(st._lib.tetris_step_greedy_staged_f32(
+                self.conf.data_ptr(), self.lengths.data_ptr(), self.B, self.k, st.C, self.p_host.data_ptr(),
+                self.d.data_ptr(), None, self.V, self.p_dev.data_ptr(), self.windows_host.data_ptr(),
+                st.windows_all.data_ptr(), st.win_offsets.data_ptr(), st.accepted.data_ptr(), st.out_tok.data_ptr(),
+                st.offsets.data_ptr(), st.tokens.data_ptr(), st.stats.data_ptr(), st.status.data_ptr(), st.ws.ptr,
+                st.ws.nbytes, s))
         else:
-            self.step.run(self.conf, self.lengths, self.p, self.q, self.d, self.u_acc, self.u_res)
-        self.offsets_host.copy_(self.step.offsets, non_blocking=True)
-        self.tokens_host.copy_(self.step.tokens, non_blocking=True)
-        self.accepted_host.copy_(self.step.accepted, non_blocking=True)
+            st.run(self.conf, self.lengths, self.p, self.q, self.d, self.u_acc, self.u_res)
+        self.offsets_host.copy_(st.offsets, non_blocking=True)
+        self.tokens_host.copy_(st.tokens, non_blocking=True)
+        self.accepted_host.copy_(st.accepted, non_blocking=True)

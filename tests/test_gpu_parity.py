@@ -536,3 +536,56 @@ def test_step_stochastic_any_vocabulary(V):
     off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
     assert np.array_equal(_np(step.offsets), off_ref)
     assert np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
+
+
+
+@pytest.mark.parametrize("B,k", [(4096, 16), (1000, 40), (20000, 3)])
+def test_cluster_selector_without_workspace(B, k):
+    """tetris_select_f64 with no workspace runs the cluster/DSMEM select_kernel for B*k > 16384 (register path for
+    k <= 16, shared-memory path above); bit-exact against the oracle like the workspace selectors."""
+    rng = np.random.default_rng(B + k)
+    a = torch.from_numpy(rng.random((B, k)) ** 0.3).to(DEV)
+    ln = torch.from_numpy(rng.integers(1, k + 1, B).astype(np.int32)).to(DEV)
+    for C in (1, B, B * k // 3, B * k - 1):
+        w = torch.empty(B, dtype=torch.int32, device=DEV)
+        off = torch.empty(B + 1, dtype=torch.int32, device=DEV)
+        cum = torch.zeros(B, k, dtype=torch.float64, device=DEV)
+        st = torch.zeros(4, dtype=torch.int64, device=DEV)
+        status = ops.new_status(DEV)
+        N.call("tetris_select_f64", a.data_ptr(), ln.data_ptr(), B, k, C, 0, w.data_ptr(), off.data_ptr(),
+               cum.data_ptr(), st.data_ptr(), status.data_ptr(), None, 0, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        ops.raise_for_status(status)
+        w_ref, cum_ref, st_ref = O.select(_np(a), C, _np(ln))
+        assert np.array_equal(_np(w), w_ref)
+        assert list(_np(st)[:3]) == list(st_ref[:3])
+        assert np.array_equal(np.diff(_np(off)), w_ref)
+
+
+def test_misaligned_probabilities_take_the_stage_by_stage_path():
+    """A contiguous but not 16-byte aligned p / q view (V % 8 == 0) must not reach the TMA sampler:
+    TetrisStep routes it to the stage-by-stage kernels with identical results."""
+    B, k, V, C = 32, 4, 4096, 80
+    bt = make_batch(B, k, V, seed=4)
+    pb = torch.empty(bt.p.numel() + 1, dtype=torch.float32, device=DEV)
+    qb = torch.empty(bt.q.numel() + 1, dtype=torch.float32, device=DEV)
+    p = pb[1:].view(bt.p.shape)
+    q = qb[1:].view(bt.q.shape)
+    p.copy_(bt.p)
+    q.copy_(bt.q)
+    assert p.data_ptr() % 16 and q.data_ptr() % 16 and p.is_contiguous()
+    s1 = ops.TetrisStep(B, k, V, C)
+    s1.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    s2 = ops.TetrisStep(B, k, V, C)
+    s2.run(bt.conf, bt.lengths, p, q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    ops.raise_for_status(s2.status)
+    assert torch.equal(s1.accepted, s2.accepted) and torch.equal(s1.out_tok, s2.out_tok)
+    assert torch.equal(s1.offsets, s2.offsets)
+
+
+def test_spec_max_requests_follows_the_device():
+    from paper_2502_15197_b200 import _native as N2
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert N2.spec_max_requests() == min(4096, 32 * sms)

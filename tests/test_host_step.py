@@ -17,7 +17,7 @@ def _np(t):
 
 
 @pytest.mark.parametrize("mode,transfer", [("stochastic", "staged"), ("stochastic", "zero-copy"),
-                                           ("greedy", "zero-copy")])
+                                           ("greedy", "staged"), ("greedy", "zero-copy")])
 @pytest.mark.parametrize("B,k,V,C", [(64, 8, 16384, 200), (200, 5, 8200, 500), (40, 3, 1003, 60)])
 def test_host_step_matches_device_step(mode, transfer, B, k, V, C):
     bt = make_batch(B, k, V, seed=B + k, mode=mode, ragged=True)
@@ -45,3 +45,44 @@ def test_host_step_matches_device_step(mode, transfer, B, k, V, C):
     off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
     assert np.array_equal(hs.offsets_host.numpy(), off_ref)
     assert np.array_equal(hs.tokens_host.numpy()[: off_ref[-1]], toks_ref)
+
+
+@pytest.mark.parametrize("mode", ["stochastic", "greedy"])
+@pytest.mark.parametrize("transfer", ["staged", "zero-copy"])
+def test_host_step_k0(mode, transfer):
+    """k = 0 (nothing drafted): every request emits its bonus token; q_host may be None."""
+    B, k, V, C = 32, 0, 4096, 10
+    bt = make_batch(B, k, V, seed=3, mode=mode)
+    dev_step = ops.TetrisStep(B, k, V, C, mode=mode)
+    dev_step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    hs = ops.HostTetrisStep(B, k, V, C, bt.p.cpu().pin_memory(), None, mode=mode, transfer=transfer)
+    small = [t.cpu().pin_memory() for t in (bt.conf, bt.lengths, bt.d, bt.u_acc, bt.u_res)]
+    hs.run(*(small if mode == "stochastic" else small[:3]))
+    torch.cuda.synchronize()
+    ops.raise_for_status(hs.step.status)
+    assert int(hs.offsets_host[-1]) == B
+    assert np.array_equal(hs.tokens_host.numpy()[:B], _np(dev_step.tokens)[:B])
+
+
+def test_pageable_host_inputs_are_registered_and_released():
+    """tetris_map_host registers pageable memory itself; the mapping is released with the step."""
+    from paper_2502_15197_b200 import _native as N
+
+    B, k, V, C = 16, 4, 2048, 40
+    bt = make_batch(B, k, V, seed=9)
+    p_h, q_h = bt.p.cpu(), bt.q.cpu()  # pageable
+    small = [t.cpu() for t in (bt.conf, bt.lengths, bt.d, bt.u_acc, bt.u_res)]
+    hs = ops.HostTetrisStep(B, k, V, C, p_h, q_h, transfer="zero-copy")
+    hs.run(*small)
+    torch.cuda.synchronize()
+    ops.raise_for_status(hs.step.status)
+    ptr = p_h.data_ptr()
+    del hs
+    import gc
+
+    gc.collect()
+    # unregistered: mapping it again registers anew (would fail with cudaErrorHostMemoryAlreadyRegistered otherwise)
+    dptr = N.map_host(ptr, p_h.numel() * 4)
+    assert dptr != 0
+    N.unmap_host(ptr)
