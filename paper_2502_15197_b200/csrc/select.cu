@@ -746,7 +746,7 @@ extern "C" int tetris_select_f64(const double* vals, const int32_t* len, int32_t
     }
     return TETRIS_OK;
   }
-  if (!vals || !windows) return abi::fail(TETRIS_INVALID_ARGUMENT, "vals and windows are required");
+  if ((k > 0 && !vals) || !windows) return abi::fail(TETRIS_INVALID_ARGUMENT, "vals and windows are required");
   SelectArgs a = {};
   a.vals = vals;
   a.len = len;
