@@ -65,6 +65,28 @@ typedef struct CUstream_st* tetris_stream_t; /* == cudaStream_t */
 #define TETRIS_CHUNK_WARPS 8
 #define TETRIS_CHUNK_ELEMS (TETRIS_SEG_ELEMS * TETRIS_WARP_SEGS * TETRIS_CHUNK_WARPS) /* 8192 */
 
+/* ---- the logits contract (bf16 entry points) --------------------------------------------------------------
+ * Entry points taking bf16 logits z (raw uint16 bf16 bits) and a caller-supplied fp32 log-sum-exp per row define each
+ * probability as the fp32 value prob(z, lse) below (every operation IEEE fp32 round-to-nearest-even, FMA fused), then
+ * apply the fp32 contract above to it unchanged (accept test, residual / bonus weights, sampling):
+ *   x = (float)z + (-lse);  x = min(max(x, TETRIS_EXP_LO), TETRIS_EXP_HI)     (NaN -> TETRIS_EXP_LO)
+ *   t = fma(x, TETRIS_EXP_L2E, TETRIS_EXP_MAGIC);  j = t + (-TETRIS_EXP_MAGIC);  r = fma(j, -TETRIS_EXP_LN2, x)
+ *   e = fma(fma(fma(fma(fma(C5, r, C4), r, C3), r, C2), r, C1), r, C0)
+ *   bits(prob) = bits(t) * 2^23 + bits(e)   (uint32 arithmetic, i.e. e * 2^round(x * log2(e)))
+ * Relative error against exp(x) <= 1e-6 for x in [-86, 88]; probabilities below exp(-86) read as ~exp(-86).  The CPU
+ * oracle (oracle/tetris_oracle.c, oracle_probs_from_logits_bf16) computes the same bits with C fmaf(). */
+#define TETRIS_EXP_LO (-86.0f)
+#define TETRIS_EXP_HI 88.0f
+#define TETRIS_EXP_L2E 0x1.715476p+0f
+#define TETRIS_EXP_LN2 0x1.62e430p-1f
+#define TETRIS_EXP_MAGIC 0x1.8p+23f
+#define TETRIS_EXP_C0 0x1p+0f
+#define TETRIS_EXP_C1 0x1.ffffdep-1f
+#define TETRIS_EXP_C2 0x1.fffde6p-2f
+#define TETRIS_EXP_C3 0x1.556974p-3f
+#define TETRIS_EXP_C4 0x1.571f3cp-5f
+#define TETRIS_EXP_C5 0x1.08822ap-7f
+
 #define TETRIS_MAX_K 255        /* depth fits the 8-bit tie-break field of the selection key                  */
 #define TETRIS_MAX_SELECT_ROWS 65535
 
@@ -179,6 +201,35 @@ int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B
                                int32_t V, int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
                                double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status,
                                void* ws, size_t ws_bytes, tetris_stream_t stream);
+
+/* The same stochastic step on LOGITS ("fused logits -> probs"): zp [B][k+1][V] and zq [B][k][V] are
+ * bf16 logits (raw uint16 bits) with a caller-supplied fp32 log-sum-exp per row, lse_p [B][k+1] and lse_q [B][k]
+ * (the LM head's softmax normaliser).  Every probability the step reads is prob(z, lse) of the logits contract above,
+ * computed on the fly inside the kernels (the accept-test gathers, the streamed rows, the descent): the results equal
+ * tetris_step_stochastic_f32's on p = prob(zp, lse_p), q = prob(zq, lse_q) bit for bit, while the streamed bytes
+ * halve.  V % 8 == 0 and 16-byte aligned zp / zq.  Also as its two halves (tetris_select_accept_bf16, then
+ * tetris_resample_bf16 with u_acc / len non-NULL for the speculative start, B <= tetris_spec_max_requests()). */
+int tetris_step_stochastic_bf16(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                int32_t row0, int32_t B, const uint16_t* zp, const float* lse_p, const uint16_t* zq,
+                                const float* lse_q, const int32_t* d, const double* u_acc, int32_t u_packed,
+                                const double* u_res, const int32_t* cap, int32_t V, int32_t* windows,
+                                int32_t* win_offsets, int32_t* accepted, int32_t* out_tok, double* mass_out,
+                                int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
+                                size_t ws_bytes, tetris_stream_t stream);
+int tetris_select_accept_bf16(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                              int32_t row0, int32_t B, const uint16_t* zp, const float* lse_p, const uint16_t* zq,
+                              const float* lse_q, const int32_t* d, const double* u_acc, int32_t u_packed,
+                              const int32_t* cap, int32_t V, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
+                              int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
+                              size_t ws_bytes, tetris_stream_t stream);
+int tetris_resample_bf16(const uint16_t* zp, const float* lse_p, const uint16_t* zq, const float* lse_q,
+                         const double* u_res, const double* u_acc, const int32_t* len, int32_t B, int32_t k, int32_t V,
+                         const int32_t* d, const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
+                         double* mass_out, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
+                         tetris_stream_t stream);
+/* The logits contract materialised: out[r][v] = prob(z[r][v], lse[r]) for R rows of V (fp32 out). */
+int tetris_probs_from_logits_bf16(const uint16_t* z, const float* lse, int64_t R, int32_t V, float* out,
+                                  tetris_stream_t stream);
 
 /* Stage (3) greedy: verify_token on one-hot distributions (accept_model.py:309-313): position j is accepted iff
  * d[b][j] == argmax_v p[b][j][v] (first maximal index, NaN ranks highest as in numpy.argmax); the emitted token is

@@ -46,6 +46,8 @@ def _load():
                                                      _p, C.c_int]
         lib.oracle_verify_greedy_f32.restype = None
         lib.oracle_verify_greedy_f32.argtypes = [_p, _p, _p, C.c_int, C.c_int, C.c_int, _p, _p, C.c_int]
+        lib.oracle_probs_from_logits_bf16.restype = None
+        lib.oracle_probs_from_logits_bf16.argtypes = [_p, _p, C.c_int64, C.c_int, _p]
         lib.oracle_compact.restype = None
         lib.oracle_compact.argtypes = [_p, _p, _p, _p, C.c_int, C.c_int, _p, _p]
         _lib = lib
@@ -160,3 +162,15 @@ def compact(accepted, out_tok, d, cap=None):
     tokens = np.zeros(B * (k + 1), np.int32)
     _load().oracle_compact(_ptr(acc), _ptr(tok), _ptr(d), _ptr(capa), B, k, _ptr(offsets), _ptr(tokens))
     return offsets, tokens[: offsets[-1]]
+
+
+def probs_from_logits_bf16(z_bits, lse):
+    """The logits contract (include/tetris_b200.h): z_bits [..., V] uint16 bf16 bits, lse [...] f32 -> fp32 probs."""
+    z = _a(z_bits, np.uint16)
+    lse = _a(lse, np.float32)
+    V = z.shape[-1]
+    R = int(np.prod(z.shape[:-1]))
+    assert lse.size == R
+    out = np.empty(z.shape, np.float32)
+    _load().oracle_probs_from_logits_bf16(_ptr(z), _ptr(lse), R, V, _ptr(out))
+    return out

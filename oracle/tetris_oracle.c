@@ -18,6 +18,9 @@
  *   oracle_verify_greedy     verify_token on one-hot distributions (accept_model.py:309-313) = argmax match.
  *   oracle_compact           credit min(acc+1, remaining) (sim_engine.py:467-471) + token gather.
  *   oracle_expected_accepted expected_accepted (selector.py:286-306).
+ *   oracle_probs_from_logits_bf16  the logits contract of include/tetris_b200.h (bf16 logits + row lse -> fp32
+ *                            probabilities with C fmaf()); no reference counterpart: the logits
+ *                            steps are checked as the fp32 oracle applied to these probabilities.
  * Pinned against golden vectors produced by the reference itself: tests/golden/ (tests/golden/make_golden.py).
  *
  * Build: oracle/Makefile (gcc -O2 -ffp-contract=off: every fp64 operation is one IEEE round-to-nearest op).
@@ -448,4 +451,30 @@ void oracle_compact(const int32_t* accepted, const int32_t* out_tok, const int32
     off += n;
   }
   offsets[B] = (int32_t)off;
+}
+
+/* ---- the logits contract (tetris_b200.h): prob(z, lse) with C99 fmaf (correctly rounded), fp32 RN ------------ */
+static float prob_from_logit(uint16_t z16, float lse) {
+  union {
+    uint32_t u;
+    float f;
+  } z, t, e, o;
+  z.u = (uint32_t)z16 << 16;
+  float x = z.f + (-lse);
+  x = fminf(fmaxf(x, TETRIS_EXP_LO), TETRIS_EXP_HI);
+  t.f = fmaf(x, TETRIS_EXP_L2E, TETRIS_EXP_MAGIC);
+  const float j = t.f + (-TETRIS_EXP_MAGIC);
+  const float r = fmaf(j, -TETRIS_EXP_LN2, x);
+  float p = fmaf(TETRIS_EXP_C5, r, TETRIS_EXP_C4);
+  p = fmaf(p, r, TETRIS_EXP_C3);
+  p = fmaf(p, r, TETRIS_EXP_C2);
+  p = fmaf(p, r, TETRIS_EXP_C1);
+  e.f = fmaf(p, r, TETRIS_EXP_C0);
+  o.u = (t.u << 23) + e.u;
+  return o.f;
+}
+
+void oracle_probs_from_logits_bf16(const uint16_t* z, const float* lse, int64_t R, int V, float* out) {
+  for (int64_t r = 0; r < R; ++r)
+    for (int v = 0; v < V; ++v) out[r * V + v] = prob_from_logit(z[r * V + v], lse[r]);
 }

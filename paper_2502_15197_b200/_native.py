@@ -78,6 +78,15 @@ _SIGNATURES = {
     "tetris_step_stochastic_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p,
                   _p, _p, _p, _sz, _p]),
+    "tetris_step_stochastic_bf16": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _i32, _p, _p, _p, _p, _p,
+                  _p, _p, _p, _p, _p, _sz, _p]),
+    "tetris_select_accept_bf16": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p,
+                  _p, _p, _sz, _p]),
+    "tetris_resample_bf16": (
+        C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "tetris_probs_from_logits_bf16": (C.c_int, [_p, _p, _i64, _i32, _p, _p]),
     "tetris_verify_greedy_f32": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_step_stochastic_staged_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,

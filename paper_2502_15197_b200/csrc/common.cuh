@@ -113,6 +113,90 @@ __device__ __forceinline__ int seq_find(const double* v, int n, double& T) {
   return last;
 }
 
+// ---- logits -> probabilities (the logits contract, tetris_b200.h) ------------------------------------------------
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t z16) { return __uint_as_float(z16 << 16); }
+
+// Scalar prob(z, lse) (gathers: the accept test, the descent's recomputation)
+__device__ __forceinline__ float prob_from_logit(float z, float lse) {
+  float x = __fadd_rn(z, -lse);
+  x = fminf(fmaxf(x, TETRIS_EXP_LO), TETRIS_EXP_HI);
+  const float t = __fmaf_rn(x, TETRIS_EXP_L2E, TETRIS_EXP_MAGIC);
+  const float j = __fadd_rn(t, -TETRIS_EXP_MAGIC);
+  const float r = __fmaf_rn(j, -TETRIS_EXP_LN2, x);
+  float e = __fmaf_rn(TETRIS_EXP_C5, r, TETRIS_EXP_C4);
+  e = __fmaf_rn(e, r, TETRIS_EXP_C3);
+  e = __fmaf_rn(e, r, TETRIS_EXP_C2);
+  e = __fmaf_rn(e, r, TETRIS_EXP_C1);
+  e = __fmaf_rn(e, r, TETRIS_EXP_C0);
+  return __uint_as_float((__float_as_uint(t) << 23) + __float_as_uint(e));
+}
+
+// Packed fp32x2 (FFMA2 / FADD2 on sm_100a): two elements per instruction on the FMA pipe; elementwise IEEE RN, so the
+// results are the scalar function's bits.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// prob(z, lse) for the two bf16 logits packed in `w` (element 0 in the low half).  nlse2 = pk2(-lse, -lse).
+__device__ __forceinline__ void prob2_from_bf16(uint32_t w, f32x2 nlse2, float& p0, float& p1) {
+  float x0, x1;
+  upk2(add2(pk2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)), nlse2), x0, x1);
+  x0 = fminf(fmaxf(x0, TETRIS_EXP_LO), TETRIS_EXP_HI);
+  x1 = fminf(fmaxf(x1, TETRIS_EXP_LO), TETRIS_EXP_HI);
+  const f32x2 x = pk2(x0, x1);
+  const f32x2 t = fma2(x, pk2(TETRIS_EXP_L2E, TETRIS_EXP_L2E), pk2(TETRIS_EXP_MAGIC, TETRIS_EXP_MAGIC));
+  const f32x2 j = add2(t, pk2(-TETRIS_EXP_MAGIC, -TETRIS_EXP_MAGIC));
+  const f32x2 r = fma2(j, pk2(-TETRIS_EXP_LN2, -TETRIS_EXP_LN2), x);
+  f32x2 e = fma2(pk2(TETRIS_EXP_C5, TETRIS_EXP_C5), r, pk2(TETRIS_EXP_C4, TETRIS_EXP_C4));
+  e = fma2(e, r, pk2(TETRIS_EXP_C3, TETRIS_EXP_C3));
+  e = fma2(e, r, pk2(TETRIS_EXP_C2, TETRIS_EXP_C2));
+  e = fma2(e, r, pk2(TETRIS_EXP_C1, TETRIS_EXP_C1));
+  e = fma2(e, r, pk2(TETRIS_EXP_C0, TETRIS_EXP_C0));
+  float t0, t1, e0, e1;
+  upk2(t, t0, t1);
+  upk2(e, e0, e1);
+  p0 = __uint_as_float((__float_as_uint(t0) << 23) + __float_as_uint(e0));
+  p1 = __uint_as_float((__float_as_uint(t1) << 23) + __float_as_uint(e1));
+}
+
+// 8 consecutive bf16 logits (one 16-byte word) -> 8 probabilities
+__device__ __forceinline__ void prob8_from_bf16(const uint4 raw, float lse, float (&v)[8]) {
+  const f32x2 nl = pk2(-lse, -lse);
+  prob2_from_bf16(raw.x, nl, v[0], v[1]);
+  prob2_from_bf16(raw.y, nl, v[2], v[3]);
+  prob2_from_bf16(raw.z, nl, v[4], v[5]);
+  prob2_from_bf16(raw.w, nl, v[6], v[7]);
+}
+
+// The probability of token t in row `row` of the target (p) / draft (q) input, whichever form the kernel was given:
+// fp32 probabilities, or bf16 logits + per-row lse (A: SelectArgs / StreamArgs).
+template <typename A>
+__device__ __forceinline__ double gather_p(const A& a, int64_t row, int t) {
+  if (a.zp) return (double)prob_from_logit(bf16_bits_to_f32(a.zp[row * a.V + t]), a.lse_p[row]);
+  return (double)a.p[row * a.V + t];
+}
+template <typename A>
+__device__ __forceinline__ double gather_q(const A& a, int64_t row, int t) {
+  if (a.zq) return (double)prob_from_logit(bf16_bits_to_f32(a.zq[row * a.V + t]), a.lse_q[row]);
+  return (double)a.q[row * a.V + t];
+}
+
 __device__ __forceinline__ void set_status(uint32_t* status, uint32_t bits) {
   if (status && bits) atomicOr(status, bits);
 }

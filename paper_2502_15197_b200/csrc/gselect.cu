@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
 
   // ---- accept verdicts of this CTA's rows in the epilogue range, issued first (two dependent gathers each) --------
   const int ep0 = a.ep_row0, ep1 = a.ep_row0 + a.ep_rows;
-  if (a.p != nullptr) {
+  if (a.p != nullptr || a.zp != nullptr) {
     const int lo_r = max(r0, ep0), hi_r = min(r0 + nr, ep1);
     for (int e = tid; e < (hi_r - lo_r) * k; e += kGThreads) {
       const int r = lo_r + e / k, j = e - (e / k) * k;
@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
         if (t < 0 || t >= a.V) {
           v |= 2;
         } else {
-          const double s = (double)a.q[pos * a.V + t];
-          const double m = (double)a.p[((int64_t)lr * (k + 1) + j) * a.V + t];
+          const double s = gather_q(a, pos, t);
+          const double m = gather_p(a, (int64_t)lr * (k + 1) + j, t);
           v |= ((s <= m) || (u < m / s)) ? 1 : 0;  // accept_model.py:311-313
         }
       }
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
   if (stamp) a.dbg[4] = clock64();
 
   // ---- epilogue (fused step): first rejection, the row to resample from, compaction offsets ----------------------
-  if (a.p != nullptr) {
+  if (a.p != nullptr || a.zp != nullptr) {
     uint32_t vbad = 0;
     const bool mine = row && gr >= ep0 && gr < ep1;
     int n_emit = 0;

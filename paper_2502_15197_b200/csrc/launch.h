@@ -22,6 +22,10 @@ struct SelectArgs {
   int ep_row0, ep_rows;
   const float* p;
   const float* q;
+  const uint16_t* zp;   // logits form (nullptr: fp32 probabilities p / q): bf16 logits + per-row lse
+  const uint16_t* zq;
+  const float* lse_p;
+  const float* lse_q;
   const int32_t* d;
   const double* u_acc;
   int u_packed;
@@ -47,6 +51,10 @@ long long* debug_buffer();
 struct StreamArgs {
   const float* p;
   const float* q;
+  const uint16_t* zp;  // logits form (the bf16 kernels): bf16 logits rows + per-row lse; p / q unused
+  const uint16_t* zq;
+  const float* lse_p;
+  const float* lse_q;
   int V, nch, R;
   const long long* prow;     // p row of request b at prow[b * row_stride]
   const long long* qrow;     // q row (-1: plain / bonus row) at qrow[b * row_stride]; nullptr: all plain
@@ -113,8 +121,7 @@ bool persist_greedy_eligible(const float* p, int V);
 int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys, int j0,
                          cudaStream_t st);
 int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st);
-int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,
-                      int B, int k, int V, uint8_t* acc_bytes, cudaStream_t st);
+int launch_pre_accept(const SelectArgs& a, cudaStream_t st);
 int launch_accept(const float* p, const float* q, const int32_t* d, const int32_t* windows, const int32_t* win_off,
                   const double* u_acc, int B, int k, int V, int32_t* accepted, long long* rowinfo, uint32_t* status,
                   cudaStream_t st);

@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(REG ? kRegMaxThreads : kSelMaxThreads, 1) sele
         if (t < 0 || t >= a.V) {
           v |= 2;
         } else {
-          const double s = (double)a.q[e * a.V + t];
-          const double m = (double)a.p[((int64_t)b * (k + 1) + j) * a.V + t];
+          const double s = gather_q(a, e, t);
+          const double m = gather_p(a, (int64_t)b * (k + 1) + j, t);
           v |= ((s <= m) || (u < m / s)) ? 1 : 0;
         }
       }
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(REG ? kRegMaxThreads : kSelMaxThreads, 1) sele
   if (stamp) a.dbg[4] = clock64();
 
   // ---- optional epilogue: first rejection, row to resample from, compaction offsets (fused step) ---------------
-  if (a.p != nullptr) {
+  if (a.p != nullptr || a.zp != nullptr) {
     uint32_t vbad = 0;
     const int ep0 = a.ep_row0, ep1 = a.ep_row0 + a.ep_rows;
     if (a.accept_ctas > 0 && tid == 0) {
@@ -468,8 +468,8 @@ __global__ void __launch_bounds__(REG ? kRegMaxThreads : kSelMaxThreads, 1) sele
           for (int i = 0; i < 8; ++i) {
             const int j = j0 + i;
             const bool ok = (j < w) && t[i] >= 0 && t[i] < a.V;
-            s[i] = ok ? (double)a.q[((int64_t)lr * k + j) * a.V + t[i]] : 0.0;
-            m[i] = ok ? (double)a.p[((int64_t)lr * (k + 1) + j) * a.V + t[i]] : 0.0;
+            s[i] = ok ? gather_q(a, (int64_t)lr * k + j, t[i]) : 0.0;
+            m[i] = ok ? gather_p(a, (int64_t)lr * (k + 1) + j, t[i]) : 0.0;
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -713,8 +713,7 @@ int launch_select(const SelectArgs& args_in, cudaStream_t st) {
   if (e != cudaSuccess && extra_clusters > 0) {
     // cooperative cluster launch unavailable: run the verdicts as their own grid first, then the selection
     cudaGetLastError();
-    int rc = launch_pre_accept(a.p, a.q, a.d, a.u_acc, a.len ? a.len + a.ep_row0 : nullptr, a.ep_rows, a.k, a.V,
-                               a.acc_bytes, st);
+    int rc = launch_pre_accept(a, st);
     if (rc) return rc;
     a.accept_ctas = 0;
     cfg.gridDim = dim3(G, 1, 1);

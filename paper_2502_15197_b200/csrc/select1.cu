@@ -50,8 +50,8 @@ __device__ void accept_role(const SelectArgs& a, int acta, int nacta) {
       if (t < 0 || t >= a.V) {
         v |= 2;
       } else {
-        const double s = (double)a.q[e * a.V + t];
-        const double m = (double)a.p[((int64_t)b * (k + 1) + j) * a.V + t];
+        const double s = gather_q(a, e, t);
+        const double m = gather_p(a, (int64_t)b * (k + 1) + j, t);
         v |= ((s <= m) || (u < m / s)) ? 1 : 0;
       }
     }
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(NT, 1) select1_kernel(const SelectArgs a) {
   }
 
   // ---- optional epilogue: first rejection, row to resample from, compaction offsets --------------------------------
-  if (a.p != nullptr) {
+  if (a.p != nullptr || a.zp != nullptr) {
     uint32_t vbad = 0;
     const int ep0 = a.ep_row0, ep1 = a.ep_row0 + a.ep_rows;
     if (a.accept_ctas > 0) {
@@ -405,8 +405,8 @@ __global__ void __launch_bounds__(NT, 1) select1_kernel(const SelectArgs a) {
             vbad |= TETRIS_ST_BAD_TOKEN;
             rej = true;
           } else {
-            const double s = (double)a.q[((int64_t)lr * k + j) * a.V + t];
-            const double m = (double)a.p[((int64_t)lr * (k + 1) + j) * a.V + t];
+            const double s = gather_q(a, (int64_t)lr * k + j, t);
+            const double m = gather_p(a, (int64_t)lr * (k + 1) + j, t);
             rej = !(s <= m) && !(u < m / s);  // accept_model.py:311-313
           }
           if (rej) {

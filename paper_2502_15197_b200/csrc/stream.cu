@@ -26,7 +26,21 @@
 
 namespace tetris {
 
-constexpr int kStages = 3;
+// Element form of the streamed rows: fp32 probabilities (3 stages of 64 KB), or bf16 logits + per-row lse (the logits
+// contract, tetris_b200.h; 6 stages of 32 KB: the same bytes in flight per SM)
+template <bool BF>
+struct Elem {
+  using T = float;
+  static constexpr int kBytes = 4;
+  static constexpr int kStages = 3;
+};
+template <>
+struct Elem<true> {
+  using T = uint16_t;
+  static constexpr int kBytes = 2;
+  static constexpr int kStages = 6;
+};
+constexpr int kMaxStages = 6;
 constexpr int kConsumerWarps = 16;                         // 2 segments of the staged chunk each
 constexpr int kSegsPerChunk = kChunkElems / kSegElems;     // 32
 constexpr int kSegsPerConsumer = kSegsPerChunk / kConsumerWarps;
@@ -34,9 +48,13 @@ constexpr int kProducerWarp = kConsumerWarps;
 constexpr int kPublisherWarp = kConsumerWarps + 1;
 constexpr int kPersistThreads = (kConsumerWarps + 2) * 32;
 constexpr int kRing = 64;
-constexpr size_t kStageRowBytes = (size_t)kChunkElems * sizeof(float);  // 32 KB
-constexpr size_t kStageBytes = 2 * kStageRowBytes;                         // p + q chunk
-constexpr size_t kPersistSmem = kStages * kStageBytes;                     // 192 KB dynamic
+constexpr size_t kPersistSmem = 192 * 1024;  // dynamic: the stage ring (p + q chunk per stage)
+template <bool BF>
+__host__ __device__ constexpr size_t stage_row_bytes() { return (size_t)kChunkElems * Elem<BF>::kBytes; }
+template <bool BF>
+__host__ __device__ constexpr size_t stage_bytes() { return 2 * stage_row_bytes<BF>(); }
+static_assert(Elem<false>::kStages * stage_bytes<false>() == kPersistSmem, "fp32 ring");
+static_assert(Elem<true>::kStages * stage_bytes<true>() == kPersistSmem, "bf16 ring");
 
 
 
@@ -51,6 +69,7 @@ __device__ __forceinline__ void gstamp(const StreamArgs& a, int slot) {
 
 struct StageMeta {
   int b, c, res, phase;  // phase 1: speculative (phase A) item
+  float lp, lq;          // logits form: the lse of the p / q row
 };
 
 constexpr int kSpecMaxR = 4096;  // speculative variant: requests per call (lists in shared memory)
@@ -64,26 +83,38 @@ struct SpecShared {
 };
 
 struct PersistShared {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
   uint64_t ring_full[kRing];
   uint64_t ring_free[kRing];
-  StageMeta meta[kStages];
+  StageMeta meta[kMaxStages];
   StageMeta ring_meta[kRing];
   double ring_g[kRing][kSegsPerChunk];  // segment sums of each published chunk
 };
 
+// A lane's 8 staged elements as fp32 probabilities: an fp32 stage (two 16-byte halves, swizzled), or 8 bf16 logits
+// (one 16-byte word; consecutive lanes read consecutive words, conflict-free) through the logits contract.
+template <bool BF>
+__device__ __forceinline__ void stage_lane(const uint8_t* row, int off, int lane, float lse, float (&v)[8]) {
+  if (BF) {
+    prob8_from_bf16(*reinterpret_cast<const uint4*>(row + (size_t)off * 2), lse, v);
+  } else {
+    lds8_swz(reinterpret_cast<const float*>(row) + off, lane, v);
+  }
+}
+
 // Segment sum (lane fold + xor butterfly) of the staged segment at chunk offset `off0` (element e0 of the row).
-__device__ __forceinline__ double consume_segment(const float* __restrict__ sp, const float* __restrict__ sq, bool res,
-                                                  int64_t e0, int off0, int V, int lane) {
+template <bool BF>
+__device__ __forceinline__ double consume_segment(const uint8_t* __restrict__ sp, const uint8_t* __restrict__ sq,
+                                                  bool res, int64_t e0, int off0, int V, int lane, float lp, float lq) {
   const int off = off0 + lane * kLaneElems;
   double w[8];
   if (e0 + lane * kLaneElems < V) {
     float pv[8];
-    lds8_swz(sp + off, lane, pv);
+    stage_lane<BF>(sp, off, lane, lp, pv);
     if (res) {
       float qv[8];
-      lds8_swz(sq + off, lane, qv);
+      stage_lane<BF>(sq, off, lane, lq, qv);
 #pragma unroll
       for (int i = 0; i < 8; ++i) w[i] = w_res32(pv[i], qv[i]);
     } else {
@@ -97,16 +128,35 @@ __device__ __forceinline__ double consume_segment(const float* __restrict__ sp, 
   return seg_sum(fold8(w));
 }
 
+// A lane's 8 row elements from global memory as fp32 probabilities (zeros past the row end)
+template <bool BF>
+__device__ __forceinline__ void row_lane(const void* row, int64_t e, int V, float lse, float (&v)[8]) {
+  if (BF) {
+    if (e < V) {
+      uint4 raw;
+      asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+          : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+          : "l"(reinterpret_cast<const uint16_t*>(row) + e));
+      prob8_from_bf16(raw, lse, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    }
+  } else {
+    load_lane<float, true>(reinterpret_cast<const float*>(row), e, V, v);
+  }
+}
+
 // descent below the warp level, reading the warp run from global memory (all 32 lanes, T uniform)
-template <bool RES>
-__device__ int descend_global(const float* __restrict__ P, const float* __restrict__ Q, int64_t e0, int V, int lane,
-                              double T) {
+template <bool RES, bool BF>
+__device__ int descend_global(const void* __restrict__ P, const void* __restrict__ Q, int64_t e0, int V, int lane,
+                              double T, float lp, float lq) {
   double G[kWarpSegs];
   float pv[kWarpSegs][8], qv[kWarpSegs][8];
 #pragma unroll
   for (int s = 0; s < kWarpSegs; ++s) {
-    load_lane<float, true>(P, e0 + s * kSegElems + lane * kLaneElems, V, pv[s]);
-    if (RES) load_lane<float, true>(Q, e0 + s * kSegElems + lane * kLaneElems, V, qv[s]);
+    row_lane<BF>(P, e0 + s * kSegElems + lane * kLaneElems, V, lp, pv[s]);
+    if (RES) row_lane<BF>(Q, e0 + s * kSegElems + lane * kLaneElems, V, lq, qv[s]);
   }
 #pragma unroll
   for (int s = 0; s < kWarpSegs; ++s) {
@@ -155,11 +205,14 @@ __device__ int descend_global(const float* __restrict__ P, const float* __restri
 
 // Descent for request b after every chunk sum is published (one warp): the chunk and warp sums of all chunks are
 // fetched in one round trip (lane l holds sums l, l+32, ...), then the one warp run holding the sample is re-read.
+template <bool BF>
 __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane, const double* chunk_sums,
                                  const double* warp_sums) {
   const int nch = a.nch;
   const long long prow = a.prow[(int64_t)b * a.row_stride];
   const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+  const float lp = BF ? a.lse_p[prow] : 0.f;
+  const float lq = (BF && qrow >= 0) ? a.lse_q[qrow] : 0.f;
   const double* cs = chunk_sums + (int64_t)b * nch;
   const double* ws = warp_sums + (int64_t)b * nch * kChunkWarps;
   double s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
@@ -208,9 +261,11 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
     const int ww = seq_find(Wc, kChunkWarps, T);
     if (cc >= 0 && ww >= 0) {
       const int64_t e0 = (int64_t)cc * kChunkElems + ww * kWarpElems;
-      const float* Pr = a.p + prow * (int64_t)a.V;
-      tok = res ? descend_global<true>(Pr, a.q + qrow * (int64_t)a.V, e0, a.V, lane, T)
-                : descend_global<false>(Pr, nullptr, e0, a.V, lane, T);
+      const void* Pr = BF ? (const void*)(a.zp + prow * (int64_t)a.V) : (const void*)(a.p + prow * (int64_t)a.V);
+      const void* Qr = !res ? nullptr
+                       : BF ? (const void*)(a.zq + qrow * (int64_t)a.V) : (const void*)(a.q + qrow * (int64_t)a.V);
+      tok = res ? descend_global<true, BF>(Pr, Qr, e0, a.V, lane, T, lp, lq)
+                : descend_global<false, BF>(Pr, nullptr, e0, a.V, lane, T, lp, lq);
     }
   }
   if (tok < 0) bad |= TETRIS_ST_DEGENERATE;
@@ -222,26 +277,35 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
   }
 }
 
-// Producer helper: one item (request b, chunk c) of rows prow / qrow (qrow < 0: plain) into stage t.
+// Producer helper: one item (request b, chunk c) of rows prow / qrow (qrow < 0: plain) into stage t.  The logits
+// form's row lse values are loaded before the wait for a free stage, so their latency hides behind it.
+template <bool BF>
 __device__ __forceinline__ void issue_item(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, int b,
                                            int c, long long prow, long long qrow, int phase, uint64_t pol) {
-  const int s = t % kStages;
-  if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
-  const int n = min(kChunkElems, a.V - c * kChunkElems);
-  const uint32_t bytes = (uint32_t)n * sizeof(float);
+  constexpr int S = Elem<BF>::kStages;
   const bool res = qrow >= 0;
-  sh.meta[s] = StageMeta{b, c, res ? 1 : 0, phase};
-  float* sp = reinterpret_cast<float*>(stage_mem + s * kStageBytes);
+  const float lp = BF ? __ldg(a.lse_p + prow) : 0.f;
+  const float lq = (BF && res) ? __ldg(a.lse_q + qrow) : 0.f;
+  const int s = t % S;
+  if (t >= S) mbar_wait(&sh.empty[s], (uint32_t)(((t / S) & 1) ^ 1u));
+  const int n = min(kChunkElems, a.V - c * kChunkElems);
+  const uint32_t bytes = (uint32_t)n * Elem<BF>::kBytes;
+  sh.meta[s] = StageMeta{b, c, res ? 1 : 0, phase, lp, lq};
+  uint8_t* sp = stage_mem + s * stage_bytes<BF>();
+  const uint8_t* P = BF ? (const uint8_t*)a.zp : (const uint8_t*)a.p;
+  const uint8_t* Q = BF ? (const uint8_t*)a.zq : (const uint8_t*)a.q;
+  const int64_t eb = Elem<BF>::kBytes;
   mbar_arrive_expect_tx(&sh.full[s], res ? 2 * bytes : bytes);
-  bulk_g2s_stream(sp, a.p + prow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s], pol);
+  bulk_g2s_stream(sp, P + (prow * (int64_t)a.V + (int64_t)c * kChunkElems) * eb, bytes, &sh.full[s], pol);
   if (res)
-    bulk_g2s_stream(sp + kChunkElems, a.q + qrow * (int64_t)a.V + (int64_t)c * kChunkElems, bytes, &sh.full[s], pol);
+    bulk_g2s_stream(sp + stage_row_bytes<BF>(), Q + (qrow * (int64_t)a.V + (int64_t)c * kChunkElems) * eb, bytes,
+                    &sh.full[s], pol);
 }
 
 // Producer helper: stream the items (list[y], c), y < count, c < nch, taken one at a time from `work` in order with
 // two items of look-ahead on the counter and one on the row lookup — the plain producer's schedule over a list.
 // rows(b, prow, qrow) gives the rows of request b.  Returns the next stage index.
-template <typename Rows>
+template <bool BF, typename Rows>
 __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, const uint16_t* list,
                            int count, unsigned long long* work, int phase, uint64_t pol, Rows rows) {
   const int nch = a.nch;
@@ -257,13 +321,14 @@ __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stag
     if (i >= total) break;
     i_next2 = (long long)atomicAdd(work, 1ull);
     if (i_next < total) rows((int)list[i_next / nch], pn, qn);
-    issue_item(a, sh, stage_mem, t++, (int)list[i / nch], (int)(i % nch), prow, qrow, phase, pol);
+    issue_item<BF>(a, sh, stage_mem, t++, (int)list[i / nch], (int)(i % nch), prow, qrow, phase, pol);
   }
   return t;
 }
 
-template <bool SPEC>
+template <bool SPEC, bool BF>
 __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_stream_kernel(const StreamArgs a) {
+  constexpr int kStages = Elem<BF>::kStages;
   extern __shared__ __align__(128) uint8_t stage_mem[];
   __shared__ PersistShared sh;
   __shared__ SpecShared sx;  // speculative variant only
@@ -309,8 +374,8 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           if (t < 0 || t >= a.V) {
             rej = true;
           } else {
-            const double s = (double)a.q[(int64_t)b * k * a.V + t];
-            const double m = (double)a.p[(int64_t)b * (k + 1) * a.V + t];
+            const double s = gather_q(a, (int64_t)b * k, t);
+            const double m = gather_p(a, (int64_t)b * (k + 1), t);
             rej = !((s <= m) || (u < m / s));
           }
         }
@@ -371,7 +436,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           const int b = sx.own;
           for (int cc = 0; cc < nch; ++cc) {
             if (t == 0) gstamp(a, 2);
-            issue_item(a, sh, stage_mem, t++, b, cc, (long long)b * (k + 1), (long long)b * k, 1, pol);
+            issue_item<BF>(a, sh, stage_mem, t++, b, cc, (long long)b * (k + 1), (long long)b * k, 1, pol);
           }
         }
         long long i_cur = (long long)atomicAdd(work_a, 1ull);
@@ -384,8 +449,8 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           int e_nxt = 0;
           if (y_nxt < R) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e_nxt) : "l"(a.spec_list + y_nxt));
           if (t == 0) gstamp(a, 2);
-          issue_item(a, sh, stage_mem, t++, b_cur, (int)(i_cur % nch), (long long)b_cur * (k + 1),
-                     (long long)b_cur * k, 1, pol);
+          issue_item<BF>(a, sh, stage_mem, t++, b_cur, (int)(i_cur % nch), (long long)b_cur * (k + 1),
+                         (long long)b_cur * k, 1, pol);
           b_cur = e_nxt ? e_nxt - 1 : entry(i_nxt);
           i_cur = i_nxt;
           i_nxt = i_nxt2;
@@ -394,7 +459,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         mbar_wait(&sx.listB_ready, 0);
         asm volatile("griddepcontrol.wait;" ::: "memory");  // the selector's row info (no-op by now)
         gstamp(a, 1);
-        t = stream_list(a, sh, stage_mem, t, sx.listB, sx.countB, work, 0, pol,
+        t = stream_list<BF>(a, sh, stage_mem, t, sx.listB, sx.countB, work, 0, pol,
                         [&](int b, long long& pr, long long& qr) {
                           pr = a.prow[(int64_t)b * a.row_stride];
                           qr = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
@@ -437,7 +502,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           break;
         }
         if (t == 0) gstamp(a, 2);
-        issue_item(a, sh, stage_mem, t, (int)(i / nch), (int)(i % nch), prow, qrow, 0, pol);
+        issue_item<BF>(a, sh, stage_mem, t, (int)(i / nch), (int)(i % nch), prow, qrow, 0, pol);
       }
     }
     __syncwarp();
@@ -457,13 +522,14 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         break;
       }
       if (t == 0 && warp == 0 && lane == 0) gstamp(a, 4);
-      const float* sp = reinterpret_cast<const float*>(stage_mem + s * kStageBytes);
+      const uint8_t* sp = stage_mem + s * stage_bytes<BF>();
       double Gs[kSegsPerConsumer];
 #pragma unroll
       for (int x = 0; x < kSegsPerConsumer; ++x) {
         const int seg = warp * kSegsPerConsumer + x;
-        Gs[x] = consume_segment(sp, sp + kChunkElems, m.res != 0, (int64_t)m.c * kChunkElems + seg * kSegElems,
-                                seg * kSegElems, a.V, lane);
+        Gs[x] = consume_segment<BF>(sp, sp + stage_row_bytes<BF>(), m.res != 0,
+                                    (int64_t)m.c * kChunkElems + seg * kSegElems, seg * kSegElems, a.V, lane, m.lp,
+                                    m.lq);
       }
       __syncwarp();
       if (lane == 0) {
@@ -586,8 +652,8 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         }
       }
       __syncwarp();
-      finalize_request(a, b, qrow >= 0, lane, doneA ? a.chunk_sums_spec : a.chunk_sums,
-                       doneA ? a.warp_sums_spec : a.warp_sums);
+      finalize_request<BF>(a, b, qrow >= 0, lane, doneA ? a.chunk_sums_spec : a.chunk_sums,
+                           doneA ? a.warp_sums_spec : a.warp_sums);
     }
     // the last CTA out resets the work counters and the phase-A list (every producer is done with them)
     __syncthreads();
@@ -624,35 +690,35 @@ __global__ void __launch_bounds__(128) finalize_kernel(const StreamArgs a) {
   const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (b >= a.R) return;
   const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
-  finalize_request(a, b, qrow >= 0, lane, a.chunk_sums, a.warp_sums);
+  finalize_request<false>(a, b, qrow >= 0, lane, a.chunk_sums, a.warp_sums);
 }
 
 // ---- pre-accept: verify_token on every drafted position, one thread each (runs before the selection) -----------
 // The accept test of position (b, j) does not depend on the selection, so all B*k random gathers of p[b][j][d] and
 // q[b][j][d] are issued at once by a full grid instead of serially by the selector's single cluster.  Verdict byte:
 // bit0 accept (accept_model.py:311-313), bit1 draft token outside the vocabulary, bit2 uniform outside [0, 1).
-__global__ void pre_accept_kernel(const float* __restrict__ p, const float* __restrict__ q,
-                                  const int32_t* __restrict__ d, const double* __restrict__ u_acc,
-                                  const int32_t* __restrict__ len, int B, int k, int V, uint8_t* __restrict__ out) {
+__global__ void pre_accept_kernel(const SelectArgs a) {
+  const int B = a.ep_rows, k = a.k, V = a.V;
+  const int32_t* len = a.len ? a.len + a.ep_row0 : nullptr;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)B * k) return;
   const int b = (int)(e / k), j = (int)(e - (int64_t)b * k);
   const int L = len ? len[b] : k;
   if (j >= L) {
-    out[e] = 0;
+    a.acc_bytes[e] = 0;
     return;
   }
-  const int t = d[e];
-  const double u = u_acc[e];
+  const int t = a.d[e];
+  const double u = a.u_acc[e];
   uint8_t v = (u >= 0.0 && u < 1.0) ? 0 : 4;
   if (t < 0 || t >= V) {
     v |= 2;  // rejected
   } else {
-    const double s = (double)q[e * V + t];
-    const double m = (double)p[((int64_t)b * (k + 1) + j) * V + t];
+    const double s = gather_q(a, e, t);
+    const double m = gather_p(a, (int64_t)b * (k + 1) + j, t);
     v |= ((s <= m) || (u < m / s)) ? 1 : 0;
   }
-  out[e] = v;
+  a.acc_bytes[e] = v;
 }
 
 // ---- stand-alone accept test (verify_stochastic without the fused selector epilogue) ----------------------------
@@ -725,7 +791,11 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
                (a.R + (int)std::min<long long>((long long)a.R * a.nch, g_num_sms) - 1) /
                        (int)std::min<long long>((long long)a.R * a.nch, g_num_sms) > 32))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "speculative sampler: R=%d > %d or missing buffers", a.R, kSpecMaxR);
-  const void* fn = spec ? (const void*)persist_stream_kernel<true> : (const void*)persist_stream_kernel<false>;
+  const bool bf = a.zp != nullptr;
+  if (bf && (!a.lse_p || (a.qrow && (!a.zq || !a.lse_q)) || a.req_cnt == nullptr))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "logits form: zq / lse_p / lse_q and the fused descent are required");
+  const void* fn = spec ? (bf ? (const void*)persist_stream_kernel<true, true> : (const void*)persist_stream_kernel<true, false>)
+                        : (bf ? (const void*)persist_stream_kernel<false, true> : (const void*)persist_stream_kernel<false, false>);
   cudaError_t e = abi::ensure_smem(fn, kPersistSmem);
   if (e != cudaSuccess) return abi::cuda_fail(e);
   const long long items = (long long)a.R * a.nch;
@@ -748,7 +818,7 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
     if (e != cudaSuccess) return abi::cuda_fail(e);
     return abi::launch_check();
   }
-  persist_stream_kernel<false><<<grid, kPersistThreads, kPersistSmem, st>>>(a);
+  persist_stream_kernel<false, false><<<grid, kPersistThreads, kPersistSmem, st>>>(a);
   int rc = abi::launch_check();
   if (rc) return rc;
   finalize_kernel<<<(a.R + 3) / 4, 128, 0, st>>>(a);
@@ -764,11 +834,10 @@ bool persist_eligible(const float* p, const float* q, int V) {
          n_chunks(V) <= 64;
 }
 
-int launch_pre_accept(const float* p, const float* q, const int32_t* d, const double* u_acc, const int32_t* len,
-                      int B, int k, int V, uint8_t* acc_bytes, cudaStream_t st) {
-  const long long n = (long long)B * k;
+int launch_pre_accept(const SelectArgs& a, cudaStream_t st) {
+  const long long n = (long long)a.ep_rows * a.k;
   if (n == 0) return TETRIS_OK;
-  pre_accept_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, q, d, u_acc, len, B, k, V, acc_bytes);
+  pre_accept_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
   return abi::launch_check();
 }
 

@@ -467,12 +467,32 @@ extern "C" int tetris_verify_stochastic_f32(const float* p, const float* q, cons
   return abi::launch_check();
 }
 
-extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
-                                        int32_t row0, int32_t B, const float* p, const float* q, const int32_t* d,
-                                        const double* u_acc, int32_t u_packed, const int32_t* cap, int32_t V,
-                                        int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* offsets,
-                                        int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
-                                        tetris_stream_t stream) {
+// The step's inputs: fp32 probabilities p / q, or bf16 logits zp / zq with per-row lse (the logits contract).
+struct ProbIn {
+  const float* p;
+  const float* q;
+  const uint16_t* zp;
+  const uint16_t* zq;
+  const float* lse_p;
+  const float* lse_q;
+  bool logits() const { return zp != nullptr; }
+  const void* pbase() const { return logits() ? (const void*)zp : (const void*)p; }
+  const void* qbase() const { return logits() ? (const void*)zq : (const void*)q; }
+};
+
+static bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
+
+// the TMA sampler's requirements: whole 16-byte lanes per row (V % 8 == 0) and 16-byte aligned row bases
+static bool persist_eligible_in(const ProbIn& in, int V) {
+  if (!in.logits()) return persist_eligible(in.p, in.q, V);
+  return V % 8 == 0 && n_chunks(V) <= 64 && aligned16(in.zp) && (!in.zq || aligned16(in.zq)) && in.lse_p;
+}
+
+static int select_accept_impl(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                              int32_t row0, int32_t B, const ProbIn& in, const int32_t* d, const double* u_acc,
+                              int32_t u_packed, const int32_t* cap, int32_t V, int32_t* windows, int32_t* win_offsets,
+                              int32_t* accepted, int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status,
+                              void* ws, size_t ws_bytes, tetris_stream_t stream) {
   int rc = check_shape(B, k, V);
   if (rc) return rc;
   if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
@@ -480,7 +500,8 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
   if (B_sel < B || B_sel > TETRIS_MAX_SELECT_ROWS || row0 < 0 || row0 + B > B_sel)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "local rows [%d, %d) outside the %d selected rows", row0, row0 + B, B_sel);
   if (u_packed && B != B_sel) return abi::fail(TETRIS_INVALID_ARGUMENT, "packed uniforms need the whole batch");
-  if ((k > 0 && (!conf || !d || !u_acc || !q)) || !p || !windows || !win_offsets || !accepted || !offsets || !tokens)
+  if ((k > 0 && (!conf || !d || !u_acc || !in.qbase() || (in.logits() && !in.lse_q))) || !in.pbase() ||
+      (in.logits() && !in.lse_p) || !windows || !win_offsets || !accepted || !offsets || !tokens)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   SelectArgs sa = {};
@@ -495,8 +516,12 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
   sa.status = status;
   sa.ep_row0 = row0;
   sa.ep_rows = B;
-  sa.p = p;
-  sa.q = q;
+  sa.p = in.p;
+  sa.q = in.q;
+  sa.zp = in.zp;
+  sa.zq = in.zq;
+  sa.lse_p = in.lse_p;
+  sa.lse_q = in.lse_q;
   sa.d = d;
   sa.u_acc = u_acc;
   sa.u_packed = u_packed;
@@ -517,24 +542,52 @@ extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, 
   return launch_select(sa, (cudaStream_t)stream);
 }
 
+extern "C" int tetris_select_accept_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                        int32_t row0, int32_t B, const float* p, const float* q, const int32_t* d,
+                                        const double* u_acc, int32_t u_packed, const int32_t* cap, int32_t V,
+                                        int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* offsets,
+                                        int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                        tetris_stream_t stream) {
+  const ProbIn in = {p, q, nullptr, nullptr, nullptr, nullptr};
+  return select_accept_impl(conf, len, B_sel, k, C, row0, B, in, d, u_acc, u_packed, cap, V, windows, win_offsets,
+                            accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
+}
+
+extern "C" int tetris_select_accept_bf16(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                         int32_t row0, int32_t B, const uint16_t* zp, const float* lse_p,
+                                         const uint16_t* zq, const float* lse_q, const int32_t* d, const double* u_acc,
+                                         int32_t u_packed, const int32_t* cap, int32_t V, int32_t* windows,
+                                         int32_t* win_offsets, int32_t* accepted, int32_t* offsets, int32_t* tokens,
+                                         int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                         tetris_stream_t stream) {
+  const ProbIn in = {nullptr, nullptr, zp, zq, lse_p, lse_q};
+  return select_accept_impl(conf, len, B_sel, k, C, row0, B, in, d, u_acc, u_packed, cap, V, windows, win_offsets,
+                            accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
+}
+
 constexpr long long kSpecMinChunks = 4096;  // see tetris_step_stochastic_f32
 
-static int resample_impl(const float* p, const float* q, const double* u_res, const double* u_acc_spec,
-                         const int32_t* len_spec, int B, int k, int V, const int32_t* d, const int32_t* accepted,
-                         const int32_t* offsets, int32_t* out_tok, double* mass_out, int32_t* tokens, uint32_t* status,
-                         void* ws, size_t ws_bytes, cudaStream_t st) {
+static int resample_impl(const ProbIn& in, const double* u_res, const double* u_acc_spec, const int32_t* len_spec,
+                         int B, int k, int V, const int32_t* d, const int32_t* accepted, const int32_t* offsets,
+                         int32_t* out_tok, double* mass_out, int32_t* tokens, uint32_t* status, void* ws,
+                         size_t ws_bytes, cudaStream_t st) {
   int rc = check_shape(B, k, V);
   if (rc) return rc;
   if (B == 0) return TETRIS_OK;
-  if (!p || (k > 0 && !q) || !u_res || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (!in.pbase() || (k > 0 && !in.qbase()) || !u_res || !out_tok)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
-  if (!persist_eligible(p, q, V))
-    return abi::fail(TETRIS_INVALID_ARGUMENT, "the streaming sampler needs V %% 8 == 0 and 16-byte aligned p/q");
+  if (!persist_eligible_in(in, V))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "the streaming sampler needs V %% 8 == 0 and 16-byte aligned rows");
   long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   StreamArgs a = {};
-  a.p = p;
-  a.q = q;
+  a.p = in.p;
+  a.q = in.q;
+  a.zp = in.zp;
+  a.zq = in.zq;
+  a.lse_p = in.lse_p;
+  a.lse_q = in.lse_q;
   a.V = V;
   a.nch = n_chunks(V);
   a.R = B;
@@ -577,7 +630,8 @@ extern "C" int tetris_resample_f32(const float* p, const float* q, const double*
                                    const int32_t* d, const int32_t* accepted, const int32_t* offsets, int32_t* out_tok,
                                    double* mass_out, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
                                    tetris_stream_t stream) {
-  return resample_impl(p, q, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status,
+  const ProbIn in = {p, q, nullptr, nullptr, nullptr, nullptr};
+  return resample_impl(in, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status,
                        ws, ws_bytes, (cudaStream_t)stream);
 }
 
@@ -587,9 +641,30 @@ extern "C" int tetris_resample_spec_f32(const float* p, const float* q, const do
                                         double* mass_out, int32_t* tokens, uint32_t* status, void* ws,
                                         size_t ws_bytes, tetris_stream_t stream) {
   if (k > 0 && (!u_acc || !d)) return abi::fail(TETRIS_INVALID_ARGUMENT, "the speculative sampler needs u_acc and d");
-  return resample_impl(p, q, u_res, u_acc, len, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status, ws,
+  const ProbIn in = {p, q, nullptr, nullptr, nullptr, nullptr};
+  return resample_impl(in, u_res, u_acc, len, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status, ws,
                        ws_bytes, (cudaStream_t)stream);
 }
+
+extern "C" int tetris_resample_bf16(const uint16_t* zp, const float* lse_p, const uint16_t* zq, const float* lse_q,
+                                    const double* u_res, const double* u_acc, const int32_t* len, int32_t B,
+                                    int32_t k, int32_t V, const int32_t* d, const int32_t* accepted,
+                                    const int32_t* offsets, int32_t* out_tok, double* mass_out, int32_t* tokens,
+                                    uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
+  if (u_acc && k > 0 && !d) return abi::fail(TETRIS_INVALID_ARGUMENT, "the speculative sampler needs d");
+  if (u_acc && B > spec_max_requests())
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "speculative sampler: B=%d > %d", B, spec_max_requests());
+  const ProbIn in = {nullptr, nullptr, zp, zq, lse_p, lse_q};
+  return resample_impl(in, u_res, u_acc, len, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens, status, ws,
+                       ws_bytes, (cudaStream_t)stream);
+}
+
+static int step_stochastic_impl(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                int32_t row0, int32_t B, const ProbIn& in, const int32_t* d, const double* u_acc,
+                                int32_t u_packed, const double* u_res, const int32_t* cap, int32_t V, int32_t* windows,
+                                int32_t* win_offsets, int32_t* accepted, int32_t* out_tok, double* mass_out,
+                                int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
+                                size_t ws_bytes, tetris_stream_t stream);
 
 extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k,
                                           int64_t C, int32_t row0, int32_t B, const float* p, const float* q,
@@ -598,18 +673,44 @@ extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len
                                           int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
                                           double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4,
                                           uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
-  if (!persist_eligible(p, q, V))
-    return abi::fail(TETRIS_INVALID_ARGUMENT, "fused step needs V %% 8 == 0 and 16-byte aligned p/q");
+  const ProbIn in = {p, q, nullptr, nullptr, nullptr, nullptr};
+  return step_stochastic_impl(conf, len, B_sel, k, C, row0, B, in, d, u_acc, u_packed, u_res, cap, V, windows,
+                              win_offsets, accepted, out_tok, mass_out, offsets, tokens, stats4, status, ws, ws_bytes,
+                              stream);
+}
+
+static int step_stochastic_impl(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                int32_t row0, int32_t B, const ProbIn& in, const int32_t* d, const double* u_acc,
+                                int32_t u_packed, const double* u_res, const int32_t* cap, int32_t V, int32_t* windows,
+                                int32_t* win_offsets, int32_t* accepted, int32_t* out_tok, double* mass_out,
+                                int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
+                                size_t ws_bytes, tetris_stream_t stream) {
+  if (!persist_eligible_in(in, V))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "fused step needs V %% 8 == 0 and 16-byte aligned rows");
   if (!u_res || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
-  int rc = tetris_select_accept_f32(conf, len, B_sel, k, C, row0, B, p, q, d, u_acc, u_packed, cap, V, windows,
-                                    win_offsets, accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
+  int rc = select_accept_impl(conf, len, B_sel, k, C, row0, B, in, d, u_acc, u_packed, cap, V, windows, win_offsets,
+                              accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
   if (rc) return rc;
   // dense uniforms: the sampler streams the selection-independent rows while the selector runs — when there is
   // enough to stream for the early start to pay for its set-up (measured: cfg3, 16384 chunks, 158.8 -> 154.3 us per
   // step; cfg2, 1024 chunks, 30.3 -> 32.8 us)
   const bool spec = !u_packed && B <= spec_max_requests() && (long long)B * n_chunks(V) >= kSpecMinChunks;
-  return resample_impl(p, q, u_res, spec ? u_acc : nullptr, spec && len ? len + row0 : nullptr, B, k, V, d, accepted,
+  return resample_impl(in, u_res, spec ? u_acc : nullptr, spec && len ? len + row0 : nullptr, B, k, V, d, accepted,
                        offsets, out_tok, mass_out, tokens, status, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int tetris_step_stochastic_bf16(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C,
+                                           int32_t row0, int32_t B, const uint16_t* zp, const float* lse_p,
+                                           const uint16_t* zq, const float* lse_q, const int32_t* d,
+                                           const double* u_acc, int32_t u_packed, const double* u_res,
+                                           const int32_t* cap, int32_t V, int32_t* windows, int32_t* win_offsets,
+                                           int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
+                                           int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
+                                           size_t ws_bytes, tetris_stream_t stream) {
+  const ProbIn in = {nullptr, nullptr, zp, zq, lse_p, lse_q};
+  return step_stochastic_impl(conf, len, B_sel, k, C, row0, B, in, d, u_acc, u_packed, u_res, cap, V, windows,
+                              win_offsets, accepted, out_tok, mass_out, offsets, tokens, stats4, status, ws, ws_bytes,
+                              stream);
 }
 
 static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* windows, const int32_t* cap, int B,
@@ -789,7 +890,8 @@ extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32
   if ((rc = copy_h2d_batched(dsts, srcs, sizes, st))) return rc;
   if ((e = cudaMemcpyAsync(rowinfo, rowinfo_host, ri_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return abi::cuda_fail(e);
-  return resample_impl(staging, staging, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out,
+  const ProbIn staged = {staging, staging, nullptr, nullptr, nullptr, nullptr};
+  return resample_impl(staged, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out,
                        tokens, status, ws, ws_bytes, st);
 }
 
@@ -983,4 +1085,24 @@ extern "C" int tetris_step_greedy_staged_f32(const double* conf, const int32_t* 
   if ((rc = copy_h2d_batched(dsts, srcs, sizes, st))) return rc;
   return verify_greedy_impl(p_dev, d, windows, cap, B, k, V, accepted, out_tok, offsets, tokens, status, ws, ws_bytes,
                             st);
+}
+
+// ---- the logits contract materialised: prob(z, lse) for R rows of V bf16 logits (tests, adapters) ---------------
+__global__ void probs_from_logits_kernel(const uint16_t* __restrict__ z, const float* __restrict__ lse, int64_t R,
+                                         int V, float* __restrict__ out) {
+  const int64_t n = R * (int64_t)V;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = tetris::prob_from_logit(tetris::bf16_bits_to_f32(z[e]), lse[e / V]);
+}
+
+extern "C" int tetris_probs_from_logits_bf16(const uint16_t* z, const float* lse, int64_t R, int32_t V, float* out,
+                                             tetris_stream_t stream) {
+  using namespace tetris;
+  if (R < 0 || V < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "bad shape R=%lld V=%d", (long long)R, V);
+  if (R == 0 || V == 0) return TETRIS_OK;
+  if (!z || !lse || !out) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  const int64_t n = R * (int64_t)V;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  probs_from_logits_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(z, lse, R, V, out);
+  return abi::launch_check();
 }

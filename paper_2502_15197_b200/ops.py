@@ -345,6 +345,22 @@ def residual(p_draft: torch.Tensor, p_target: torch.Tensor, status: Optional[tor
     return out, mass, st
 
 
+def probs_from_logits(z: torch.Tensor, lse: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The logits contract materialised (include/tetris_b200.h): prob(z, lse) for bf16 logits z [..., V] and their
+    row log-sum-exp lse [...] f32 -> fp32 [..., V]."""
+    if not isinstance(z, torch.Tensor) or not z.is_cuda or z.dtype != torch.bfloat16 or not z.is_contiguous():
+        raise ValueError("z must be a contiguous bfloat16 CUDA tensor")
+    lse = _need_cuda("lse", lse, _F32)
+    V = z.shape[-1]
+    R = z.numel() // max(V, 1)
+    if lse.numel() != R:
+        raise ValueError(f"lse must hold one value per row ({R}), got {lse.numel()}")
+    if out is None:
+        out = torch.empty(z.shape, dtype=_F32, device=z.device)
+    N.call("tetris_probs_from_logits_bf16", z.data_ptr(), lse.data_ptr(), R, V, out.data_ptr(), _stream_handle())
+    return out
+
+
 # ---------------------------------------------------------------------------------------------------------------
 # stage (4): compaction
 # ---------------------------------------------------------------------------------------------------------------
@@ -520,6 +536,52 @@ class TetrisStep:
             self.out_tok.data_ptr(), self.offsets.data_ptr(), self.tokens.data_ptr(), self.stats.data_ptr(),
             self.status.data_ptr(), ws.ptr, ws.nbytes, s)
         self._check(rc)
+
+    def run_logits(self, conf, lengths, zp, lse_p, zq, lse_q, d, u_acc, u_res, cap=None, events=None) -> None:
+        """The stochastic step on LOGITS: zp [B, k+1, V] / zq [B, k, V] bf16 logits with their row
+        log-sum-exp lse_p [B, k+1] / lse_q [B, k] f32 (the LM head's softmax normaliser); every probability is the
+        logits contract's prob(z, lse) (include/tetris_b200.h), computed inside the kernels.  Results equal run() on
+        p = probs_from_logits(zp, lse_p), q = probs_from_logits(zq, lse_q); half the streamed bytes.  Same launches
+        as run() (select + accept, then the persistent sampler); events bracket [select | sampler | nothing]."""
+        if self.mode != "stochastic" or self.policy != "tetris":
+            raise ValueError("run_logits is the stochastic TETRIS step")
+        B, k, V = self.B, self.k, self.V
+        for name, t, shape in (("zp", zp, (B, k + 1, V)), ("zq", zq, (B, k, V))):
+            if t.dtype != torch.bfloat16 or tuple(t.shape) != shape or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous bfloat16 tensor of shape {shape}")
+        for name, t, shape in (("lse_p", lse_p, (B, k + 1)), ("lse_q", lse_q, (B, k))):
+            if t.dtype != _F32 or tuple(t.shape) != shape or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float32 tensor of shape {shape}")
+        if V % 8 or zp.data_ptr() % 16 or zq.data_ptr() % 16:
+            raise ValueError("the logits step needs V % 8 == 0 and 16-byte aligned logits")
+        lib, ws, s = self._lib, self.ws, torch.cuda.current_stream().cuda_stream
+        if events is not None:
+            events[0].record()
+        if self.world > 1 and self.group is not None:
+            from .dist import gather_scores
+
+            gather_scores(self.conf_all, self.len_all, conf, lengths, self.group)
+            sel_conf, sel_len = self.conf_all, self.len_all
+        else:
+            sel_conf, sel_len = conf, lengths
+        self._check(lib.tetris_select_accept_bf16(
+            sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, self.rank * B, B, zp.data_ptr(),
+            lse_p.data_ptr(), zq.data_ptr(), lse_q.data_ptr(), d.data_ptr(), u_acc.data_ptr(),
+            int(self.u_layout == "packed"), _ptr(cap), V, self.windows_all.data_ptr(), self.win_offsets.data_ptr(),
+            self.accepted.data_ptr(), self.offsets.data_ptr(), self.tokens.data_ptr(), self.stats.data_ptr(),
+            self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+        if events is not None:
+            events[1].record()
+        spec = self.uses_spec
+        len_local = None if (sel_len is None or not spec) else sel_len[self.rank * B:(self.rank + 1) * B]
+        self._check(lib.tetris_resample_bf16(
+            zp.data_ptr(), lse_p.data_ptr(), zq.data_ptr(), lse_q.data_ptr(), u_res.data_ptr(),
+            u_acc.data_ptr() if spec else None, _ptr(len_local), B, k, V, d.data_ptr(), self.accepted.data_ptr(),
+            self.offsets.data_ptr(), self.out_tok.data_ptr(), self.mass.data_ptr(), self.tokens.data_ptr(),
+            self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+        if events is not None:
+            events[2].record()
+            events[3].record()
 
     def _run_fixed(self, lengths, p, q, d, u_acc, u_res, cap, events, window) -> None:
         """Baseline step (fixed window / sd / dsd common window, clamped to each depth): windows kernel, then the same

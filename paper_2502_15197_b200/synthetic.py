@@ -118,3 +118,79 @@ def selection_instance(B: int, k: int, kind: str, seed: int = 0, device="cuda"):
     else:
         lengths = torch.full((B,), k, dtype=torch.int32)
     return a.to(device), lengths.to(device)
+
+
+@dataclass
+class LogitBatch:
+    """The same shapes as Batch with the rows as bf16 LOGITS plus their fp32 row log-sum-exp (the logits contract of
+    include/tetris_b200.h): zp [B, k+1, V], zq [B, k, V] bf16; lse_p [B, k+1], lse_q [B, k] f32."""
+    B: int
+    k: int
+    V: int
+    zp: torch.Tensor
+    zq: torch.Tensor
+    lse_p: torch.Tensor
+    lse_q: torch.Tensor
+    d: torch.Tensor
+    conf: torch.Tensor
+    lengths: torch.Tensor
+    u_acc: torch.Tensor
+    u_res: torch.Tensor
+
+
+def make_logit_batch(B: int, k: int, V: int, *, seed: int = 0, device="cuda", ragged: bool = False,
+                     easy_frac: float = 0.5, sigma_easy: float = 0.35, sigma_hard: float = 2.0,
+                     block_bytes: int = 1 << 30) -> LogitBatch:
+    """Spiked draft logits / noisy target logits as in make_batch, stored as bf16; lse = logsumexp of the stored bf16
+    values (fp32); draft tokens d ~ softmax(zq); conf = exp(zq[d] - lse_q) in fp64 (the draft's confidence)."""
+    import math
+
+    dev = torch.device(device)
+    g = torch.Generator(device=dev)
+    g.manual_seed(int(seed))
+    lv = math.log(V)
+    spike_lo, spike_hi = lv - 2.0, lv + 3.0
+    zp = torch.empty(B, k + 1, V, dtype=torch.bfloat16, device=dev)
+    zq = torch.empty(B, k, V, dtype=torch.bfloat16, device=dev)
+    lse_p = torch.empty(B, k + 1, dtype=torch.float32, device=dev)
+    lse_q = torch.empty(B, k, dtype=torch.float32, device=dev)
+    d = torch.zeros(B, k, dtype=torch.int64, device=dev)
+    easy = torch.rand(B, generator=g, device=dev) < easy_frac
+    sigma = torch.where(easy, torch.full((B,), sigma_easy, device=dev), torch.full((B,), sigma_hard, device=dev))
+    blk = max(1, int(block_bytes // max(1, (k + 1) * V * 4 * 3)))
+
+    def spiked(n_rows):
+        z = torch.randn(n_rows, V, generator=g, device=dev, dtype=torch.float32)
+        mode = torch.randint(0, V, (n_rows,), generator=g, device=dev)
+        h = torch.rand(n_rows, generator=g, device=dev) * (spike_hi - spike_lo) + spike_lo
+        z[torch.arange(n_rows, device=dev), mode] += h
+        return z
+
+    for b0 in range(0, B, blk):
+        b1 = min(B, b0 + blk)
+        nb = b1 - b0
+        if k > 0:
+            z = spiked(nb * k).view(nb, k, V)
+            zq[b0:b1] = z.to(torch.bfloat16)
+            zt = z.mul_(0).add_(torch.randn(nb, k, V, generator=g, device=dev)).mul_(sigma[b0:b1].view(-1, 1, 1))
+            zt.add_(zq[b0:b1].float())
+            zp[b0:b1, :k] = zt.to(torch.bfloat16)
+            del z, zt
+            lse_q[b0:b1] = torch.logsumexp(zq[b0:b1].float(), dim=-1)
+            qprob = torch.softmax(zq[b0:b1].float(), dim=-1).view(-1, V)
+            d[b0:b1] = torch.multinomial(qprob, 1, generator=g).view(nb, k)
+            del qprob
+        zp[b0:b1, k:] = spiked(nb).view(nb, 1, V).to(torch.bfloat16)
+        lse_p[b0:b1] = torch.logsumexp(zp[b0:b1].float(), dim=-1)
+    if k > 0:
+        zd = zq.gather(2, d.unsqueeze(-1)).squeeze(-1).double()
+        conf = torch.exp(zd - lse_q.double()).clamp_(0.0, 1.0).contiguous()
+    else:
+        conf = torch.zeros(B, 0, dtype=torch.float64, device=dev)
+    if ragged and k > 0:
+        lengths = torch.randint(1, k + 1, (B,), generator=g, device=dev, dtype=torch.int32)
+    else:
+        lengths = torch.full((B,), k, dtype=torch.int32, device=dev)
+    u_acc = torch.rand(B, k, generator=g, device=dev, dtype=torch.float64)
+    u_res = torch.rand(B, generator=g, device=dev, dtype=torch.float64)
+    return LogitBatch(B, k, V, zp, zq, lse_p, lse_q, d.to(torch.int32).contiguous(), conf, lengths, u_acc, u_res)
