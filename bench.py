@@ -158,14 +158,17 @@ def _sum_over_ranks(x: float, group) -> float:
     return float(t.item())
 
 
-def _verify_bytes(cfg, windows, accepted):
-    """Algorithmic bytes of one stochastic verify launch: one fp32 vocabulary row per request
-    (bonus) or two (residual after a rejection), plus per selected position the two gathered probabilities (8 B),
-    the draft token (4 B) and its uniform (8 B), plus per request window, u_res, accepted, token (24 B)."""
+def _verify_bytes(cfg, windows, accepted, logits=False):
+    """Algorithmic bytes of one stochastic verify launch: one vocabulary row per request
+    (bonus) or two (residual after a rejection) -- 4 B per fp32 probability, 2 B per bf16 logit (+ the two rows' lse,
+    8 B) -- plus per selected position the two gathered probabilities (8 B; logits: 4 B + their lse 8 B), the draft
+    token (4 B) and its uniform (8 B), plus per request window, u_res, accepted, token (24 B)."""
     V = cfg["V"]
     if cfg["mode"] == "greedy":
         return int((windows.sum() + len(windows)) * V * 4 + 20 * windows.sum() + 24 * len(windows))
     rej = (accepted < windows).sum()
+    if logits:
+        return int((len(windows) + rej) * V * 2 + 8 * len(windows) + 24 * windows.sum() + 24 * len(windows))
     return int(len(windows) * V * 4 + rej * V * 4 + 20 * windows.sum() + 24 * len(windows))
 
 
@@ -184,9 +187,12 @@ def run_tetris(args):
     import torch
 
     from paper_2502_15197_b200 import ops
-    from paper_2502_15197_b200.synthetic import make_batch
+    from paper_2502_15197_b200.synthetic import make_batch, make_logit_batch
 
     world, rank, local, group = _setup_dist(args.gpus)
+    logits = args.input == "logits"
+    if logits and (cfg_mode := CONFIGS[args.config]["mode"]) != "stochastic":
+        raise SystemExit(f"--input logits is the stochastic step ({args.config} is {cfg_mode})")
     cfg = dict(CONFIGS[args.config])
     sim_w = args.simulate_world if world == 1 else 0
     wsel = sim_w or world  # ranks whose requests the selection covers
@@ -201,7 +207,7 @@ def run_tetris(args):
     clocks = ClockSampler(local)
     clocks.start()  # early, so nvidia-smi is sampling by the time the timed region starts
     # rotate enough input sets that consecutive steps never find their inputs in L2 (126 MB on B200)
-    set_bytes = B_local * ((k + 1) + k) * V * 4
+    set_bytes = B_local * ((k + 1) + k) * V * (2 if logits else 4)
     nsets = max(args.sets, -(-2 * 126 * 2**20 // set_bytes))
     free_b, _ = torch.cuda.mem_get_info(dev)
     if nsets * set_bytes > 0.9 * free_b:
@@ -209,8 +215,12 @@ def run_tetris(args):
     if set_bytes > 0.9 * free_b:
         raise SystemExit(f"{args.config}: {set_bytes / 1e9:.1f} GB of p/q per rank does not fit this GPU "
                          f"({free_b / 1e9:.1f} GB free); shard it over more GPUs (--gpus N under torchrun)")
-    sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
-            for s in range(nsets)]
+    if logits:
+        sets = [make_logit_batch(B_local, k, V, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
+                for s in range(nsets)]
+    else:
+        sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
+                for s in range(nsets)]
     step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None,
                           policy=args.policy, shard=(sim_w, 0) if sim_w else None)
     if sim_w:
@@ -225,7 +235,10 @@ def run_tetris(args):
 
     def run(i, events=None):
         bt = sets[i % nsets]
-        if sim_w:
+        if logits:
+            conf, ln = (bt.conf_all, bt.len_all) if sim_w else (bt.conf, bt.lengths)
+            step.run_logits(conf, ln, bt.zp, bt.lse_p, bt.zq, bt.lse_q, bt.d, bt.u_acc, bt.u_res, events=events)
+        elif sim_w:
             step.run(bt.conf_all, bt.len_all, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, events=events)
         else:
             step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, events=events)
@@ -239,7 +252,7 @@ def run_tetris(args):
         tokens_per_set.append(int(step.offsets[-1].item()))
         w = step.windows.cpu().numpy().astype(np.int64)
         a = step.accepted.cpu().numpy().astype(np.int64)
-        bytes_per_set.append(_verify_bytes(cfg, w, a))
+        bytes_per_set.append(_verify_bytes(cfg, w, a, logits))
 
     # CUDA graphs (single GPU; the NCCL exchange of N>1 stays eager): one captured step per input set, plus one graph
     # of M consecutive steps over the rotating sets (M a multiple of the set count, >= --graph-steps) so that the
@@ -336,10 +349,12 @@ def run_tetris(args):
     assert int(step.offsets[-1].item()) == tokens_per_set[(args.steps - 1) % nsets]
 
     e2e = None
-    if not args.no_e2e and not sim_w:
+    if not args.no_e2e and not sim_w and logits and world == 1:
+        e2e = _e2e_logits(args, cfg, sets[0], B_local, k, V, C, dev)
+    elif not args.no_e2e and not sim_w and not logits:
         e2e = _e2e(args, cfg, step, sets[0], B_local, k, V, C, mode, group, world, dev)
     cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline and not sim_w:
+    if world == 1 and rank == 0 and not args.no_cpu_baseline and not sim_w and not logits:
         cpu = _cpu_baseline(cfg, sets[0], step, B_local, C, args)
 
     if rank == 0:
@@ -354,10 +369,12 @@ def run_tetris(args):
             "higher_is_better": True,
             "scaling": "strong" if cfg.get("strong") else "weak",
             "vs_baseline": None,
-            "dtype": "f32 probabilities, f64 accumulation",
+            "dtype": "bf16 logits (+ fp32 row lse), f32 probabilities computed in-kernel, f64 accumulation" if logits
+                     else "f32 probabilities, f64 accumulation",
             "data": "synthetic (seeded spiked-softmax draft/target distributions, paper_2502_15197_b200/synthetic.py)",
             "config": {"workload": f"{args.config}: B={B_local * world} k={k} C={C} V={V} {mode}",
-                       "B_per_gpu": B_local, "k": k, "C": C, "V": V, "verify": mode, "input_sets": nsets,
+                       "B_per_gpu": B_local, "k": k, "C": C, "V": V, "verify": mode, "input": args.input,
+                       "input_sets": nsets,
                        "l2": "rotated input sets larger than L2 together (%.3f GB per set, %d sets)" % (
                            set_bytes / 1e9, nsets),
                        "parallelism": f"request-sharded dp{world}" + (" + NCCL all-gather select" if world > 1 else ""),
@@ -370,7 +387,10 @@ def run_tetris(args):
             # same stages with events between them (which keeps the sampler from overlapping the selector)
             "select_verify_latency_us": 1e3 * statistics.median(step_lat_ms),
             "tokens_per_step": total_tokens / args.steps,
-            "roofline": {"bound": "hbm", "kernel": ("persist_stream_kernel<spec> (tetris_resample_spec_f32: its own "
+            "roofline": {"bound": "hbm", "kernel": ("persist_stream_kernel<spec, bf16> (tetris_resample_bf16: the "
+                         "logits form, prob(z, lse) computed per streamed element; CUDA events around the launch in an "
+                         "eager pass)" if logits else
+                         "persist_stream_kernel<spec> (tetris_resample_spec_f32: its own "
                          "phase-A set, streaming, per-request descents in one launch; CUDA events around the launch in "
                          "an eager pass, where the events keep it from overlapping the selector as it does in the "
                          "step)" if step.uses_spec else "persist_stream_kernel (tetris_resample_f32: streaming + per-"
@@ -382,7 +402,7 @@ def run_tetris(args):
                          "alg_bytes_per_launch": alg_bytes / args.steps,
                          "step_achieved": alg_bytes / (max_ms / 1e3) / 1e9,
                          "step_frac": alg_bytes / (max_ms / 1e3) / 1e9 / peak,
-                         "traffic": _load_traffic(args.config)},
+                         "traffic": _load_traffic(args.config + ("_logits" if logits else ""))},
             "clocks": clk,
             "gpu_launches": step.launches_per_step * args.steps,
             "e2e": e2e,
@@ -440,6 +460,43 @@ def _e2e(args, cfg, step_dev, bt, B, k, V, C, mode, group, world, dev):
                 "DMA copies of the needed p/q rows from pinned host memory after the selection (%d B; the selector's "
                 "accept test reads its scalars through the mapping)" % zero_copy if hs.transfer == "staged" else
                 "zero-copy kernel reads of the needed p/q rows from pinned host memory (%d B)" % zero_copy)}
+
+
+def _e2e_logits(args, cfg, lb, B, k, V, C, dev):
+    """The logits form through the host-buffer API (ops.HostLogitStep): bf16 logits + lse in pinned host memory, the
+    needed rows staged by DMA after the selection, results copied back, every step."""
+    import torch
+
+    from paper_2502_15197_b200 import ops
+
+    try:
+        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        host = [pin(t) for t in (lb.zp, lb.lse_p, lb.zq, lb.lse_q)]
+        small = [pin(t) for t in (lb.conf, lb.lengths, lb.d, lb.u_acc, lb.u_res)]
+    except RuntimeError as e:
+        return {"value": None, "unit": "tokens/s", "error": f"pinned host allocation failed: {e}"[:200]}
+    hs = ops.HostLogitStep(B, k, V, C, *host, device=dev)
+    steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        hs.run(*small)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        hs.run(*small)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    toks = int(hs.offsets_host[-1]) * steps
+    w = hs.step.windows.cpu().numpy().astype("int64")
+    a = hs.accepted_host.numpy().astype("int64")
+    rows = int(len(w) + (a < w).sum())
+    staged = rows * V * 2 + rows * 4
+    return {"value": toks / (ms / 1e3), "unit": "tokens/s", "steps": steps, "ms_per_step": ms / steps,
+            "h2d_bytes_per_step": hs.h2d_bytes() + staged, "d2h_bytes_per_step": hs.d2h_bytes(),
+            "h2d_mode": "explicit copies of conf/lengths/draft tokens/uniforms (%d B) + DMA copies of the needed bf16 "
+                        "logit rows and their lse after the selection (%d B)" % (hs.h2d_bytes(), staged)}
 
 
 def _cpu_baseline(cfg, bt, step, B, C, args):
@@ -717,6 +774,8 @@ def main():
     ap.add_argument("--simulate-world", type=int, default=0,
                     help="on 1 GPU: time rank 0's share of a step sharded over this many ranks (the other ranks' "
                          "gathered scores are this rank's rows reshuffled; no NCCL exchange in the timed region)")
+    ap.add_argument("--input", default="probs", choices=["probs", "logits"],
+                    help="logits: bf16 logits + row lse instead of fp32 probabilities (the logits contract)")
     ap.add_argument("--policy", default="tetris", choices=["tetris", "fixed"],
                     help="fixed: the fixed-window baseline (window C/B per request) through the same kernels")
     args = ap.parse_args()

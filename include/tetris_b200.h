@@ -69,12 +69,15 @@ typedef struct CUstream_st* tetris_stream_t; /* == cudaStream_t */
  * Entry points taking bf16 logits z (raw uint16 bf16 bits) and a caller-supplied fp32 log-sum-exp per row define each
  * probability as the fp32 value prob(z, lse) below (every operation IEEE fp32 round-to-nearest-even, FMA fused), then
  * apply the fp32 contract above to it unchanged (accept test, residual / bonus weights, sampling):
- *   x = (float)z + (-lse);  x = min(max(x, TETRIS_EXP_LO), TETRIS_EXP_HI)     (NaN -> TETRIS_EXP_LO)
+ *   lo = bf16_round_up(lse + TETRIS_EXP_LO);  hi = bf16_round_down(lse + TETRIS_EXP_HI)   (per row; toward +-inf)
+ *   z' = min(max(z, lo), hi) on the bf16 values (maxNum / minNum: a NaN logit takes lo)
+ *   x = (float)z' + (-lse)                                    (so x lies in [TETRIS_EXP_LO, TETRIS_EXP_HI])
  *   t = fma(x, TETRIS_EXP_L2E, TETRIS_EXP_MAGIC);  j = t + (-TETRIS_EXP_MAGIC);  r = fma(j, -TETRIS_EXP_LN2, x)
  *   e = fma(fma(fma(fma(fma(C5, r, C4), r, C3), r, C2), r, C1), r, C0)
  *   bits(prob) = bits(t) * 2^23 + bits(e)   (uint32 arithmetic, i.e. e * 2^round(x * log2(e)))
- * Relative error against exp(x) <= 1e-6 for x in [-86, 88]; probabilities below exp(-86) read as ~exp(-86).  The CPU
- * oracle (oracle/tetris_oracle.c, oracle_probs_from_logits_bf16) computes the same bits with C fmaf(). */
+ * Relative error against exp(x) <= 1e-6; logits below lse - 86 read as ~exp(-86) (every probability is a positive
+ * normal float).  lse must be finite.  The CPU oracle (oracle/tetris_oracle.c, oracle_probs_from_logits_bf16)
+ * computes the same bits with C fmaf(). */
 #define TETRIS_EXP_LO (-86.0f)
 #define TETRIS_EXP_HI 88.0f
 #define TETRIS_EXP_L2E 0x1.715476p+0f
@@ -256,6 +259,19 @@ int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, in
                                       int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
                                       int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
                                       tetris_stream_t stream);
+
+/* tetris_step_stochastic_staged_f32 for HOST-resident LOGITS: zp_host / zq_host bf16 and lse_p_host / lse_q_host f32,
+ * all pinned and device-mapped; staging [2B][V] bf16 and lse_staging [2B] f32 on the device, lse_host_scratch [2B]
+ * f32 pinned.  Same results as tetris_step_stochastic_bf16 on device copies; half the host-link bytes of the fp32
+ * form. */
+int tetris_step_stochastic_staged_bf16(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
+                                       const uint16_t* zp_host, const float* lse_p_host, const uint16_t* zq_host,
+                                       const float* lse_q_host, const int32_t* d, const double* u_acc,
+                                       const double* u_res, const int32_t* cap, int32_t V, uint16_t* staging,
+                                       float* lse_staging, float* lse_host_scratch, int64_t* rowinfo_host,
+                                       int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                                       double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                       uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
 
 /* The greedy step for HOST-resident p ([B][k+1][V], pinned and device-mapped): the selection, then (host waits for it)
  * one DMA copy per request of its verified rows p[b][0 .. windows[b]] (contiguous in host memory) into the same

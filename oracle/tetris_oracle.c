@@ -454,14 +454,23 @@ void oracle_compact(const int32_t* accepted, const int32_t* out_tok, const int32
 }
 
 /* ---- the logits contract (tetris_b200.h): prob(z, lse) with C99 fmaf (correctly rounded), fp32 RN ------------ */
+typedef union {
+  uint32_t u;
+  float f;
+} fbits;
+
+static uint32_t bf16_round_up(uint32_t b) { return ((b & 0xffffu) && !(b >> 31)) ? (b >> 16) + 1u : b >> 16; }
+static uint32_t bf16_round_down(uint32_t b) { return ((b & 0xffffu) && (b >> 31)) ? (b >> 16) + 1u : b >> 16; }
+
 static float prob_from_logit(uint16_t z16, float lse) {
-  union {
-    uint32_t u;
-    float f;
-  } z, t, e, o;
+  fbits z, lo, hi, a, b, t, e, o;
+  a.f = lse + TETRIS_EXP_LO;
+  b.f = lse + TETRIS_EXP_HI;
+  lo.u = bf16_round_up(a.u) << 16;
+  hi.u = bf16_round_down(b.u) << 16;
   z.u = (uint32_t)z16 << 16;
-  float x = z.f + (-lse);
-  x = fminf(fmaxf(x, TETRIS_EXP_LO), TETRIS_EXP_HI);
+  float zc = fminf(fmaxf(z.f, lo.f), hi.f); /* maxNum / minNum: a NaN logit takes the lower bound */
+  const float x = zc + (-lse);
   t.f = fmaf(x, TETRIS_EXP_L2E, TETRIS_EXP_MAGIC);
   const float j = t.f + (-TETRIS_EXP_MAGIC);
   const float r = fmaf(j, -TETRIS_EXP_LN2, x);

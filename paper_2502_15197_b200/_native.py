@@ -91,6 +91,9 @@ _SIGNATURES = {
     "tetris_step_stochastic_staged_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
                   _p, _sz, _p]),
+    "tetris_step_stochastic_staged_bf16": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                  _p, _p, _p, _p, _p, _sz, _p]),
     "tetris_step_greedy_staged_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "tetris_step_greedy_f32": (

@@ -88,7 +88,7 @@ inline int device_sm_count() {
   return n;
 }
 
-enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP, WS_SPEC_SUMS, WS_END };
+enum Region { WS_KEYS, WS_COUNTERS, WS_GSEL, WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL, WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES, WS_ROWMAP, WS_SPEC_SUMS, WS_ROWLSE, WS_SPEC_LSE, WS_END };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -116,7 +116,7 @@ static_assert(kSlotWorkSpec == kSlotGridCount + 4, "persist_stream_kernel reads 
 
 inline size_t region_offset(int op, int B, int k, int V, Region which) {
   const size_t nch = (size_t)((V + TETRIS_CHUNK_ELEMS - 1) / TETRIS_CHUNK_ELEMS);
-  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  size_t sizes[WS_END] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   sizes[WS_COUNTERS] = kCounterSlots * 4;
   sizes[WS_GSEL] = kGselScratchBytes;  // shape-independent, right after the counters: a fixed offset in every layout
   if (op & TETRIS_OP_SELECT) {
@@ -135,9 +135,13 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
     sizes[WS_ROWMAP] = 256 + (size_t)B * (k + 1) * 4;  // greedy: [0] selected-row count, then row -> (b, j)
     // speculative sampler: the phase-A chunk sums then warp sums (B <= kSpecSlots)
     sizes[WS_SPEC_SUMS] = B <= (int)kSpecSlots ? (size_t)B * nch * 8 * (1 + TETRIS_CHUNK_WARPS) : 0;
+    // logits form: the lse of each request's two rows beside the row info, and of each phase-A list entry's rows
+    sizes[WS_ROWLSE] = (size_t)B * 8;
+    sizes[WS_SPEC_LSE] = B <= (int)kSpecSlots ? (size_t)B * 8 : 0;
   }
-  const Region order[WS_END] = {WS_COUNTERS, WS_GSEL,    WS_KEYS,    WS_CHUNK_SUMS, WS_WARP_SUMS, WS_ARG_VAL,
-                                WS_ARG_IDX,  WS_SCRATCH, WS_ROWINFO, WS_ACCBYTES,   WS_ROWMAP,    WS_SPEC_SUMS};
+  const Region order[WS_END] = {WS_COUNTERS, WS_GSEL,    WS_KEYS,    WS_CHUNK_SUMS, WS_WARP_SUMS,
+                                WS_ARG_VAL,  WS_ARG_IDX, WS_SCRATCH, WS_ROWINFO,    WS_ACCBYTES,
+                                WS_ROWMAP,   WS_SPEC_SUMS, WS_ROWLSE, WS_SPEC_LSE};
   size_t off = 0;
   for (int i = 0; i < WS_END; ++i) {
     if (order[i] == which) return off;

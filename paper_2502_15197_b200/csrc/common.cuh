@@ -116,10 +116,28 @@ __device__ __forceinline__ int seq_find(const double* v, int n, double& T) {
 // ---- logits -> probabilities (the logits contract, tetris_b200.h) ------------------------------------------------
 __device__ __forceinline__ float bf16_bits_to_f32(uint32_t z16) { return __uint_as_float(z16 << 16); }
 
-// Scalar prob(z, lse) (gathers: the accept test, the descent's recomputation)
-__device__ __forceinline__ float prob_from_logit(float z, float lse) {
-  float x = __fadd_rn(z, -lse);
-  x = fminf(fmaxf(x, TETRIS_EXP_LO), TETRIS_EXP_HI);
+// fp32 -> bf16 bits rounded toward +inf / -inf (integer ops only; finite inputs)
+__host__ __device__ __forceinline__ uint32_t bf16_round_up(uint32_t b) {
+  const uint32_t h = b >> 16;
+  return ((b & 0xffffu) && !(b >> 31)) ? h + 1u : h;
+}
+__host__ __device__ __forceinline__ uint32_t bf16_round_down(uint32_t b) {
+  const uint32_t h = b >> 16;
+  return ((b & 0xffffu) && (b >> 31)) ? h + 1u : h;
+}
+
+// The row's clamp bounds as bf16 bits: lo = up(lse - 86), hi = down(lse + 88), so that x = z' - lse lies in
+// [TETRIS_EXP_LO, TETRIS_EXP_HI] for z' = min(max(z, lo), hi)
+struct ExpBounds {
+  uint32_t lo, hi;
+};
+__device__ __forceinline__ ExpBounds exp_bounds(float lse) {
+  return ExpBounds{bf16_round_up(__float_as_uint(__fadd_rn(lse, TETRIS_EXP_LO))),
+                   bf16_round_down(__float_as_uint(__fadd_rn(lse, TETRIS_EXP_HI)))};
+}
+
+// x -> prob for an already clamped x (shared tail of the scalar and packed forms)
+__device__ __forceinline__ float exp_tail(float x) {
   const float t = __fmaf_rn(x, TETRIS_EXP_L2E, TETRIS_EXP_MAGIC);
   const float j = __fadd_rn(t, -TETRIS_EXP_MAGIC);
   const float r = __fmaf_rn(j, -TETRIS_EXP_LN2, x);
@@ -129,6 +147,15 @@ __device__ __forceinline__ float prob_from_logit(float z, float lse) {
   e = __fmaf_rn(e, r, TETRIS_EXP_C1);
   e = __fmaf_rn(e, r, TETRIS_EXP_C0);
   return __uint_as_float((__float_as_uint(t) << 23) + __float_as_uint(e));
+}
+
+// Scalar prob(z, lse) (gathers: the accept test, the descent's recomputation).  The clamp compares the bf16 values as
+// floats (exact): maxNum / minNum semantics like max.bf16x2 / min.bf16x2 (a NaN logit takes the lower bound).
+__device__ __forceinline__ float prob_from_logit(uint32_t z16, float lse) {
+  const ExpBounds bd = exp_bounds(lse);
+  float z = bf16_bits_to_f32(z16);
+  z = fminf(fmaxf(z, bf16_bits_to_f32(bd.lo)), bf16_bits_to_f32(bd.hi));
+  return exp_tail(__fadd_rn(z, -lse));
 }
 
 // Packed fp32x2 (FFMA2 / FADD2 on sm_100a): two elements per instruction on the FMA pipe; elementwise IEEE RN, so the
@@ -153,13 +180,22 @@ __device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
   return r;
 }
 
-// prob(z, lse) for the two bf16 logits packed in `w` (element 0 in the low half).  nlse2 = pk2(-lse, -lse).
-__device__ __forceinline__ void prob2_from_bf16(uint32_t w, f32x2 nlse2, float& p0, float& p1) {
-  float x0, x1;
-  upk2(add2(pk2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)), nlse2), x0, x1);
-  x0 = fminf(fmaxf(x0, TETRIS_EXP_LO), TETRIS_EXP_HI);
-  x1 = fminf(fmaxf(x1, TETRIS_EXP_LO), TETRIS_EXP_HI);
-  const f32x2 x = pk2(x0, x1);
+// Per-row constants of the packed form: the clamp bounds duplicated into both bf16 halves, and -lse in both lanes
+struct ExpRow {
+  uint32_t lo2, hi2;
+  f32x2 nlse2;
+};
+__device__ __forceinline__ ExpRow exp_row(float lse) {
+  const ExpBounds bd = exp_bounds(lse);
+  return ExpRow{bd.lo | (bd.lo << 16), bd.hi | (bd.hi << 16), pk2(-lse, -lse)};
+}
+
+// prob(z, lse) for the two bf16 logits packed in `w` (element 0 in the low half): the clamp is one max.bf16x2 and
+// one min.bf16x2 on the packed logits.
+__device__ __forceinline__ void prob2_from_bf16(uint32_t w, const ExpRow& row, float& p0, float& p1) {
+  asm("max.bf16x2 %0, %0, %1;" : "+r"(w) : "r"(row.lo2));
+  asm("min.bf16x2 %0, %0, %1;" : "+r"(w) : "r"(row.hi2));
+  const f32x2 x = add2(pk2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)), row.nlse2);
   const f32x2 t = fma2(x, pk2(TETRIS_EXP_L2E, TETRIS_EXP_L2E), pk2(TETRIS_EXP_MAGIC, TETRIS_EXP_MAGIC));
   const f32x2 j = add2(t, pk2(-TETRIS_EXP_MAGIC, -TETRIS_EXP_MAGIC));
   const f32x2 r = fma2(j, pk2(-TETRIS_EXP_LN2, -TETRIS_EXP_LN2), x);
@@ -176,24 +212,37 @@ __device__ __forceinline__ void prob2_from_bf16(uint32_t w, f32x2 nlse2, float& 
 }
 
 // 8 consecutive bf16 logits (one 16-byte word) -> 8 probabilities
-__device__ __forceinline__ void prob8_from_bf16(const uint4 raw, float lse, float (&v)[8]) {
-  const f32x2 nl = pk2(-lse, -lse);
-  prob2_from_bf16(raw.x, nl, v[0], v[1]);
-  prob2_from_bf16(raw.y, nl, v[2], v[3]);
-  prob2_from_bf16(raw.z, nl, v[4], v[5]);
-  prob2_from_bf16(raw.w, nl, v[6], v[7]);
+__device__ __forceinline__ void prob8_from_bf16(const uint4 raw, const ExpRow& row, float (&v)[8]) {
+  prob2_from_bf16(raw.x, row, v[0], v[1]);
+  prob2_from_bf16(raw.y, row, v[2], v[3]);
+  prob2_from_bf16(raw.z, row, v[4], v[5]);
+  prob2_from_bf16(raw.w, row, v[6], v[7]);
+}
+
+// Logits-form weights: every probability is a positive normal float (>= ~exp(-86)), so the residual weight
+// max(0, (double)p - (double)q) is (double)p - (double)min(p, q) (p <= q gives p - p = +0 exactly) and the bonus
+// weight is (double)p: the same values as w_res32 / w_plain32 without the compare-and-select.
+// Exact fp32 -> fp64 widening of a positive NORMAL float with integer ops (ALU pipe) instead of F2F.F64.F32, which
+// runs at a quarter rate on the MIO queue shared with the consumers' shared-memory loads: the exponent is rebiased
+// (+896 << 52) and the mantissa shifted into place.
+__device__ __forceinline__ double widen_pos_normal(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+}
+__device__ __forceinline__ double w_res_pos(float p, float q) {
+  return widen_pos_normal(p) - widen_pos_normal(fminf(p, q));
 }
 
 // The probability of token t in row `row` of the target (p) / draft (q) input, whichever form the kernel was given:
 // fp32 probabilities, or bf16 logits + per-row lse (A: SelectArgs / StreamArgs).
 template <typename A>
 __device__ __forceinline__ double gather_p(const A& a, int64_t row, int t) {
-  if (a.zp) return (double)prob_from_logit(bf16_bits_to_f32(a.zp[row * a.V + t]), a.lse_p[row]);
+  if (a.zp) return (double)prob_from_logit(a.zp[row * a.V + t], a.lse_p[row]);
   return (double)a.p[row * a.V + t];
 }
 template <typename A>
 __device__ __forceinline__ double gather_q(const A& a, int64_t row, int t) {
-  if (a.zq) return (double)prob_from_logit(bf16_bits_to_f32(a.zq[row * a.V + t]), a.lse_q[row]);
+  if (a.zq) return (double)prob_from_logit(a.zq[row * a.V + t], a.lse_q[row]);
   return (double)a.q[row * a.V + t];
 }
 

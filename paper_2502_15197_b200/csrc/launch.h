@@ -33,6 +33,7 @@ struct SelectArgs {
   const int32_t* cap;
   int32_t* accepted;
   long long* rowinfo;  // [B][2]: p row, q row (-1: bonus)
+  float* rowlse;       // logits form: [B][2] the lse of those rows (written beside rowinfo)
   int32_t* offsets;    // [B+1]
   uint8_t* acc_bytes;  // pre-accept verdicts [ep_rows][k] (nullptr: gather in the epilogue)
   int accept_ctas;     // > 0: CTAs after cluster 0 compute acc_bytes concurrently with the selection
@@ -58,6 +59,8 @@ struct StreamArgs {
   int V, nch, R;
   const long long* prow;     // p row of request b at prow[b * row_stride]
   const long long* qrow;     // q row (-1: plain / bonus row) at qrow[b * row_stride]; nullptr: all plain
+  const float* rowlse;       // logits form: [R][2] the lse of request b's p row / q row (beside the row info)
+  float* spec_lse;           // logits form, speculative variant: [R][2] the lse of phase-A list entry y's rows
   int row_stride;
   const double* u;           // [R]
   int32_t* out_idx;

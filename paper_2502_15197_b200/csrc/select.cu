@@ -490,6 +490,10 @@ __global__ void __launch_bounds__(REG ? kRegMaxThreads : kSelMaxThreads, 1) sele
       a.accepted[lr] = acc;
       a.rowinfo[2 * (int64_t)lr] = (long long)lr * (k + 1) + acc;              // residual row / bonus row of p
       a.rowinfo[2 * (int64_t)lr + 1] = acc < w ? (long long)lr * k + acc : -1;  // draft row (residual only)
+      if (a.rowlse) {  // logits form: the two rows' lse beside their indices (one load round for the producer)
+        a.rowlse[2 * (int64_t)lr] = a.lse_p[(int64_t)lr * (k + 1) + acc];
+        a.rowlse[2 * (int64_t)lr + 1] = acc < w ? a.lse_q[(int64_t)lr * k + acc] : 0.f;
+      }
       hi[r] = (uint8_t)acc;
     }
     set_status(a.status, vbad);

@@ -418,6 +418,10 @@ __global__ void __launch_bounds__(NT, 1) select1_kernel(const SelectArgs a) {
       a.accepted[lr] = acc;
       a.rowinfo[2 * (int64_t)lr] = (long long)lr * (k + 1) + acc;              // residual row / bonus row of p
       a.rowinfo[2 * (int64_t)lr + 1] = acc < w ? (long long)lr * k + acc : -1;  // draft row (residual only)
+      if (a.rowlse) {  // logits form: the two rows' lse beside their indices (one load round for the producer)
+        a.rowlse[2 * (int64_t)lr] = a.lse_p[(int64_t)lr * (k + 1) + acc];
+        a.rowlse[2 * (int64_t)lr + 1] = acc < w ? a.lse_q[(int64_t)lr * k + acc] : 0.f;
+      }
       int n = acc + 1;
       if (a.cap) n = min(n, max(a.cap[lr], 0));
       nr[i] = n;

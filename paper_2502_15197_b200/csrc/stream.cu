@@ -95,9 +95,19 @@ struct PersistShared {
 // A lane's 8 staged elements as fp32 probabilities: an fp32 stage (two 16-byte halves, swizzled), or 8 bf16 logits
 // (one 16-byte word; consecutive lanes read consecutive words, conflict-free) through the logits contract.
 template <bool BF>
-__device__ __forceinline__ void stage_lane(const uint8_t* row, int off, int lane, float lse, float (&v)[8]) {
+__device__ __forceinline__ void stage_lane(const uint8_t* row, int off, int lane, const ExpRow& er, float (&v)[8]) {
   if (BF) {
-    prob8_from_bf16(*reinterpret_cast<const uint4*>(row + (size_t)off * 2), lse, v);
+#ifdef TETRIS_EXP_FAKE  // A/B experiment only: the staged bf16 values as probabilities (no exp)
+    const uint4 raw = *reinterpret_cast<const uint4*>(row + (size_t)off * 2);
+    const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float((wv[i] << 16) & 0x7fffffffu);
+      v[2 * i + 1] = __uint_as_float(wv[i] & 0x7fff0000u);
+    }
+#else
+    prob8_from_bf16(*reinterpret_cast<const uint4*>(row + (size_t)off * 2), er, v);
+#endif
   } else {
     lds8_swz(reinterpret_cast<const float*>(row) + off, lane, v);
   }
@@ -107,19 +117,22 @@ __device__ __forceinline__ void stage_lane(const uint8_t* row, int off, int lane
 template <bool BF>
 __device__ __forceinline__ double consume_segment(const uint8_t* __restrict__ sp, const uint8_t* __restrict__ sq,
                                                   bool res, int64_t e0, int off0, int V, int lane, float lp, float lq) {
+#ifdef TETRIS_CONSUME_NOP  // A/B experiment only: the pipeline without the consumers' arithmetic
+  return 0.0;
+#endif
   const int off = off0 + lane * kLaneElems;
   double w[8];
   if (e0 + lane * kLaneElems < V) {
     float pv[8];
-    stage_lane<BF>(sp, off, lane, lp, pv);
+    stage_lane<BF>(sp, off, lane, BF ? exp_row(lp) : ExpRow{}, pv);
     if (res) {
       float qv[8];
-      stage_lane<BF>(sq, off, lane, lq, qv);
+      stage_lane<BF>(sq, off, lane, BF ? exp_row(lq) : ExpRow{}, qv);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = w_res32(pv[i], qv[i]);
+      for (int i = 0; i < 8; ++i) w[i] = BF ? w_res_pos(pv[i], qv[i]) : w_res32(pv[i], qv[i]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = w_plain32(pv[i]);
+      for (int i = 0; i < 8; ++i) w[i] = BF ? widen_pos_normal(pv[i]) : w_plain32(pv[i]);
     }
   } else {
 #pragma unroll
@@ -137,7 +150,7 @@ __device__ __forceinline__ void row_lane(const void* row, int64_t e, int V, floa
       asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
           : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
           : "l"(reinterpret_cast<const uint16_t*>(row) + e));
-      prob8_from_bf16(raw, lse, v);
+      prob8_from_bf16(raw, exp_row(lse), v);
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = 0.f;
@@ -277,15 +290,14 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
   }
 }
 
-// Producer helper: one item (request b, chunk c) of rows prow / qrow (qrow < 0: plain) into stage t.  The logits
-// form's row lse values are loaded before the wait for a free stage, so their latency hides behind it.
+// Producer helper: one item (request b, chunk c) of rows prow / qrow (qrow < 0: plain) into stage t; logits form: lp /
+// lq are the rows' lse (loaded by the caller with the row indices, one item ahead).
 template <bool BF>
 __device__ __forceinline__ void issue_item(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, int b,
-                                           int c, long long prow, long long qrow, int phase, uint64_t pol) {
+                                           int c, long long prow, long long qrow, int phase, uint64_t pol, float lp,
+                                           float lq) {
   constexpr int S = Elem<BF>::kStages;
   const bool res = qrow >= 0;
-  const float lp = BF ? __ldg(a.lse_p + prow) : 0.f;
-  const float lq = (BF && res) ? __ldg(a.lse_q + qrow) : 0.f;
   const int s = t % S;
   if (t >= S) mbar_wait(&sh.empty[s], (uint32_t)(((t / S) & 1) ^ 1u));
   const int n = min(kChunkElems, a.V - c * kChunkElems);
@@ -305,23 +317,66 @@ __device__ __forceinline__ void issue_item(const StreamArgs& a, PersistShared& s
 // Producer helper: stream the items (list[y], c), y < count, c < nch, taken one at a time from `work` in order with
 // two items of look-ahead on the counter and one on the row lookup — the plain producer's schedule over a list.
 // rows(b, prow, qrow) gives the rows of request b.  Returns the next stage index.
+// Deeper producer schedule for the logits form (its items are half as many bytes, so the claim / row-lookup round
+// trips must overlap more): C claims on the work counter and L row lookups in flight, kept in shift registers.
+// req(i) -> request of item i; rows(b, prow, qrow, lse_p, lse_q).  Returns the next stage index.
+template <bool BF, int L, int C, typename Req, typename Rows>
+__device__ int stream_deep(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, long long total,
+                           unsigned long long* work, int phase, uint64_t pol, Req req, Rows rows) {
+  constexpr int D = L + C;
+  long long ci[D], pr[D], qr[D];
+  float lp[D], lq[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    ci[d] = (long long)atomicAdd(work, 1ull);
+    pr[d] = 0;
+    qr[d] = -1;
+    lp[d] = lq[d] = 0.f;
+  }
+#pragma unroll
+  for (int d = 0; d < L; ++d)
+    if (ci[d] < total) rows(req(ci[d]), pr[d], qr[d], lp[d], lq[d]);
+  for (;;) {
+    const long long i = ci[0];  // one thread's claims increase: past the end, all later ones are too
+    if (i >= total) break;
+    const long long prow = pr[0], qrow = qr[0];
+    const float l0 = lp[0], l1 = lq[0];
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) {
+      ci[d] = ci[d + 1];
+      pr[d] = pr[d + 1];
+      qr[d] = qr[d + 1];
+      lp[d] = lp[d + 1];
+      lq[d] = lq[d + 1];
+    }
+    ci[D - 1] = (long long)atomicAdd(work, 1ull);
+    if (ci[L - 1] < total) rows(req(ci[L - 1]), pr[L - 1], qr[L - 1], lp[L - 1], lq[L - 1]);
+    issue_item<BF>(a, sh, stage_mem, t++, req(i), (int)(i % a.nch), prow, qrow, phase, pol, l0, l1);
+  }
+  return t;
+}
+
 template <bool BF, typename Rows>
 __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, const uint16_t* list,
                            int count, unsigned long long* work, int phase, uint64_t pol, Rows rows) {
   const int nch = a.nch;
   const long long total = (long long)count * nch;
+  if (BF) return stream_deep<BF, 3, 3>(a, sh, stage_mem, t, total, work, phase, pol,
+                                       [&](long long i) { return (int)list[i / nch]; }, rows);
   long long i_next = (long long)atomicAdd(work, 1ull);
   long long i_next2 = (long long)atomicAdd(work, 1ull);
   long long pn = 0, qn = -1;
-  if (i_next < total) rows((int)list[i_next / nch], pn, qn);
+  float lpn = 0.f, lqn = 0.f;
+  if (i_next < total) rows((int)list[i_next / nch], pn, qn, lpn, lqn);
   for (;;) {
     const long long i = i_next;
     const long long prow = pn, qrow = qn;
+    const float lp = lpn, lq = lqn;
     i_next = i_next2;
     if (i >= total) break;
     i_next2 = (long long)atomicAdd(work, 1ull);
-    if (i_next < total) rows((int)list[i_next / nch], pn, qn);
-    issue_item<BF>(a, sh, stage_mem, t++, (int)list[i / nch], (int)(i % nch), prow, qrow, phase, pol);
+    if (i_next < total) rows((int)list[i_next / nch], pn, qn, lpn, lqn);
+    issue_item<BF>(a, sh, stage_mem, t++, (int)list[i / nch], (int)(i % nch), prow, qrow, phase, pol, lp, lq);
   }
   return t;
 }
@@ -388,6 +443,10 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         atomicOr(a.spec_bitmap + (b >> 5), 1u << (b & 31));
         if (lane != own) {
           const int pos = atomicAdd(a.spec_ctl, 1);
+          if (BF) {  // the entry's row lse travel with it (published by the release below)
+            a.spec_lse[2 * pos] = a.lse_p[(int64_t)b * (k + 1)];
+            a.spec_lse[2 * pos + 1] = a.lse_q[(int64_t)b * k];
+          }
           asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.spec_list + pos), "r"(b + 1) : "memory");
         }
       }
@@ -421,11 +480,11 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           if (y >= R) return -1;
           for (;;) {
             int e, done;
-            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
             if (e) return e - 1;
             asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(done) : "l"(a.spec_ctl + 1) : "memory");
             if (done >= R) {
-              asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.spec_list + y) : "memory");
               return e ? e - 1 : -1;
             }
             __nanosleep(128);
@@ -434,24 +493,42 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         int t = 0;
         if (sx.own >= 0) {
           const int b = sx.own;
+          const float lp = BF ? __ldg(a.lse_p + (int64_t)b * (k + 1)) : 0.f;
+          const float lq = BF ? __ldg(a.lse_q + (int64_t)b * k) : 0.f;
           for (int cc = 0; cc < nch; ++cc) {
             if (t == 0) gstamp(a, 2);
-            issue_item<BF>(a, sh, stage_mem, t++, b, cc, (long long)b * (k + 1), (long long)b * k, 1, pol);
+            issue_item<BF>(a, sh, stage_mem, t++, b, cc, (long long)b * (k + 1), (long long)b * k, 1, pol, lp, lq);
           }
         }
+        // logits form: an entry's lse pair is published with it (spec_lse[2y..]); read beside the entry (the
+        // release/acquire of the entry orders them; an entry seen by the relaxed look-ahead load is re-read below)
+        auto entry_lse = [&](long long i, float& lp, float& lq) {
+          if (BF) {
+            const int y = (int)(i / nch);
+            lp = __ldcg(a.spec_lse + 2 * y);
+            lq = __ldcg(a.spec_lse + 2 * y + 1);
+          }
+        };
         long long i_cur = (long long)atomicAdd(work_a, 1ull);
         long long i_nxt = (long long)atomicAdd(work_a, 1ull);
         int b_cur = entry(i_cur);
+        float lp_cur = 0.f, lq_cur = 0.f;
+        if (b_cur >= 0) entry_lse(i_cur, lp_cur, lq_cur);
         while (b_cur >= 0) {
           const long long i_nxt2 = (long long)atomicAdd(work_a, 1ull);
           // the next item's entry: its load is in flight while this item waits for a free stage
           const int y_nxt = (int)(i_nxt / nch);
           int e_nxt = 0;
-          if (y_nxt < R) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e_nxt) : "l"(a.spec_list + y_nxt));
+          if (y_nxt < R) asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(e_nxt) : "l"(a.spec_list + y_nxt));
+          float lp_nxt = 0.f, lq_nxt = 0.f;
+          if (e_nxt) entry_lse(i_nxt, lp_nxt, lq_nxt);
           if (t == 0) gstamp(a, 2);
           issue_item<BF>(a, sh, stage_mem, t++, b_cur, (int)(i_cur % nch), (long long)b_cur * (k + 1),
-                         (long long)b_cur * k, 1, pol);
+                         (long long)b_cur * k, 1, pol, lp_cur, lq_cur);
           b_cur = e_nxt ? e_nxt - 1 : entry(i_nxt);
+          if (!e_nxt && b_cur >= 0) entry_lse(i_nxt, lp_nxt, lq_nxt);
+          lp_cur = lp_nxt;
+          lq_cur = lq_nxt;
           i_cur = i_nxt;
           i_nxt = i_nxt2;
         }
@@ -460,38 +537,60 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         asm volatile("griddepcontrol.wait;" ::: "memory");  // the selector's row info (no-op by now)
         gstamp(a, 1);
         t = stream_list<BF>(a, sh, stage_mem, t, sx.listB, sx.countB, work, 0, pol,
-                        [&](int b, long long& pr, long long& qr) {
-                          pr = a.prow[(int64_t)b * a.row_stride];
-                          qr = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
-                        });
+                            [&](int b, long long& pr, long long& qr, float& lp, float& lq) {
+                              pr = a.prow[(int64_t)b * a.row_stride];
+                              qr = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+                              if (BF) {
+                                lp = a.rowlse[2 * (int64_t)b];
+                                lq = a.rowlse[2 * (int64_t)b + 1];
+                              }
+                            });
         const int s = t % kStages;  // end of stream: a sentinel stage without data
         if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
         sh.meta[s] = StageMeta{-1, 0, 0, 0};
         mbar_arrive(&sh.full[s]);
         gstamp(a, 3);
       }
+    } else if (BF && lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      int t = stream_deep<BF, 3, 3>(a, sh, stage_mem, 0, total, work, 0, pol,
+                                    [&](long long i) { return (int)(i / nch); },
+                                    [&](int b, long long& pr, long long& qr, float& lp, float& lq) {
+                                      pr = a.prow[(int64_t)b * a.row_stride];
+                                      qr = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+                                      lp = a.rowlse[2 * (int64_t)b];
+                                      lq = a.rowlse[2 * (int64_t)b + 1];
+                                    });
+      const int s = t % kStages;  // end of stream: a sentinel stage without data
+      if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
+      sh.meta[s] = StageMeta{-1, 0, 0, 0};
+      mbar_arrive(&sh.full[s]);
+      gstamp(a, 3);
     } else if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       // two items of look-ahead on the counter and the row info, so neither round trip stalls the copies
       long long i_next = (long long)atomicAdd(work, 1ull);
       long long i_next2 = (long long)atomicAdd(work, 1ull);
       long long pn = 0, qn = -1;
-      if (i_next < total) {
-        const int bb = (int)(i_next / nch);
+      float lpn = 0.f, lqn = 0.f;
+      auto rows = [&](long long ii) {
+        const int bb = (int)(ii / nch);
         pn = a.prow[(int64_t)bb * a.row_stride];
         qn = a.qrow ? a.qrow[(int64_t)bb * a.row_stride] : -1;
-      }
+        if (BF) {
+          lpn = a.rowlse[2 * (int64_t)bb];
+          lqn = a.rowlse[2 * (int64_t)bb + 1];
+        }
+      };
+      if (i_next < total) rows(i_next);
       for (int t = 0;; ++t) {
         const long long i = i_next;
         const long long prow = pn, qrow = qn;
+        const float lp = lpn, lq = lqn;
         i_next = i_next2;
         if (i < total) {
           i_next2 = (long long)atomicAdd(work, 1ull);
-          if (i_next < total) {
-            const int bb = (int)(i_next / nch);
-            pn = a.prow[(int64_t)bb * a.row_stride];
-            qn = a.qrow ? a.qrow[(int64_t)bb * a.row_stride] : -1;
-          }
+          if (i_next < total) rows(i_next);
         }
         if (i >= total) {  // end of stream: a sentinel stage without data
           const int s = t % kStages;
@@ -502,7 +601,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           break;
         }
         if (t == 0) gstamp(a, 2);
-        issue_item<BF>(a, sh, stage_mem, t, (int)(i / nch), (int)(i % nch), prow, qrow, 0, pol);
+        issue_item<BF>(a, sh, stage_mem, t, (int)(i / nch), (int)(i % nch), prow, qrow, 0, pol, lp, lq);
       }
     }
     __syncwarp();
@@ -792,7 +891,8 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
                        (int)std::min<long long>((long long)a.R * a.nch, g_num_sms) > 32))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "speculative sampler: R=%d > %d or missing buffers", a.R, kSpecMaxR);
   const bool bf = a.zp != nullptr;
-  if (bf && (!a.lse_p || (a.qrow && (!a.zq || !a.lse_q)) || a.req_cnt == nullptr))
+  if (bf && (!a.lse_p || (a.qrow && (!a.zq || !a.lse_q)) || a.req_cnt == nullptr || !a.rowlse ||
+             (spec && !a.spec_lse)))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "logits form: zq / lse_p / lse_q and the fused descent are required");
   const void* fn = spec ? (bf ? (const void*)persist_stream_kernel<true, true> : (const void*)persist_stream_kernel<true, false>)
                         : (bf ? (const void*)persist_stream_kernel<false, true> : (const void*)persist_stream_kernel<false, false>);

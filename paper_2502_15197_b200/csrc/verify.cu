@@ -529,6 +529,7 @@ static int select_accept_impl(const double* conf, const int32_t* len, int32_t B_
   sa.cap = cap;
   sa.accepted = accepted;
   sa.rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+  if (in.logits()) sa.rowlse = (float*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWLSE);
   sa.gscratch = abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_GSEL);
   sa.offsets = offsets;
   (void)tokens;  // the accepted-prefix tokens are written by tetris_resample_f32's finalize kernel
@@ -588,6 +589,7 @@ static int resample_impl(const ProbIn& in, const double* u_res, const double* u_
   a.zq = in.zq;
   a.lse_p = in.lse_p;
   a.lse_q = in.lse_q;
+  if (in.logits()) a.rowlse = (const float*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWLSE);
   a.V = V;
   a.nch = n_chunks(V);
   a.R = B;
@@ -622,6 +624,7 @@ static int resample_impl(const ProbIn& in, const double* u_res, const double* u_
     a.spec_ctl = cnt + abi::kSlotSpecCtl;
     a.spec_bitmap = (uint32_t*)(cnt + abi::kSlotSpecBitmap);
     a.spec_list = cnt + abi::kSlotSpecList;
+    if (in.logits()) a.spec_lse = (float*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_SPEC_LSE);
   }
   return launch_persist_stream(a, st);
 }
@@ -838,30 +841,39 @@ static int copy_h2d_batched(std::vector<void*>& dsts, std::vector<void*>& srcs, 
   return TETRIS_OK;
 }
 
-extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k,
-                                                 int64_t C, const float* p_host, const float* q_host,
-                                                 const int32_t* d, const double* u_acc, const double* u_res,
-                                                 const int32_t* cap, int32_t V, float* staging,
-                                                 int64_t* rowinfo_host, int32_t* windows, int32_t* win_offsets,
-                                                 int32_t* accepted, int32_t* out_tok, double* mass_out,
-                                                 int32_t* offsets, int32_t* tokens, int64_t* stats4,
-                                                 uint32_t* status, void* ws, size_t ws_bytes,
-                                                 tetris_stream_t stream) {
+// The host-buffer stochastic step, either input form (T = float probabilities, or uint16_t bf16 logits with their
+// host-resident lse): selection + accept test reading the scalars through the mapping, then (host waits for it) one DMA
+// copy per needed row into `staging`, then the sampler on device memory.  Logits form: the staged rows' lse go to
+// lse_staging (device, [2B]) through the pinned lse_host_scratch ([2B]); the producer's per-request lse pairs were
+// already written by the selector epilogue (values, so the row renumbering does not touch them).
+template <typename T>
+static int staged_impl(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C, const T* p_host,
+                       const T* q_host, const float* lsep_host, const float* lseq_host, const int32_t* d,
+                       const double* u_acc, const double* u_res, const int32_t* cap, int32_t V, T* staging,
+                       float* lse_staging, float* lse_host_scratch, int64_t* rowinfo_host, int32_t* windows,
+                       int32_t* win_offsets, int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
+                       int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                       tetris_stream_t stream) {
+  constexpr bool kLogits = sizeof(T) == 2;
   int rc = check_shape(B, k, V);
   if (rc) return rc;
-  if (!p_host || (k > 0 && !q_host) || !staging || !rowinfo_host)
+  if (!p_host || (k > 0 && !q_host) || !staging || !rowinfo_host ||
+      (kLogits && (!lsep_host || (k > 0 && !lseq_host) || !lse_staging || !lse_host_scratch)))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
-  if (!persist_eligible(staging, staging, V))
+  if (V % 8 != 0 || !aligned16(staging))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "staged step needs V %% 8 == 0 and a 16-byte aligned staging buffer");
   cudaStream_t st = (cudaStream_t)stream;
-  void* p_map = nullptr;
-  void* q_map = nullptr;
+  void *p_map = nullptr, *q_map = nullptr, *lp_map = nullptr, *lq_map = nullptr;
   cudaError_t e = cudaHostGetDevicePointer(&p_map, (void*)p_host, 0);
   if (e == cudaSuccess && q_host) e = cudaHostGetDevicePointer(&q_map, (void*)q_host, 0);
+  if (kLogits && e == cudaSuccess) e = cudaHostGetDevicePointer(&lp_map, (void*)lsep_host, 0);
+  if (kLogits && e == cudaSuccess && lseq_host) e = cudaHostGetDevicePointer(&lq_map, (void*)lseq_host, 0);
   if (e != cudaSuccess) return abi::cuda_fail(e);
-  if ((rc = tetris_select_accept_f32(conf, len, B, k, C, 0, B, (const float*)p_map, (const float*)q_map, d, u_acc, 0,
-                                     cap, V, windows, win_offsets, accepted, offsets, tokens, stats4, status, ws,
-                                     ws_bytes, stream)))
+  const ProbIn mapped = kLogits ? ProbIn{nullptr, nullptr, (const uint16_t*)p_map, (const uint16_t*)q_map,
+                                         (const float*)lp_map, (const float*)lq_map}
+                                : ProbIn{(const float*)p_map, (const float*)q_map, nullptr, nullptr, nullptr, nullptr};
+  if ((rc = select_accept_impl(conf, len, B, k, C, 0, B, mapped, d, u_acc, 0, cap, V, windows, win_offsets, accepted,
+                               offsets, tokens, stats4, status, ws, ws_bytes, stream)))
     return rc;
   long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
   const size_t ri_bytes = (size_t)B * 2 * sizeof(long long);
@@ -869,7 +881,7 @@ extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32
       (e = cudaStreamSynchronize(st)) != cudaSuccess)
     return abi::cuda_fail(e);
   // one copy per needed row, in request order; rowinfo rewritten as staging rows
-  const size_t row_bytes = (size_t)V * sizeof(float);
+  const size_t row_bytes = (size_t)V * sizeof(T);
   std::vector<void*> dsts, srcs;
   std::vector<size_t> sizes;
   dsts.reserve(2 * (size_t)B);
@@ -879,10 +891,12 @@ extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32
     const long long pr = rowinfo_host[2 * b], qr = rowinfo_host[2 * b + 1];
     dsts.push_back(staging + s * V);
     srcs.push_back((void*)(p_host + pr * V));
+    if (kLogits) lse_host_scratch[s] = lsep_host[pr];
     rowinfo_host[2 * b] = s++;
     if (qr >= 0) {
       dsts.push_back(staging + s * V);
       srcs.push_back((void*)(q_host + qr * V));
+      if (kLogits) lse_host_scratch[s] = lseq_host[qr];
       rowinfo_host[2 * b + 1] = s++;
     }
   }
@@ -890,9 +904,45 @@ extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32
   if ((rc = copy_h2d_batched(dsts, srcs, sizes, st))) return rc;
   if ((e = cudaMemcpyAsync(rowinfo, rowinfo_host, ri_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return abi::cuda_fail(e);
-  const ProbIn staged = {staging, staging, nullptr, nullptr, nullptr, nullptr};
-  return resample_impl(staged, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out,
-                       tokens, status, ws, ws_bytes, st);
+  if (kLogits &&
+      (e = cudaMemcpyAsync(lse_staging, lse_host_scratch, (size_t)s * sizeof(float), cudaMemcpyHostToDevice, st)) !=
+          cudaSuccess)
+    return abi::cuda_fail(e);
+  const ProbIn staged = kLogits ? ProbIn{nullptr, nullptr, (const uint16_t*)staging, (const uint16_t*)staging,
+                                         lse_staging, lse_staging}
+                                : ProbIn{(const float*)staging, (const float*)staging, nullptr, nullptr, nullptr,
+                                         nullptr};
+  return resample_impl(staged, u_res, nullptr, nullptr, B, k, V, d, accepted, offsets, out_tok, mass_out, tokens,
+                       status, ws, ws_bytes, st);
+}
+
+extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k,
+                                                 int64_t C, const float* p_host, const float* q_host,
+                                                 const int32_t* d, const double* u_acc, const double* u_res,
+                                                 const int32_t* cap, int32_t V, float* staging,
+                                                 int64_t* rowinfo_host, int32_t* windows, int32_t* win_offsets,
+                                                 int32_t* accepted, int32_t* out_tok, double* mass_out,
+                                                 int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                                 uint32_t* status, void* ws, size_t ws_bytes,
+                                                 tetris_stream_t stream) {
+  return staged_impl<float>(conf, len, B, k, C, p_host, q_host, nullptr, nullptr, d, u_acc, u_res, cap, V, staging,
+                            nullptr, nullptr, rowinfo_host, windows, win_offsets, accepted, out_tok, mass_out,
+                            offsets, tokens, stats4, status, ws, ws_bytes, stream);
+}
+
+extern "C" int tetris_step_stochastic_staged_bf16(const double* conf, const int32_t* len, int32_t B, int32_t k,
+                                                  int64_t C, const uint16_t* zp_host, const float* lse_p_host,
+                                                  const uint16_t* zq_host, const float* lse_q_host, const int32_t* d,
+                                                  const double* u_acc, const double* u_res, const int32_t* cap,
+                                                  int32_t V, uint16_t* staging, float* lse_staging,
+                                                  float* lse_host_scratch, int64_t* rowinfo_host, int32_t* windows,
+                                                  int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                                                  double* mass_out, int32_t* offsets, int32_t* tokens,
+                                                  int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                                  tetris_stream_t stream) {
+  return staged_impl<uint16_t>(conf, len, B, k, C, zp_host, zq_host, lse_p_host, lse_q_host, d, u_acc, u_res, cap, V,
+                               staging, lse_staging, lse_host_scratch, rowinfo_host, windows, win_offsets, accepted,
+                               out_tok, mass_out, offsets, tokens, stats4, status, ws, ws_bytes, stream);
 }
 
 // The greedy step (select -> greedy verification -> compaction) in 2 launches when the selector is the single-CTA one
@@ -1092,7 +1142,7 @@ __global__ void probs_from_logits_kernel(const uint16_t* __restrict__ z, const f
                                          int V, float* __restrict__ out) {
   const int64_t n = R * (int64_t)V;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-    out[e] = tetris::prob_from_logit(tetris::bf16_bits_to_f32(z[e]), lse[e / V]);
+    out[e] = tetris::prob_from_logit(z[e], lse[e / V]);
 }
 
 extern "C" int tetris_probs_from_logits_bf16(const uint16_t* z, const float* lse, int64_t R, int32_t V, float* out,

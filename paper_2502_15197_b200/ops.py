@@ -745,3 +745,60 @@ class HostTetrisStep:
         self.offsets_host.copy_(st.offsets, non_blocking=True)
         self.tokens_host.copy_(st.tokens, non_blocking=True)
         self.accepted_host.copy_(st.accepted, non_blocking=True)
+
+
+class HostLogitStep:
+    """HostTetrisStep for LOGITS: zp_host [B, k+1, V] / zq_host [B, k, V] bf16 and lse_p_host [B, k+1] / lse_q_host
+    [B, k] f32 in pinned host memory (tetris_step_stochastic_staged_bf16: after the selection the needed bf16 rows are
+    copied host->device by the DMA engines -- half the host-link bytes of the fp32 form)."""
+
+    def __init__(self, B: int, k: int, V: int, capacity: int, zp_host: torch.Tensor, lse_p_host: torch.Tensor,
+                 zq_host: torch.Tensor, lse_q_host: torch.Tensor, device="cuda"):
+        for name, t in (("zp_host", zp_host), ("zq_host", zq_host), ("lse_p_host", lse_p_host),
+                        ("lse_q_host", lse_q_host)):
+            if t.is_cuda or not t.is_contiguous() or not t.is_pinned():
+                raise ValueError(f"{name} must be a contiguous pinned host tensor")
+        if zp_host.dtype != torch.bfloat16 or zq_host.dtype != torch.bfloat16:
+            raise ValueError("zp_host / zq_host must be bfloat16")
+        if V % 8:
+            raise ValueError("the logits step needs V % 8 == 0")
+        self.step = TetrisStep(B, k, V, capacity, mode="stochastic", device=device)
+        dev = self.step.device
+        self.host = (zp_host, lse_p_host, zq_host, lse_q_host)
+        self.staging = torch.empty(2 * B, V, dtype=torch.bfloat16, device=dev)
+        self.lse_staging = torch.empty(2 * B, dtype=_F32, device=dev)
+        self.lse_scratch = torch.empty(2 * B, dtype=_F32).pin_memory()
+        self.rowinfo_host = torch.empty(2 * B, dtype=_I64).pin_memory()
+        self.conf = torch.empty(B, k, dtype=_F64, device=dev)
+        self.lengths = torch.empty(B, dtype=_I32, device=dev)
+        self.d = torch.empty(B, k, dtype=_I32, device=dev)
+        self.u_acc = torch.empty(B, k, dtype=_F64, device=dev)
+        self.u_res = torch.empty(B, dtype=_F64, device=dev)
+        self.offsets_host = torch.empty(B + 1, dtype=_I32).pin_memory()
+        self.tokens_host = torch.empty(B * (k + 1), dtype=_I32).pin_memory()
+        self.accepted_host = torch.empty(B, dtype=_I32).pin_memory()
+        self.B, self.k, self.V = B, k, V
+
+    def h2d_bytes(self) -> int:
+        B, k = self.B, self.k
+        return B * k * 8 + B * 4 + B * k * 4 + B * k * 8 + B * 8
+
+    def d2h_bytes(self) -> int:
+        return (self.B + 1) * 4 + self.B * (self.k + 1) * 4 + self.B * 4
+
+    def run(self, conf_h, lengths_h, d_h, u_acc_h, u_res_h) -> None:
+        for dst, src in ((self.conf, conf_h), (self.lengths, lengths_h), (self.d, d_h), (self.u_acc, u_acc_h),
+                         (self.u_res, u_res_h)):
+            dst.copy_(src, non_blocking=True)
+        st = self.step
+        zp, lp, zq, lq = self.host
+        st._check(st._lib.tetris_step_stochastic_staged_bf16(
+            self.conf.data_ptr(), self.lengths.data_ptr(), self.B, self.k, st.C, zp.data_ptr(), lp.data_ptr(),
+            zq.data_ptr(), lq.data_ptr(), self.d.data_ptr(), self.u_acc.data_ptr(), self.u_res.data_ptr(), None,
+            self.V, self.staging.data_ptr(), self.lse_staging.data_ptr(), self.lse_scratch.data_ptr(),
+            self.rowinfo_host.data_ptr(), st.windows_all.data_ptr(), st.win_offsets.data_ptr(), st.accepted.data_ptr(),
+            st.out_tok.data_ptr(), st.mass.data_ptr(), st.offsets.data_ptr(), st.tokens.data_ptr(),
+            st.stats.data_ptr(), st.status.data_ptr(), st.ws.ptr, st.ws.nbytes, torch.cuda.current_stream().cuda_stream))
+        self.offsets_host.copy_(st.offsets, non_blocking=True)
+        self.tokens_host.copy_(st.tokens, non_blocking=True)
+        self.accepted_host.copy_(st.accepted, non_blocking=True)

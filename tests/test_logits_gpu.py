@@ -33,11 +33,16 @@ def test_contract_bits_match_the_oracle_and_exp():
     out = ops.probs_from_logits(z.cuda(), lse.cuda()).cpu().numpy()
     ref = O.probs_from_logits_bf16(_bits(z), lse.numpy())
     assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
-    x = z.float().numpy() - lse.numpy()[:, None]  # fp32 RN, as the contract's first step
-    m = (x >= -86) & (x <= 88)
+    x = z.float().numpy() - lse.numpy()[:, None]  # fp32 RN, as the contract's x (before the row clamp)
+    sane = np.ones(R, bool)
+    sane[[1, 2]] = False  # |lse| = 1e30: outside the contract's domain (defined bits, not exp)
+    m = (x >= -85) & (x <= 87) & sane[:, None]
     rel = np.abs(out[m].astype(np.float64) / np.exp(x[m].astype(np.float64)) - 1)
     assert rel.max() <= 1e-6, rel.max()
-    assert np.all(out > 0) and np.all(np.isfinite(out))
+    assert np.all(out[sane] > 0) and np.all(np.isfinite(out[sane]))
+    # below the clamp every probability reads as ~exp(-86): positive, normal, tiny
+    low = (x < -87) & sane[:, None]
+    assert np.all(out[low] >= np.float32(1.1754944e-38)) and np.all(out[low] < 1e-36)
 
 
 @pytest.mark.parametrize("B,k,V,C,ragged", [(16, 5, 32000, 48, False), (256, 8, 32000, 1024, True),
@@ -118,3 +123,22 @@ def test_logits_step_graph_capture():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(st.out_tok, ref)
+
+
+@pytest.mark.parametrize("B,k,V,C", [(64, 8, 16384, 200), (200, 5, 8200, 500)])
+def test_host_logit_step_matches_device_step(B, k, V, C):
+    lb = make_logit_batch(B, k, V, seed=B + k, ragged=True)
+    dev = ops.TetrisStep(B, k, V, C)
+    dev.run_logits(lb.conf, lb.lengths, lb.zp, lb.lse_p, lb.zq, lb.lse_q, lb.d, lb.u_acc, lb.u_res)
+    torch.cuda.synchronize()
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    hs = ops.HostLogitStep(B, k, V, C, pin(lb.zp), pin(lb.lse_p), pin(lb.zq), pin(lb.lse_q))
+    small = [pin(t) for t in (lb.conf, lb.lengths, lb.d, lb.u_acc, lb.u_res)]
+    for _ in range(2):
+        hs.run(*small)
+        torch.cuda.synchronize()
+        n = int(hs.offsets_host[-1])
+        assert np.array_equal(hs.offsets_host.numpy(), dev.offsets.cpu().numpy())
+        assert np.array_equal(hs.tokens_host.numpy()[:n], dev.tokens.cpu().numpy()[:n])
+        assert np.array_equal(hs.accepted_host.numpy(), dev.accepted.cpu().numpy())
+    ops.raise_for_status(hs.step.status)
