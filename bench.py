@@ -393,7 +393,11 @@ def run_tetris(args):
                          "persist_stream_kernel<spec> (tetris_resample_spec_f32: its own "
                          "phase-A set, streaming, per-request descents in one launch; CUDA events around the launch in "
                          "an eager pass, where the events keep it from overlapping the selector as it does in the "
-                         "step)" if step.uses_spec else "persist_stream_kernel (tetris_resample_f32: streaming + per-"
+                         "step)" if step.uses_spec else
+                         "persist_stream_kernel<fused> (tetris_step_stochastic_f32 on a small batch: the selection, "
+                         "accept test and offset scans as the sampler's prologue, streaming, per-request descents — the "
+                         "whole step in one launch; CUDA events around the launch, eager pass)" if step.fused else
+                         "persist_stream_kernel (tetris_resample_f32: streaming + per-"
                          "request descent in the same launch; CUDA events around the launch, eager pass)")
                          if mode == "stochastic"
                          else "greedy_rowmap_kernel + persist_greedy_kernel (tetris_verify_greedy_compact_f32: argmax "

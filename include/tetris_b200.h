@@ -113,7 +113,9 @@ int tetris_abi_version(void);
  * tetris_step_stochastic_f32 falls back to the plain sampler above it. */
 int tetris_spec_max_requests(void);
 
-/* Diagnostics: when dev_buf != NULL the selector writes clock64() stamps of its phases (CTA 0) into dev_buf[0..9]. */
+/* Diagnostics (tools/dbg_*.py): when dev_buf != NULL the selector writes clock64() stamps of its phases (CTA 0) into
+ * dev_buf[0..49] and the persistent kernels per-CTA %globaltimer / clock64() stamps from dev_buf[64] on; dev_buf must
+ * hold 64 + 32 x (SM count) int64.  NULL turns them off (the default). */
 int tetris_debug_timestamps(void* dev_buf);
 
 /* Stages (1)+(2): prefix products and capacity-constrained greedy selection.

@@ -103,6 +103,7 @@ constexpr size_t kSlotWorkSpec = kRequestSlots + 6;      // the speculative samp
 constexpr size_t kSlotSpecCnt = kRequestSlots + 64;      // its per-request completion counters [64 + 0, 64 + 4096)
 constexpr size_t kSpecSlots = 4096;
 constexpr size_t kSlotSpecCtl = kRequestSlots + 8;       // [2]: phase-A list length, requests processed
+constexpr size_t kSlotFusedCtl = kRequestSlots + 10;     // [2]: fused step: CTAs published, scans done
 constexpr size_t kSlotSpecBitmap = kSlotSpecCnt + kSpecSlots;   // [kSpecSlots / 32]: the phase-A set
 constexpr size_t kSlotSpecList = kSlotSpecBitmap + kSpecSlots / 32;  // [kSpecSlots]: the phase-A list
 constexpr size_t kSlotGreedyKey0 = kSlotSpecList + kSpecSlots;  // [2 * 65536]: greedy row-0 argmax keys (u64)

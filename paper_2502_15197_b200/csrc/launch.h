@@ -49,6 +49,28 @@ struct SelectArgs {
 void set_debug_buffer(long long* p);
 long long* debug_buffer();
 
+// The selection fused into the sampler's launch (persist_stream_kernel<.., FUSED>, small batches: B_sel * k <=
+// kFusedMaxCells): every CTA computes the keys of all B_sel rows, the exact rank of the cells of its own rows
+// (g, g + G, ...) and from them the rows' windows, accept verdicts and row choice; the last CTA to publish writes
+// the offset scans and the PolicyStats.  conf == nullptr: off.
+struct FusedSel {
+  const double* conf;   // [B_sel][k]
+  const int32_t* len;   // [B_sel] nullable (k)
+  const double* u_acc;  // [R][k] dense accept uniforms
+  int B_sel, row0;      // selected rows; local rows [row0, row0 + R)
+  long long C;
+  int32_t* windows;     // [B_sel]
+  int32_t* win_offsets; // [B_sel + 1]
+  long long* stats;     // [4] nullable
+  const int32_t* cap;   // [R] nullable
+  int32_t* accepted;    // [R]
+  long long* rowinfo;   // [R][2]
+  float* rowlse;        // [R][2] logits form
+  int32_t* offsets;     // [R + 1]
+  int* ctl;             // [2] rows published (CTAs), scans done (zero, left at zero)
+};
+constexpr int kFusedMaxCells = 2048;
+
 struct StreamArgs {
   const float* p;
   const float* q;
@@ -89,7 +111,9 @@ struct StreamArgs {
   int* spec_ctl;             // [2]: phase-A list length, requests processed (zero, left at zero)
   uint32_t* spec_bitmap;     // [ceil(R / 32)]: the phase-A set (zero, left at zero)
   int* spec_list;            // [R]: the phase-A list, entry b + 1 (zero, left at zero)
+  FusedSel fs;               // fused selection (fs.conf != nullptr; not with the speculative variant)
 };
+bool fused_step_eligible(int B_sel, int k, int u_packed);
 int spec_max_requests();
 
 // Greedy verification (greedy.cu): the persistent argmax stream over the rows listed by greedy_rowmap_kernel.

@@ -22,6 +22,7 @@
 // slower here).
 // HBM is touched once per streamed element; the descent's re-read is 4-8 KB per request.
 #include "common.cuh"
+#include "fused_select.cuh"
 #include "launch.h"
 
 namespace tetris {
@@ -63,7 +64,8 @@ __device__ __forceinline__ void gstamp(const StreamArgs& a, int slot) {
   if (a.dbg) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.dbg[64 + 8 * blockIdx.x + slot] = t;
+    a.dbg[64 + 16 * blockIdx.x + slot] = t;
+    a.dbg[64 + 16 * gridDim.x + 16 * blockIdx.x + slot] = clock64();  // SM cycles, for in-CTA phase lengths
   }
 }
 
@@ -222,25 +224,49 @@ template <bool BF>
 __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane, const double* chunk_sums,
                                  const double* warp_sums) {
   const int nch = a.nch;
-  const long long prow = a.prow[(int64_t)b * a.row_stride];
-  const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+  const long long prow = __ldcg(a.prow + (int64_t)b * a.row_stride);
+  const long long qrow = a.qrow ? __ldcg(a.qrow + (int64_t)b * a.row_stride) : -1;
   const float lp = BF ? a.lse_p[prow] : 0.f;
   const float lq = (BF && qrow >= 0) ? a.lse_q[qrow] : 0.f;
   const double* cs = chunk_sums + (int64_t)b * nch;
   const double* ws = warp_sums + (int64_t)b * nch * kChunkWarps;
-  double s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
-  double s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
+  // nch <= 16: all nch * 8 warp sums in ONE round trip (lane l holds sums l, l + 32, l + 64, l + 96: chunk c's eight
+  // are register c / 4, lanes 8 (c % 4) .. + 7); the chunk sums are re-folded from them left to right (the
+  // publisher's exact arithmetic).  Larger rows: chunk sums first, the chosen chunk's warp sums second.
+  const bool one_trip = nch <= 16;
+  double wv[4];
+  double s_lo = 0.0, s_hi = 0.0;
+  if (one_trip) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) wv[x] = lane + 32 * x < nch * kChunkWarps ? __ldcg(ws + lane + 32 * x) : 0.0;
+  } else {
+    s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
+    s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
+  }
   // accepted-prefix tokens of the compacted stream, in parallel with the loads above
   int acc = 0, off = 0, end = 0;
   if (a.accepted) {
-    acc = a.accepted[b];
-    off = a.offsets[b];
-    end = a.offsets[b + 1];
+    acc = __ldcg(a.accepted + b);
+    off = __ldcg(a.offsets + b);
+    end = __ldcg(a.offsets + b + 1);
     for (int j = lane; j < acc && off + j < end; j += 32) a.tokens[off + j] = a.d[(int64_t)b * a.k + j];
   }
   const double u = a.u[b];
   uint32_t bad = 0;
   if (!(u >= 0.0 && u < 1.0)) bad |= TETRIS_ST_BAD_UNIFORM;
+  if (one_trip) {
+    double t4[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      double S = 0.0;  // lane l: the sum of chunk 4x + l / 8
+#pragma unroll
+      for (int w = 0; w < kChunkWarps; ++w) S = S + __shfl_sync(kFull, wv[x], (lane & 24) + w);
+      t4[x] = __shfl_sync(kFull, S, 8 * (lane & 3));  // lane l: the sum of chunk 4x + l % 4
+    }
+    const int xl = (lane >> 2) & 3;  // lane c < 16 takes chunk c = 4 * (c / 4) + c % 4
+    s_lo = xl == 0 ? t4[0] : xl == 1 ? t4[1] : xl == 2 ? t4[2] : t4[3];
+    if (lane >= nch) s_lo = 0.0;
+  }
   // mass = chunk sums folded left to right (every lane holds the same value)
   double mass = 0.0;
   for (int c = 0; c < nch; ++c) mass = mass + __shfl_sync(kFull, c < 32 ? s_lo : s_hi, c & 31);
@@ -266,11 +292,18 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
       cc = last_pos;
       T = __longlong_as_double(0x7ff0000000000000ll);
     }
-    // the 8 warp sums of the chosen chunk (lanes 0..7 load, then broadcast)
-    const double wl = (cc >= 0 && lane < kChunkWarps) ? __ldcg(ws + (int64_t)cc * kChunkWarps + lane) : 0.0;
+    // the 8 warp sums of the chosen chunk (from lane cc's registers, or lanes 0..7 load them, then broadcast)
     double Wc[kChunkWarps];
+    if (one_trip) {
+      const int c0 = cc < 0 ? 0 : cc, xr = c0 >> 2;
+      const double src = xr == 0 ? wv[0] : xr == 1 ? wv[1] : xr == 2 ? wv[2] : wv[3];
 #pragma unroll
-    for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __shfl_sync(kFull, wl, w);
+      for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __shfl_sync(kFull, src, 8 * (c0 & 3) + w);
+    } else {
+      const double wl = (cc >= 0 && lane < kChunkWarps) ? __ldcg(ws + (int64_t)cc * kChunkWarps + lane) : 0.0;
+#pragma unroll
+      for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __shfl_sync(kFull, wl, w);
+    }
     const int ww = seq_find(Wc, kChunkWarps, T);
     if (cc >= 0 && ww >= 0) {
       const int64_t e0 = (int64_t)cc * kChunkElems + ww * kWarpElems;
@@ -320,9 +353,12 @@ __device__ __forceinline__ void issue_item(const StreamArgs& a, PersistShared& s
 // Deeper producer schedule for the logits form (its items are half as many bytes, so the claim / row-lookup round
 // trips must overlap more): C claims on the work counter and L row lookups in flight, kept in shift registers.
 // req(i) -> request of item i; rows(b, prow, qrow, lse_p, lse_q).  Returns the next stage index.
+// gate != nullptr (fused step): the claims go out first, then the row lookups wait until every CTA has published
+// its rows (*gate == gridDim.x).
 template <bool BF, int L, int C, typename Req, typename Rows>
 __device__ int stream_deep(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, long long total,
-                           unsigned long long* work, int phase, uint64_t pol, Req req, Rows rows) {
+                           unsigned long long* work, int phase, uint64_t pol, Req req, Rows rows,
+                           const int* gate = nullptr) {
   constexpr int D = L + C;
   long long ci[D], pr[D], qr[D];
   float lp[D], lq[D];
@@ -332,6 +368,10 @@ __device__ int stream_deep(const StreamArgs& a, PersistShared& sh, uint8_t* stag
     pr[d] = 0;
     qr[d] = -1;
     lp[d] = lq[d] = 0.f;
+  }
+  if (gate) {
+    spin_acquire_geq(gate, (int)gridDim.x);
+    gstamp(a, 7);
   }
 #pragma unroll
   for (int d = 0; d < L; ++d)
@@ -381,7 +421,154 @@ __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stag
   return t;
 }
 
-template <bool SPEC, bool BF>
+// ---- the selection fused into the sampler's launch (FUSED variant, B_sel * k <= kFusedMaxCells) ------------------
+// fused_select.cuh's rank selection on all 576 threads, with this kernel's per-row epilogue: verify_token's first
+// rejection among the selected positions (accept_model.py:309-313, sim_engine.py:397-401) from verdicts gathered in
+// the selection's first round trip, the row to resample from, and — in the last CTA to publish — the compaction
+// offsets.  The producers wait for every CTA's rows (ctl[0] == G), the descents for the scans (ctl[1]).
+// An own cell's accept-test inputs, loaded raw in one phase and turned into the verdict in a later one, so the
+// dependent gathers overlap the key and rank phases instead of stalling the first.
+struct FusedCell {
+  int t;        // drafted token
+  double u;     // accept uniform
+  float pv, qv; // p[lr][j][t], q[lr][j][t] (fp32 form) / lse of those rows (logits form)
+  uint32_t zz;  // logits form: the two bf16 logits (p low, q high)
+};
+constexpr int kFusedCellsPerThread = 4;  // own cells <= B_sel * k <= kFusedMaxCells <= 4 * 576
+
+template <bool BF>
+__device__ void fused_select(const StreamArgs& a, uint8_t* smem) {
+  const FusedSel& f = a.fs;
+  const int tid = threadIdx.x, NT = blockDim.x, G = gridDim.x, g = blockIdx.x, k = a.k;
+  const FusedView v = fused_view(f, k, smem);
+  __shared__ int s_last;
+  __shared__ long long s_tmp[33];
+  // phase 0: scores + lengths (shared), the own cells' drafted tokens and uniforms (registers)
+  FusedCell cell[kFusedCellsPerThread];
+  int64_t ce[kFusedCellsPerThread];  // (lr * k + j) of the cell, -1: not a local drafted cell
+#pragma unroll
+  for (int x = 0; x < kFusedCellsPerThread; ++x) {
+    const int c = tid + x * NT;
+    ce[x] = -1;
+    if (c < v.ncell) {
+      const int oi = c / k, j = c - oi * k, lr = g + oi * G - f.row0;
+      if (lr >= 0 && lr < a.R) ce[x] = (int64_t)lr * k + j;
+    }
+    cell[x].t = ce[x] >= 0 ? __ldg(a.d + ce[x]) : 0;
+    cell[x].u = ce[x] >= 0 ? __ldg(f.u_acc + ce[x]) : 0.0;
+  }
+  fused_stage(f, k, v, tid, NT);
+  fused_bar(NT);
+  if (tid == 0) gstamp(a, 8);
+  // phase 1: the gathers p[lr][j][t], q[lr][j][t] go out, then the keys are built while they are in flight
+#pragma unroll
+  for (int x = 0; x < kFusedCellsPerThread; ++x) {
+    const int t = cell[x].t;
+    cell[x].zz = 0u;
+    cell[x].pv = cell[x].qv = 0.f;
+    if (ce[x] >= 0 && t >= 0 && t < a.V) {
+      const int64_t e = ce[x], lr = e / k, prow = lr * (k + 1) + (e - lr * k);
+      if (BF) {
+        cell[x].zz = (uint32_t)__ldg(a.zp + prow * a.V + t) | ((uint32_t)__ldg(a.zq + e * a.V + t) << 16);
+        cell[x].pv = __ldg(a.lse_p + prow);
+        cell[x].qv = __ldg(a.lse_q + e);
+      } else {
+        cell[x].pv = __ldg(a.p + prow * a.V + t);
+        cell[x].qv = __ldg(a.q + e * a.V + t);
+      }
+    }
+  }
+  fused_keys(f, k, v, tid, NT, a.status);
+  fused_bar(NT);
+  if (tid == 0) gstamp(a, 9);
+  // phase 2: ranks; then the verdicts (verify_token, accept_model.py:309-313) of the own cells.  Verdict byte: bit0
+  // accept, bit1 drafted token outside the vocabulary, bit2 uniform outside [0, 1)
+  fused_ranks(k, v, tid, NT);
+#pragma unroll
+  for (int x = 0; x < kFusedCellsPerThread; ++x) {
+    const int c = tid + x * NT;
+    if (c >= v.ncell) continue;
+    uint8_t vb = 0;
+    if (ce[x] >= 0) {
+      const double u = cell[x].u;
+      const int t = cell[x].t;
+      vb = (u >= 0.0 && u < 1.0) ? 0 : 4;
+      if (t < 0 || t >= a.V) {
+        vb |= 2;
+      } else {
+        const double m = BF ? (double)prob_from_logit(cell[x].zz & 0xffffu, cell[x].pv) : (double)cell[x].pv;
+        const double s = BF ? (double)prob_from_logit(cell[x].zz >> 16, cell[x].qv) : (double)cell[x].qv;
+        vb |= ((s <= m) || (u < m / s)) ? 1 : 0;
+      }
+    }
+    v.verd[c] = vb;
+  }
+  fused_bar(NT);
+  if (tid == 0) gstamp(a, 10);
+  // phase 3: the own rows' windows, first rejection (sim_engine.py:397-401), row to resample from
+  for (int oi = tid; oi < v.nown; oi += NT) {
+    const int r = g + oi * G;
+    const int w = fused_window(f, k, v, oi);
+    f.windows[r] = w;
+    const int lr = r - f.row0;
+    if (lr >= 0 && lr < a.R) {
+      uint32_t vbad = 0;
+      int acc = w;
+      for (int j = 0; j < w; ++j) {
+        const uint8_t vb = v.verd[oi * k + j];
+        vbad |= (vb & 2 ? TETRIS_ST_BAD_TOKEN : 0u) | (vb & 4 ? TETRIS_ST_BAD_UNIFORM : 0u);
+        if (!(vb & 1)) {
+          acc = j;
+          break;
+        }
+      }
+      f.accepted[lr] = acc;
+      f.rowinfo[2 * (int64_t)lr] = (long long)lr * (k + 1) + acc;              // residual row / bonus row of p
+      f.rowinfo[2 * (int64_t)lr + 1] = acc < w ? (long long)lr * k + acc : -1;  // draft row (residual only)
+      if (BF) {
+        f.rowlse[2 * (int64_t)lr] = __ldg(a.lse_p + (int64_t)lr * (k + 1) + acc);
+        f.rowlse[2 * (int64_t)lr + 1] = acc < w ? __ldg(a.lse_q + (int64_t)lr * k + acc) : 0.f;
+      }
+      set_status(a.status, vbad);
+    }
+  }
+  if (fused_publish(f, tid, NT, &s_last)) {
+    if (tid == 0) gstamp(a, 11);
+    // the last CTA to publish: windows -> win_offsets + PolicyStats; emitted counts -> offsets (compact's contract);
+    // both scans' inputs in one round trip
+    int wr[kFusedMaxRpt], nr[kFusedMaxRpt];
+    fused_load_windows(f, tid, NT, wr);
+    const int R = a.R, rpl = (R + NT - 1) / NT, l0 = tid * rpl;
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) {
+      const int lr = l0 + i;
+      nr[i] = (i < rpl && lr < R) ? __ldcg(f.accepted + lr) + 1 : 0;
+      if (f.cap && i < rpl && lr < R) nr[i] = min(nr[i], max(__ldg(f.cap + lr), 0));
+    }
+    fused_win_scan(f, v, tid, NT, s_tmp, wr);
+    long long my = 0;
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) my += nr[i];
+    long long etot;
+    long long eex = fused_excl_scan<long long>(my, s_tmp, etot, tid, NT);
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) {
+      const int lr = l0 + i;
+      if (i < rpl && lr < R) {
+        f.offsets[lr] = (int32_t)eex;
+        eex += nr[i];
+      }
+    }
+    if (tid == 0) f.offsets[R] = (int32_t)etot;
+    fused_release_done(f, tid, NT);
+    if (tid == 0) gstamp(a, 12);
+  }
+  // the stage ring is written by the TMA engine (async proxy) after these generic shared-memory accesses
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+}
+
+template <bool SPEC, bool BF, bool FUSED = false>
 __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_stream_kernel(const StreamArgs a) {
   constexpr int kStages = Elem<BF>::kStages;
   extern __shared__ __align__(128) uint8_t stage_mem[];
@@ -460,11 +647,13 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
   }
   __syncthreads();
   if (!SPEC) {
-    // launched as a programmatic dependent of the selector: wait for it (and its memory) before the first read of
-    // the row info it wrote; no-op for a plain launch
+    // launched as a programmatic dependent of the selector (FUSED: of whatever precedes the step — it may have written
+    // the inputs): wait for it (and its memory) before the first read of the row info it wrote; no-op for a plain
+    // launch
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) gstamp(a, 1);
   }
+  if (FUSED) fused_select<BF>(a, stage_mem);
 
   if (warp == kProducerWarp) {
     // ---------------------------------------------------------------- producer
@@ -556,11 +745,11 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       int t = stream_deep<BF, 3, 3>(a, sh, stage_mem, 0, total, work, 0, pol,
                                     [&](long long i) { return (int)(i / nch); },
                                     [&](int b, long long& pr, long long& qr, float& lp, float& lq) {
-                                      pr = a.prow[(int64_t)b * a.row_stride];
-                                      qr = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
-                                      lp = a.rowlse[2 * (int64_t)b];
-                                      lq = a.rowlse[2 * (int64_t)b + 1];
-                                    });
+                                      pr = __ldcg(a.prow + (int64_t)b * a.row_stride);
+                                      qr = a.qrow ? __ldcg(a.qrow + (int64_t)b * a.row_stride) : -1;
+                                      lp = __ldcg(a.rowlse + 2 * (int64_t)b);
+                                      lq = __ldcg(a.rowlse + 2 * (int64_t)b + 1);
+                                    }, FUSED ? a.fs.ctl : nullptr);
       const int s = t % kStages;  // end of stream: a sentinel stage without data
       if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
       sh.meta[s] = StageMeta{-1, 0, 0, 0};
@@ -571,15 +760,19 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       // two items of look-ahead on the counter and the row info, so neither round trip stalls the copies
       long long i_next = (long long)atomicAdd(work, 1ull);
       long long i_next2 = (long long)atomicAdd(work, 1ull);
+      if (FUSED) {  // the claims are out; the row lookups need every CTA's rows published
+        spin_acquire_geq(a.fs.ctl, G);
+        gstamp(a, 7);
+      }
       long long pn = 0, qn = -1;
       float lpn = 0.f, lqn = 0.f;
       auto rows = [&](long long ii) {
         const int bb = (int)(ii / nch);
-        pn = a.prow[(int64_t)bb * a.row_stride];
-        qn = a.qrow ? a.qrow[(int64_t)bb * a.row_stride] : -1;
+        pn = __ldcg(a.prow + (int64_t)bb * a.row_stride);
+        qn = a.qrow ? __ldcg(a.qrow + (int64_t)bb * a.row_stride) : -1;
         if (BF) {
-          lpn = a.rowlse[2 * (int64_t)bb];
-          lqn = a.rowlse[2 * (int64_t)bb + 1];
+          lpn = __ldcg(a.rowlse + 2 * (int64_t)bb);
+          lqn = __ldcg(a.rowlse + 2 * (int64_t)bb + 1);
         }
       };
       if (i_next < total) rows(i_next);
@@ -725,11 +918,17 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
     // Descent, one warp per request (requests strided over the CTAs so the re-reads spread over all SMs), as soon
     // as the request's nch chunks are published.  A warp only ever waits for chunks already claimed from the work
     // counter by CTAs that are running, so no co-residency (cooperative launch) is needed.
+    if (FUSED) {
+      // the next launch on the stream may be scheduled onto the SMs as this grid's CTAs leave (it waits for the whole
+      // grid before touching anything); the descents need the fused selection's offset scans
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      if (tid == 0) spin_acquire_geq(a.fs.ctl + 1, 1);
+    }
     __syncthreads();
     if (SPEC) asm volatile("griddepcontrol.wait;" ::: "memory");  // the selector's row info (no-op by now)
     const int nwarps = blockDim.x >> 5;
     for (int b = warp * G + blockIdx.x; b < R; b += G * nwarps) {
-      const long long qrow = a.qrow ? a.qrow[(int64_t)b * a.row_stride] : -1;
+      const long long qrow = a.qrow ? __ldcg(a.qrow + (int64_t)b * a.row_stride) : -1;
       const bool inA = SPEC && ((sx.inA[b >> 5] >> (b & 31)) & 1u);
       const bool doneA = inA && qrow == (long long)b * k;
       if (lane == 0) {
@@ -764,6 +963,10 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       if (s_last) {
         *work = 0ull;
         if (SPEC) *work_a = 0ull;
+        if (FUSED) {
+          a.fs.ctl[0] = 0;
+          a.fs.ctl[1] = 0;
+        }
         *done = 0u;
       }
     }
@@ -894,12 +1097,19 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
   if (bf && (!a.lse_p || (a.qrow && (!a.zq || !a.lse_q)) || a.req_cnt == nullptr || !a.rowlse ||
              (spec && !a.spec_lse)))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "logits form: zq / lse_p / lse_q and the fused descent are required");
-  const void* fn = spec ? (bf ? (const void*)persist_stream_kernel<true, true> : (const void*)persist_stream_kernel<true, false>)
+  const bool fused = a.fs.conf != nullptr;
+  if (fused && (spec || a.req_cnt == nullptr || !a.accepted || !a.fs.ctl || !a.fs.u_acc || !a.d ||
+                (long long)a.fs.B_sel * a.k > kFusedMaxCells || (bf && !a.fs.rowlse)))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "fused step: B_sel * k > %d or missing buffers", kFusedMaxCells);
+  const void* fn = fused ? (bf ? (const void*)persist_stream_kernel<false, true, true>
+                               : (const void*)persist_stream_kernel<false, false, true>)
+                   : spec ? (bf ? (const void*)persist_stream_kernel<true, true> : (const void*)persist_stream_kernel<true, false>)
                         : (bf ? (const void*)persist_stream_kernel<false, true> : (const void*)persist_stream_kernel<false, false>);
   cudaError_t e = abi::ensure_smem(fn, kPersistSmem);
   if (e != cudaSuccess) return abi::cuda_fail(e);
   const long long items = (long long)a.R * a.nch;
-  const int grid = (int)(items < g_num_sms ? items : g_num_sms);
+  // fused: every SM (the selection's rank work is spread over the CTAs, and more CTAs shorten it)
+  const int grid = fused ? g_num_sms : (int)(items < g_num_sms ? items : g_num_sms);
   const int threads = kPersistThreads + (spec ? 32 : 0);
   if (a.req_cnt != nullptr) {
     // one launch: streaming + per-request completion counters + descent
@@ -928,6 +1138,11 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
 // requests one speculative call can take on the current device: its shared-memory lists hold kSpecMaxR, and each CTA
 // evaluates at most 32 requests' position-0 verdicts in the prologue (ceil(R / grid) <= 32)
 int spec_max_requests() { return std::min(kSpecMaxR, 32 * abi::device_sm_count()); }
+
+bool fused_step_eligible(int B_sel, int k, int u_packed) {
+  static const bool off = std::getenv("TETRIS_NO_FUSED") != nullptr;  // A/B timing switch: the two-launch step
+  return !u_packed && B_sel >= 1 && (long long)B_sel * k <= kFusedMaxCells && !off;
+}
 
 bool persist_eligible(const float* p, const float* q, int V) {
   return (V % kLaneElems == 0) && (((uintptr_t)p & 15u) == 0) && (!q || (((uintptr_t)q & 15u) == 0)) &&

@@ -669,6 +669,75 @@ static int step_stochastic_impl(const double* conf, const int32_t* len, int32_t 
                                 int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
                                 size_t ws_bytes, tetris_stream_t stream);
 
+// Small batches (B_sel * k <= kFusedMaxCells, dense uniforms): the whole step in ONE launch — the selection, accept
+// test, row choice and offset scans run as the persistent sampler's prologue (stream.cu, fused_select), so the step
+// pays one launch and no selector latency chain.  Same arguments, checks and results as the two-launch step.
+static int fused_step_impl(const double* conf, const int32_t* len, int32_t B_sel, int32_t k, int64_t C, int32_t row0,
+                           int32_t B, const ProbIn& in, const int32_t* d, const double* u_acc, const double* u_res,
+                           const int32_t* cap, int32_t V, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
+                           int32_t* out_tok, double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                           uint32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
+  int rc = check_shape(B, k, V);
+  if (rc) return rc;
+  if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
+  if (B_sel < B || B_sel > TETRIS_MAX_SELECT_ROWS || row0 < 0 || row0 + B > B_sel)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "local rows [%d, %d) outside the %d selected rows", row0, row0 + B, B_sel);
+  if ((k > 0 && (!conf || !d || !u_acc || !in.qbase() || (in.logits() && !in.lse_q))) || !in.pbase() ||
+      (in.logits() && !in.lse_p) || !windows || !win_offsets || !accepted || !offsets || !tokens)
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
+  long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
+  int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
+  StreamArgs a = {};
+  a.p = in.p;
+  a.q = in.q;
+  a.zp = in.zp;
+  a.zq = in.zq;
+  a.lse_p = in.lse_p;
+  a.lse_q = in.lse_q;
+  float* rowlse = in.logits() ? (float*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWLSE) : nullptr;
+  a.rowlse = rowlse;
+  a.V = V;
+  a.nch = n_chunks(V);
+  a.R = B;
+  a.k = k;
+  a.d = d;
+  a.prow = rowinfo;
+  a.qrow = rowinfo + 1;
+  a.row_stride = 2;
+  a.u = u_res;
+  a.out_idx = out_tok;
+  a.mass_out = mass_out;
+  a.status = status;
+  a.counters = cnt;
+  a.chunk_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_CHUNK_SUMS);
+  a.warp_sums = (double*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_WARP_SUMS);
+  a.grid_bar = (unsigned*)cnt + abi::kSlotGridCount;
+  a.req_cnt = cnt;
+  a.accepted = accepted;
+  a.offsets = offsets;
+  a.tokens = tokens;
+  FusedSel& f = a.fs;
+  static const double kNoScores = 0.0;  // k == 0: nothing is read through these
+  f.conf = conf ? conf : &kNoScores;
+  f.len = len;
+  f.u_acc = u_acc ? u_acc : &kNoScores;
+  f.B_sel = B_sel;
+  f.row0 = row0;
+  f.C = (long long)C;
+  f.windows = windows;
+  f.win_offsets = win_offsets;
+  f.stats = (long long*)stats4;
+  f.cap = cap;
+  f.accepted = accepted;
+  f.rowinfo = rowinfo;
+  f.rowlse = rowlse;
+  f.offsets = offsets;
+  f.ctl = cnt + abi::kSlotFusedCtl;
+  if (k == 0) a.d = d ? d : (const int32_t*)&kNoScores;
+  return launch_persist_stream(a, st);
+}
+
 extern "C" int tetris_step_stochastic_f32(const double* conf, const int32_t* len, int32_t B_sel, int32_t k,
                                           int64_t C, int32_t row0, int32_t B, const float* p, const float* q,
                                           const int32_t* d, const double* u_acc, int32_t u_packed,
@@ -691,6 +760,10 @@ static int step_stochastic_impl(const double* conf, const int32_t* len, int32_t 
   if (!persist_eligible_in(in, V))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "fused step needs V %% 8 == 0 and 16-byte aligned rows");
   if (!u_res || !out_tok) return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (fused_step_eligible(B_sel, k, u_packed) && B >= 1)
+    return fused_step_impl(conf, len, B_sel, k, C, row0, B, in, d, u_acc, u_res, cap, V, windows, win_offsets,
+                           accepted, out_tok, mass_out, offsets, tokens, stats4, status, ws, ws_bytes,
+                           (cudaStream_t)stream);
   int rc = select_accept_impl(conf, len, B_sel, k, C, row0, B, in, d, u_acc, u_packed, cap, V, windows, win_offsets,
                               accepted, offsets, tokens, stats4, status, ws, ws_bytes, stream);
   if (rc) return rc;

@@ -391,6 +391,8 @@ SPEC_MAX_REQUESTS = 4096  # tetris_resample_spec_f32's limit (per call, local ro
 # below this much streaming the early start does not pay (csrc/verify.cu kSpecMinChunks); env override for A/B runs
 SPEC_MIN_CHUNKS = int(os.environ.get("TETRIS_SPEC_MIN_CHUNKS", "4096"))
 _NO_SPEC = os.environ.get("TETRIS_NO_SPEC") == "1"  # A/B timing switch: the plain sampler
+FUSED_MAX_CELLS = 2048  # csrc/launch.h kFusedMaxCells: the one-launch stochastic step up to this many cells
+_NO_FUSED = "TETRIS_NO_FUSED" in os.environ  # A/B timing switch: the two-launch step (read by the library too)
 
 
 class TetrisStep:
@@ -486,6 +488,21 @@ class TetrisStep:
             if events is not None:
                 events[3].record()
             return
+        if self.mode == "stochastic" and self.fused:
+            # small batch: the whole step is ONE launch (tetris_step_stochastic_f32 -> the sampler with the selection
+            # as its prologue, csrc/stream.cu fused_select); events bracket [nothing | the step | nothing]
+            if events is not None:
+                events[1].record()
+            self._check(lib.tetris_step_stochastic_f32(
+                sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, self.rank * B, B, p.data_ptr(), q.data_ptr(),
+                d.data_ptr(), u_acc.data_ptr(), 0, u_res.data_ptr(), _ptr(cap), V, self.windows_all.data_ptr(),
+                self.win_offsets.data_ptr(), self.accepted.data_ptr(), self.out_tok.data_ptr(), self.mass.data_ptr(),
+                self.offsets.data_ptr(), self.tokens.data_ptr(), self.stats.data_ptr(), self.status.data_ptr(),
+                ws.ptr, ws.nbytes, s))
+            if events is not None:
+                events[2].record()
+                events[3].record()
+            return
         if self.mode == "stochastic":
             # == tetris_step_stochastic_f32, called as its two halves so an event can sit between the kernels
             rc = lib.tetris_select_accept_f32(
@@ -564,6 +581,19 @@ class TetrisStep:
             sel_conf, sel_len = self.conf_all, self.len_all
         else:
             sel_conf, sel_len = conf, lengths
+        if self.fused:
+            if events is not None:
+                events[1].record()
+            self._check(lib.tetris_step_stochastic_bf16(
+                sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, self.rank * B, B, zp.data_ptr(),
+                lse_p.data_ptr(), zq.data_ptr(), lse_q.data_ptr(), d.data_ptr(), u_acc.data_ptr(), 0,
+                u_res.data_ptr(), _ptr(cap), V, self.windows_all.data_ptr(), self.win_offsets.data_ptr(),
+                self.accepted.data_ptr(), self.out_tok.data_ptr(), self.mass.data_ptr(), self.offsets.data_ptr(),
+                self.tokens.data_ptr(), self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+            if events is not None:
+                events[2].record()
+                events[3].record()
+            return
         self._check(lib.tetris_select_accept_bf16(
             sel_conf.data_ptr(), _ptr(sel_len), self.Bg, k, self.C, self.rank * B, B, zp.data_ptr(),
             lse_p.data_ptr(), zq.data_ptr(), lse_q.data_ptr(), d.data_ptr(), u_acc.data_ptr(),
@@ -621,6 +651,13 @@ class TetrisStep:
             raise ValueError(msg) if rc == N.INVALID_ARGUMENT else N.TetrisError(rc, msg)
 
     @property
+    def fused(self) -> bool:
+        """True when the stochastic step is ONE launch: the selection runs as the sampler's prologue (small batches,
+        Bg * k <= FUSED_MAX_CELLS, dense uniforms; csrc/stream.cu fused_select)."""
+        return (self.mode == "stochastic" and self.policy == "tetris" and self.u_layout == "dense"
+                and self.Bg * self.k <= FUSED_MAX_CELLS and not _NO_FUSED)
+
+    @property
     def uses_spec(self) -> bool:
         """True when the stochastic step runs the speculative sampler (tetris_resample_spec_f32)."""
         return (self.mode == "stochastic" and self.policy == "tetris" and self.u_layout == "dense"
@@ -636,7 +673,9 @@ class TetrisStep:
         if self.policy == "fixed":
             return 4 if self.mode == "stochastic" else 3
         if self.mode == "stochastic":
-            return 2 if self.V % 8 == 0 else 3  # V % 8 != 0: select, verify (one sample_kernel), compact
+            if self.V % 8 != 0:
+                return 3  # select, verify (one sample_kernel), compact
+            return 1 if self.fused else 2
         return 2 if self.Bg * self.k <= 16384 and self.Bg <= 4096 else 3
 
 

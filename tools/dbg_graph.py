@@ -1,5 +1,5 @@
 """Step timeline under CUDA-graph replay (the bench's launch mode): %globaltimer stamps of the selector (CTA 0 start /
-end, dbg[48..49]) and of the sampler's CTAs (dbg[64 + 8 cta + slot]) for one replay of a 2-step graph, so the gaps
+end, dbg[48..49]) and of the sampler's CTAs (dbg[64 + 16 cta + slot]) for one replay of a 2-step graph, so the gaps
 between kernels and between steps show.  usage: python tools/dbg_graph.py [B k V C]"""
 import sys
 from pathlib import Path
@@ -16,7 +16,7 @@ bt = make_batch(B, k, V, seed=0)
 step = ops.TetrisStep(B, k, V, C)
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
 lib = N.load()
-dbgs = [torch.zeros(64 + 8 * nsm, dtype=torch.int64, device="cuda") for _ in range(2)]
+dbgs = [torch.zeros(64 + 32 * nsm, dtype=torch.int64, device="cuda") for _ in range(2)]
 run = lambda: step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)  # noqa: E731
 run()
 torch.cuda.synchronize()
@@ -44,7 +44,7 @@ t0 = None
 for i, d in enumerate(dbgs):
     d = d.cpu()
     sel0, sel1 = int(d[48]), int(d[49])
-    st = d[64:].view(nsm, 8)
+    st = d[64:64 + 16 * nsm].view(nsm, 16)
     t0 = sel0 if t0 is None else t0
     rel = lambda x: (x - t0) / 1e3  # noqa: E731
     col = lambda j: st[:, j][st[:, j] > 0]  # noqa: E731

@@ -16,7 +16,7 @@ bt = make_batch(B, k, V, seed=0, mode="greedy")
 step = ops.TetrisStep(B, k, V, C, mode="greedy")
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
 lib = N.load()
-dbg = torch.zeros(64 + 8 * nsm, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(64 + 32 * nsm, dtype=torch.int64, device="cuda")
 run = lambda: step.run(bt.conf, bt.lengths, bt.p, None, bt.d)  # noqa: E731
 run()
 torch.cuda.synchronize()

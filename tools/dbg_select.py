@@ -12,7 +12,7 @@ from paper_2502_15197_b200.synthetic import make_batch  # noqa: E402
 B, k, V, C = (int(x) for x in sys.argv[1:5]) if len(sys.argv) >= 5 else (1024, 16, 128256, 8192)
 bt = make_batch(B, k, V, seed=0)
 step = ops.TetrisStep(B, k, V, C)
-dbg = torch.zeros(32, dtype=torch.int64, device='cuda')
+dbg = torch.zeros(64 + 32 * torch.cuda.get_device_properties(0).multi_processor_count, dtype=torch.int64, device='cuda')
 N.load().tetris_debug_timestamps(dbg.data_ptr())
 for it in range(5):
     step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)

@@ -11,7 +11,7 @@ B = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 k, C = 16, int(sys.argv[2]) if len(sys.argv) > 2 else 131072
 g = torch.Generator(device="cuda").manual_seed(0)
 conf = (torch.rand(B, k, dtype=torch.float64, device="cuda", generator=g) ** 0.3).contiguous()
-dbg = torch.zeros(32, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(64 + 32 * torch.cuda.get_device_properties(0).multi_processor_count, dtype=torch.int64, device="cuda")
 N.load().tetris_debug_timestamps(dbg.data_ptr())
 res = ops.select(conf, C)
 for it in range(4):

@@ -1,5 +1,6 @@
 """Per-CTA %globaltimer stamps of persist_stream_kernel (slots: 0 entry, 1 after griddepcontrol.wait, 2 first copy
-issued, 3 last copy issued, 4 first stage consumed, 5 publisher done, 6 descents done) for one step of a config.
+issued, 3 last copy issued, 4 first stage consumed, 5 publisher done, 6 descents done, 7..12 the speculative / fused
+prologue) for one step of a config.
 usage: python tools/dbg_stream.py [B k V C]"""
 import sys
 from pathlib import Path
@@ -18,7 +19,7 @@ B, k, V, C = (int(x) for x in argv[:4]) if len(argv) >= 4 else (1024, 16, 128256
 bt = make_logit_batch(B, k, V, seed=0) if logits else make_batch(B, k, V, seed=0)
 step = ops.TetrisStep(B, k, V, C)
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
-dbg = torch.zeros(64 + 8 * nsm, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(64 + 32 * nsm, dtype=torch.int64, device="cuda")
 lib = N.load()
 for it in range(4):
     lib.tetris_debug_timestamps(dbg.data_ptr() if it == 3 else None)
@@ -29,14 +30,28 @@ for it in range(4):
         step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, events=evs)
     torch.cuda.synchronize()
 lib.tetris_debug_timestamps(None)
-d = dbg[64:].view(nsm, 8).cpu()
+d = dbg[64:64 + 16 * nsm].view(nsm, 16).cpu()
+cyc = dbg[64 + 16 * nsm:].view(nsm, 16).cpu()
 t0 = int(d[:, 0][d[:, 0] > 0].min())
 names = ["entry", "after wait", "first copy", "last copy", "first consumed", "publisher done", "descents done",
-         "spec prologue"]
+         "spec prologue / fused: all rows published (producer)", "fused: scores loaded", "fused: keys built",
+         "fused: ranks done", "fused: last CTA publishes", "fused: scans released"]
 for s, nme in enumerate(names):
     col = d[:, s]
     col = col[col > 0]
     if len(col) == 0:
         continue
     rel = (col - t0).double() / 1e3
-    print("%-15s min %7.2f  median %7.2f  max %7.2f us (CTAs %d)" % (nme, rel.min(), rel.median(), rel.max(), len(col)))
+    print("%-52s min %7.2f  median %7.2f  max %7.2f us (CTAs %d)" % (nme, rel.min(), rel.median(), rel.max(), len(col)))
+
+# in-CTA phase lengths in SM cycles (clock64 beside each stamp): consecutive slots of the fused prologue
+for a_, b_, nme in ((1, 8, "wait -> scores loaded"), (8, 9, "scores -> keys"), (9, 10, "keys -> ranks+verdicts"),
+                    (10, 11, "ranks -> published (last CTA)"), (11, 12, "published -> scans released (last CTA)"),
+                    (1, 7, "wait -> producer sees all rows"), (7, 2, "all rows -> first copy"),
+                    (2, 3, "first -> last copy"), (3, 5, "last copy -> publisher done"),
+                    (5, 6, "publisher done -> descents done")):
+    m = (cyc[:, a_] > 0) & (cyc[:, b_] > 0)
+    if m.sum() == 0:
+        continue
+    dc = (cyc[m, b_] - cyc[m, a_]).double()
+    print("cycles %-40s min %8.0f  median %8.0f  max %8.0f (CTAs %d)" % (nme, dc.min(), dc.median(), dc.max(), int(m.sum())))

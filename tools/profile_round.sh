@@ -21,3 +21,13 @@ timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k re
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:persist_greedy -c 1 \
   -o gpurun_out/${T}_greedy python bench.py --config cfg3g --steps 3 --warmup 3 --no-graph --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ls -la gpurun_out | grep ${T}_
+# latency-bound configs: every kernel of one step, full sets (cfg2 = BASELINE configs[1], cfg1 = configs[0])
+for c in cfg2 cfg1; do
+  timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k "$K" -c 4 \
+    -o gpurun_out/${T}_full_$c python bench.py --config $c --steps 2 --warmup 3 --no-graph --no-cpu-baseline --no-e2e > /dev/null 2>&1
+  timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c 24 --csv \
+    --log-file gpurun_out/${T}_launches_$c.csv python bench.py --config $c --steps 8 --warmup 4 --no-graph \
+    --no-cpu-baseline --no-e2e > /dev/null 2>&1
+done
+timeout -s KILL 300 python bench.py --input logits > gpurun_out/${T}_bench_logits.json 2> gpurun_out/${T}_bench_logits.err
+ls -la gpurun_out | grep ${T}_
