@@ -103,12 +103,13 @@ constexpr size_t kSlotWorkSpec = kRequestSlots + 6;      // the speculative samp
 constexpr size_t kSlotSpecCnt = kRequestSlots + 64;      // its per-request completion counters [64 + 0, 64 + 4096)
 constexpr size_t kSpecSlots = 4096;
 constexpr size_t kSlotSpecCtl = kRequestSlots + 8;       // [2]: phase-A list length, requests processed
-constexpr size_t kSlotFusedCtl = kRequestSlots + 10;     // [2]: fused step: CTAs published, scans done
+constexpr size_t kSlotFusedCtl = kRequestSlots + 10;     // [3]: fused step: CTAs counted in, scans done, epoch
 constexpr size_t kSlotSpecBitmap = kSlotSpecCnt + kSpecSlots;   // [kSpecSlots / 32]: the phase-A set
 constexpr size_t kSlotSpecList = kSlotSpecBitmap + kSpecSlots / 32;  // [kSpecSlots]: the phase-A list
 constexpr size_t kSlotGreedyKey0 = kSlotSpecList + kSpecSlots;  // [2 * 65536]: greedy row-0 argmax keys (u64)
-constexpr size_t kCounterSlots = kSlotGreedyKey0 + 2 * kRequestSlots;
-static_assert(kSlotGreedyKey0 % 2 == 0, "8-byte aligned greedy row-0 keys");
+constexpr size_t kSlotFusedReady = kSlotGreedyKey0 + 2 * kRequestSlots;  // [2 * 4096]: fused step ready words (u64)
+constexpr size_t kCounterSlots = kSlotFusedReady + 2 * 4096;
+static_assert(kSlotGreedyKey0 % 2 == 0 && kSlotFusedReady % 2 == 0, "8-byte aligned greedy keys / ready words");
 constexpr size_t kGselScratchBytes = 32 * 1024;  // grid selector: radix histograms, barrier words, CTA totals
 static_assert(kSlotGridGen == kSlotGridCount + 1, "grid_barrier reads the generation at bar + 1");
 static_assert(kSlotWorkCounter == kSlotGridCount + 2 && (kSlotWorkCounter % 2) == 0,

@@ -20,6 +20,9 @@
 namespace tetris {
 
 constexpr int kFusedMaxRpt = 8;  // rows per thread in the scans: B_sel <= kFusedMaxCells <= 8 * 256
+// the key of padding and of cells past a row's length: above every real key (real keys of scores in [0, 1] lie in
+// [0x400F.., 0x7FFF..]), and still above them after the +1 of the rank test below
+constexpr uint64_t kPadKey = 0xFFFFFFFFFFFFFFFEull;
 
 __device__ __forceinline__ void fused_bar(int nt) { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); }
 
@@ -53,18 +56,18 @@ struct FusedView {
 
 __host__ __device__ inline size_t fused_scratch_bytes(int B_sel, int k, int G) {
   const int KS = k | 1, nown = (B_sel + G - 1) / G;
-  return (size_t)B_sel * KS * 8 + (size_t)B_sel * 4 + (size_t)nown * k * 5;
+  return (size_t)(((size_t)B_sel * KS + 1) & ~(size_t)1) * 8 + (size_t)B_sel * 4 + (size_t)nown * k * 5;
 }
 
 __device__ inline FusedView fused_view(const FusedSel& f, int k, uint8_t* smem) {
   FusedView v;
   const int G = gridDim.x, g = blockIdx.x, Bs = f.B_sel;
   v.KS = k | 1;
-  v.Np = Bs * v.KS;
+  v.Np = Bs * v.KS;  // the array holds (Np + 1) & ~1 keys: 16-byte pairs, an odd Np padded with kPadKey
   v.nown = g < Bs ? (Bs - 1 - g) / G + 1 : 0;
   v.ncell = v.nown * k;
   v.keys = reinterpret_cast<uint64_t*>(smem);
-  v.lens = reinterpret_cast<int*>(v.keys + v.Np);
+  v.lens = reinterpret_cast<int*>(v.keys + ((v.Np + 1) & ~1));
   v.rk = reinterpret_cast<uint32_t*>(v.lens + Bs);
   v.verd = reinterpret_cast<uint8_t*>(v.rk + v.ncell);
   return v;
@@ -94,15 +97,18 @@ __device__ inline void fused_stage(const FusedSel& f, int k, const FusedView& v,
   for (int c = pt; c < v.ncell; c += nt) v.rk[c] = 0u;
 }
 
-// phase 1: per row, prefix products left to right (selector.py:104-108), envelope, keys.  A row's values are read
-// from shared memory all at once (up to 16), then the dependent fp64 chain runs from registers.
-__device__ __forceinline__ void key_step(double x, int j, double& cum, double& env, uint64_t& key, uint32_t& bad) {
-  if (!(x >= 0.0 && x <= 1.0)) bad |= TETRIS_ST_BAD_VALUE;  // accept_model.py:55-59
-  cum = __dmul_rn(cum, x);
-  env = (j == 0 || cum < env) ? cum : env;
-  key = desc_key(env);
+// phase 1: per row, prefix products left to right (selector.py:104-108) and keys.  Scores are validated into [0, 1]
+// (accept_model.py:55-59), so each product is <= the one before it (RN is monotone) and the prefix-min envelope of
+// select1_kernel is the product itself; the key is desc_key's value for a non-negative double, ~(bits | sign)
+// (which also maps -0.0 onto +0.0).  A row's values are read at once (KM unrolled), then the fp64 chain runs from
+// registers.  Invalid rows only raise TETRIS_ST_BAD_VALUE (the reference raises ValueError).
+__device__ __forceinline__ bool score_ok(uint64_t b) { return b <= 0x3FF0000000000000ull || b == 0x8000000000000000ull; }
+__device__ __forceinline__ uint64_t key_of_nonneg(double v) {
+  return ~((uint64_t)__double_as_longlong(v) | 0x8000000000000000ull);
 }
 
+// (rolled loop: this code runs once per launch, and every launch starts with a cold instruction cache — measured
+// ~140 cycles per KB of straight-line code on B200, tools/micro/icache.cu — so compact code beats unrolled code here)
 __device__ inline void fused_keys(const FusedSel& f, int k, const FusedView& v, int pt, int nt, uint32_t* status) {
   const int KS = v.KS;
   uint32_t bad = 0;
@@ -114,52 +120,139 @@ __device__ inline void fused_keys(const FusedSel& f, int k, const FusedView& v, 
       v.lens[r] = L;
     }
     uint64_t* row = v.keys + r * KS;
-    double cum = 1.0, env = 0.0;
-    if (KS <= 17) {
-      double x[16];
+    double cum = 1.0;
+    if (KS <= 9) {  // k <= 8: the row's values at once, then a branch-free chain (1.0 past the length)
+      uint64_t x[9];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) x[j] = j < L ? __longlong_as_double((long long)row[j]) : 0.0;
+      for (int j = 0; j < 9; ++j) x[j] = j < L ? row[j] : 0x3FF0000000000000ull;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        uint64_t key = ~0ull;
-        if (j < L) key_step(x[j], j, cum, env, key, bad);
-        if (j < KS) row[j] = key;
+      for (int j = 0; j < 9; ++j) {
+        bad |= score_ok(x[j]) ? 0u : TETRIS_ST_BAD_VALUE;
+        cum = __dmul_rn(cum, __longlong_as_double((long long)x[j]));
+        if (j < KS) row[j] = j < L ? key_of_nonneg(cum) : kPadKey;
       }
-      if (KS == 17) row[16] = ~0ull;  // k == 16: the padding column
     } else {
+#pragma unroll 1
       for (int j = 0; j < KS; ++j) {
-        uint64_t key = ~0ull;
-        if (j < L) key_step(__longlong_as_double((long long)row[j]), j, cum, env, key, bad);
+        uint64_t key = kPadKey;
+        if (j < L) {
+          const uint64_t xb = row[j];
+          if (!score_ok(xb)) bad |= TETRIS_ST_BAD_VALUE;
+          cum = __dmul_rn(cum, __longlong_as_double((long long)xb));
+          key = key_of_nonneg(cum);
+        }
         row[j] = key;
       }
     }
   }
+  if (pt == 0 && (v.Np & 1)) v.keys[v.Np] = kPadKey;
   set_status(status, bad);
 }
 
-// phase 2: rank of each own cell m = #{o : key_o < key_m, or key_o == key_m and o < m} over every cell; the
-// participants split (cell, key slice) pairs, lanes of a warp on consecutive cells of one slice (broadcast reads)
-__device__ inline void fused_ranks(int k, const FusedView& v, int pt, int nt) {
-  if (v.ncell == 0) return;
+// phase 2: rank of each own cell m = #{o : key_o < key_m, or key_o == key_m and o < m} over every cell.  A group of
+// warps per own row; each thread holds 8 of the row's cell keys in registers and walks a strided slice of all the
+// other keys (coalesced loads) — keys before the row count when <= a cell's key, keys after it when < (the tie rule
+// by index); within the row, cell j is preceded by exactly its j predecessors.  Warp sums (REDUX) go to the cells'
+// counters.  ~3 instructions per (key, cell) pair, no shared-memory bottleneck.
+// n + (a >= b) for unsigned 64-bit a, b: the borrow of a - b through the carry chain (sub.cc / subc.cc produce the
+// carry of a + ~b + 1, i.e. 1 exactly when a >= b), added with addc — 3 instructions, no predicate, no select
+__device__ __forceinline__ uint32_t add_ge(uint32_t n, uint64_t a, uint64_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .u32 t0, t1;\n\t"
+      "sub.cc.u32 t0, %1, %3;\n\t"
+      "subc.cc.u32 t1, %2, %4;\n\t"
+      "addc.u32 %0, %5, 0;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)), "r"(n));
+  return r;
+}
+
+// small non-negative integer quotient a / b (a, b <= 1024) without the integer-division subroutine: the float quotient
+// is correctly rounded and at least 1/b away from the next integer, so truncation is exact
+__device__ __forceinline__ int small_div(int a, int b) { return (int)__fdiv_rn((float)a, (float)b); }
+
+__device__ inline void fused_ranks_rows(const FusedView& v, int k, int pt, int nt) {
+  constexpr int KM = 8;  // cells per pass (a row of k cells takes ceil(k / 8) passes)
+  if (v.nown == 0) return;
+  const int W = nt >> 5, wid = pt >> 5, lane = pt & 31;
+  const int wpr = v.nown <= W ? small_div(W, v.nown) : 1;  // warps per row
+  const int rq = small_div(wid, wpr), wr = wid - rq * wpr;
+  const int rpp = small_div(W, wpr);  // rows per pass
+  const int sub = wr * 32 + lane, nsub = wpr * 32;
   const int G = gridDim.x, g = blockIdx.x, KS = v.KS, Np = v.Np;
-  const int S = v.ncell >= nt ? 1 : nt / v.ncell;
-  for (int wi = pt; wi < v.ncell * S; wi += nt) {
-    const int c = wi % v.ncell, s = wi / v.ncell;
-    const int oi = c / k, j = c - oi * k, r = g + oi * G;
-    if (j >= v.lens[r]) continue;
-    const int m = r * KS + j;
-    const uint64_t km = v.keys[m];
-    const int s0 = Np * s / S, s1 = Np * (s + 1) / S;  // Np * S <= 2 * kFusedMaxCells * 1024
-    uint32_t n = 0;
-    const int e1 = min(s1, m);
-    int o = s0;
-#pragma unroll 4
-    for (; o < e1; ++o) n += v.keys[o] <= km ? 1u : 0u;
-#pragma unroll 4
-    for (o = max(s0, m + 1); o < s1; ++o) n += v.keys[o] < km ? 1u : 0u;
-    if (n) atomicAdd(&v.rk[c], n);
+  // after the warp reduction below, lane l holds the total of cell ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 +
+  // ((l >> 2) & 1) of the pass
+  const int my_cell = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  for (int oi = rq; oi < v.nown; oi += rpp) {
+    const int r = g + oi * G, L = v.lens[r], rs = r * KS, re = rs + KS;
+#pragma unroll 1
+    for (int j0 = 0; j0 < L; j0 += KM) {
+      // before the row: count key_o <= key_m (key_m >= key_o); after it: key_o < key_m (key_m - 1 >= key_o); real
+      // keys are >= 0x400F.., so key_m - 1 does not wrap
+      uint64_t km[KM], km1[KM];
+      uint32_t n[KM];
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        km[j] = j0 + j < L ? v.keys[rs + j0 + j] : 0ull;
+        km1[j] = km[j] - 1;
+        n[j] = 0u;
+      }
+      int o = sub;
+      for (; o + 3 * nsub < rs; o += 4 * nsub) {  // 4 loads in flight
+        uint64_t x[4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) x[y] = v.keys[o + y * nsub];
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int j = 0; j < KM; ++j) n[j] = add_ge(n[j], km[j], x[y]);
+      }
+      for (; o < rs; o += nsub) {
+        const uint64_t x = v.keys[o];
+#pragma unroll
+        for (int j = 0; j < KM; ++j) n[j] = add_ge(n[j], km[j], x);
+      }
+      o = re + sub;
+      for (; o + 3 * nsub < Np; o += 4 * nsub) {
+        uint64_t x[4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) x[y] = v.keys[o + y * nsub];
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int j = 0; j < KM; ++j) n[j] = add_ge(n[j], km1[j], x[y]);
+      }
+      for (; o < Np; o += nsub) {
+        const uint64_t x = v.keys[o];
+#pragma unroll
+        for (int j = 0; j < KM; ++j) n[j] = add_ge(n[j], km1[j], x);
+      }
+      // warp reduce-scatter of the 8 counters (xor 16, 8, 4 halve the set; xor 2, 1 finish the sum)
+      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t send = h16 ? n[j] : n[j + 4], keep = h16 ? n[j + 4] : n[j];
+        n[j] = keep + __shfl_xor_sync(kFull, send, 16);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t send = h8 ? n[j] : n[j + 2], keep = h8 ? n[j + 2] : n[j];
+        n[j] = keep + __shfl_xor_sync(kFull, send, 8);
+      }
+      {
+        const uint32_t send = h4 ? n[0] : n[1], keep = h4 ? n[1] : n[0];
+        n[0] = keep + __shfl_xor_sync(kFull, send, 4);
+      }
+      n[0] += __shfl_xor_sync(kFull, n[0], 2);
+      n[0] += __shfl_xor_sync(kFull, n[0], 1);
+      const int j = j0 + my_cell;
+      const uint32_t t = n[0] + (wr == 0 ? (uint32_t)j : 0u);  // cell j's own-row predecessors, counted once
+      if ((lane & 3) == 0 && j < L && t) atomicAdd(&v.rk[oi * k + j], t);
+    }
   }
 }
+
+__device__ inline void fused_ranks(int k, const FusedView& v, int pt, int nt) { fused_ranks_rows(v, k, pt, nt); }
 
 // the window of own row oi (after phase 2)
 __device__ __forceinline__ int fused_window(const FusedSel& f, int k, const FusedView& v, int oi) {
@@ -188,7 +281,7 @@ __device__ __forceinline__ void fused_load_windows(const FusedSel& f, int pt, in
   for (int i = 0; i < kFusedMaxRpt; ++i) wr[i] = (i < rpt && r0 + i < Bs) ? __ldcg(f.windows + r0 + i) : 0;
 }
 
-__device__ inline void fused_win_scan(const FusedSel& f, const FusedView& v, int pt, int nt, long long* tmp,
+__device__ inline void fused_win_scan(const FusedSel& f, int k, int pt, int nt, long long* tmp,
                                       const int (&wr)[kFusedMaxRpt]) {
   const int Bs = f.B_sel, rpt = (Bs + nt - 1) / nt, r0 = pt * rpt;
   long long pk = 0;
@@ -196,7 +289,9 @@ __device__ inline void fused_win_scan(const FusedSel& f, const FusedView& v, int
   for (int i = 0; i < kFusedMaxRpt; ++i) {
     const int r = r0 + i;
     if (i < rpt && r < Bs) {
-      const int w = wr[i], L = v.lens[r];
+      int L = f.len ? __ldg(f.len + r) : k;  // (clamped as the keys phase did)
+      L = L < 0 ? 0 : (L > k ? k : L);
+      const int w = wr[i];
       pk += (long long)w | ((long long)(w - ((w == L && L > 0) ? 1 : 0)) << 24) | ((long long)(L > 0) << 48);
     }
   }

@@ -67,7 +67,8 @@ struct FusedSel {
   long long* rowinfo;   // [R][2]
   float* rowlse;        // [R][2] logits form
   int32_t* offsets;     // [R + 1]
-  int* ctl;             // [2] rows published (CTAs), scans done (zero, left at zero)
+  int* ctl;             // [3] CTAs counted in, scans done (zero, left at zero), the last launch's epoch
+  unsigned long long* ready;  // [R] per-request ready words (fused_ready_word), self-resetting by epoch
 };
 constexpr int kFusedMaxCells = 2048;
 

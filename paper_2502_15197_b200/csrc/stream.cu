@@ -162,6 +162,20 @@ __device__ __forceinline__ void row_lane(const void* row, int64_t e, int V, floa
   }
 }
 
+// Diagnostics for tools/micro/descent.cu only (-DTETRIS_DESCENT_PROBE): clock64 at points of the descent, lane 0.
+#ifdef TETRIS_DESCENT_PROBE
+__device__ long long g_probe[4096][8];
+#define DESCENT_PROBE(i)                                                                                          \
+  do {                                                                                                             \
+    if ((threadIdx.x & 31) == 0)                                                                                   \
+      g_probe[(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & 4095][i] = clock64();                         \
+  } while (0)
+#else
+#define DESCENT_PROBE(i) \
+  do {                   \
+  } while (0)
+#endif
+
 // descent below the warp level, reading the warp run from global memory (all 32 lanes, T uniform)
 template <bool RES, bool BF>
 __device__ int descend_global(const void* __restrict__ P, const void* __restrict__ Q, int64_t e0, int V, int lane,
@@ -173,6 +187,10 @@ __device__ int descend_global(const void* __restrict__ P, const void* __restrict
     row_lane<BF>(P, e0 + s * kSegElems + lane * kLaneElems, V, lp, pv[s]);
     if (RES) row_lane<BF>(Q, e0 + s * kSegElems + lane * kLaneElems, V, lq, qv[s]);
   }
+#ifdef TETRIS_DESCENT_PROBE
+  if (pv[0][0] == -1.f) G[0] = 0.0;  // the loads are in
+#endif
+  DESCENT_PROBE(4);
 #pragma unroll
   for (int s = 0; s < kWarpSegs; ++s) {
     double wl[8];
@@ -180,6 +198,7 @@ __device__ int descend_global(const void* __restrict__ P, const void* __restrict
     for (int i = 0; i < 8; ++i) wl[i] = RES ? w_res((double)pv[s][i], (double)qv[s][i]) : w_plain((double)pv[s][i]);
     G[s] = seg_sum(fold8(wl));
   }
+  DESCENT_PROBE(5);
   const int s = seq_find(G, kWarpSegs, T);
   if (s < 0) return -1;
   double w[8];  // the chosen segment's weights, recomputed from the loaded lanes (identical arithmetic)
@@ -211,6 +230,7 @@ __device__ int descend_global(const void* __restrict__ P, const void* __restrict
       g += 1 << t;
     }
   }
+  DESCENT_PROBE(6);
   double Tl = T;
   const int li_own = seq_find(w, 8, Tl);
   const int li = __shfl_sync(kFull, li_own, g);
@@ -223,6 +243,7 @@ __device__ int descend_global(const void* __restrict__ P, const void* __restrict
 template <bool BF>
 __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane, const double* chunk_sums,
                                  const double* warp_sums) {
+  DESCENT_PROBE(0);
   const int nch = a.nch;
   const long long prow = __ldcg(a.prow + (int64_t)b * a.row_stride);
   const long long qrow = a.qrow ? __ldcg(a.qrow + (int64_t)b * a.row_stride) : -1;
@@ -230,54 +251,43 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
   const float lq = (BF && qrow >= 0) ? a.lse_q[qrow] : 0.f;
   const double* cs = chunk_sums + (int64_t)b * nch;
   const double* ws = warp_sums + (int64_t)b * nch * kChunkWarps;
-  // nch <= 16: all nch * 8 warp sums in ONE round trip (lane l holds sums l, l + 32, l + 64, l + 96: chunk c's eight
-  // are register c / 4, lanes 8 (c % 4) .. + 7); the chunk sums are re-folded from them left to right (the
-  // publisher's exact arithmetic).  Larger rows: chunk sums first, the chosen chunk's warp sums second.
+  // nch <= 16: every sum the descent needs in ONE round trip — the chunk sums (lane c holds chunk c) and the
+  // nch * 8 warp sums (lane l holds sums l, l + 32, l + 64, l + 96: chunk c's eight are register c / 4, lanes
+  // 8 (c % 4) .. + 7).  Larger rows: chunk sums (two per lane) first, the chosen chunk's warp sums second.
   const bool one_trip = nch <= 16;
   double wv[4];
-  double s_lo = 0.0, s_hi = 0.0;
+  double s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
+  double s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
   if (one_trip) {
 #pragma unroll
     for (int x = 0; x < 4; ++x) wv[x] = lane + 32 * x < nch * kChunkWarps ? __ldcg(ws + lane + 32 * x) : 0.0;
-  } else {
-    s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
-    s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
   }
-  // accepted-prefix tokens of the compacted stream, in parallel with the loads above
-  int acc = 0, off = 0, end = 0;
+  // accepted-prefix tokens of the compacted stream: every load of the descent's first round trip goes out together
+  // (the sums above, the request's counts and uniform, its first 32 drafted tokens)
+  int acc = 0, off = 0, end = 0, d0 = 0;
   if (a.accepted) {
     acc = __ldcg(a.accepted + b);
     off = __ldcg(a.offsets + b);
     end = __ldcg(a.offsets + b + 1);
-    for (int j = lane; j < acc && off + j < end; j += 32) a.tokens[off + j] = a.d[(int64_t)b * a.k + j];
+    d0 = lane < a.k ? __ldg(a.d + (int64_t)b * a.k + lane) : 0;
   }
-  const double u = a.u[b];
+  const double u = __ldg(a.u + b);
+  if (a.accepted)
+    for (int j = lane; j < acc && off + j < end; j += 32) a.tokens[off + j] = j < 32 ? d0 : a.d[(int64_t)b * a.k + j];
   uint32_t bad = 0;
   if (!(u >= 0.0 && u < 1.0)) bad |= TETRIS_ST_BAD_UNIFORM;
-  if (one_trip) {
-    double t4[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      double S = 0.0;  // lane l: the sum of chunk 4x + l / 8
-#pragma unroll
-      for (int w = 0; w < kChunkWarps; ++w) S = S + __shfl_sync(kFull, wv[x], (lane & 24) + w);
-      t4[x] = __shfl_sync(kFull, S, 8 * (lane & 3));  // lane l: the sum of chunk 4x + l % 4
-    }
-    const int xl = (lane >> 2) & 3;  // lane c < 16 takes chunk c = 4 * (c / 4) + c % 4
-    s_lo = xl == 0 ? t4[0] : xl == 1 ? t4[1] : xl == 2 ? t4[2] : t4[3];
-    if (lane >= nch) s_lo = 0.0;
-  }
+  DESCENT_PROBE(1);
   // mass = chunk sums folded left to right (every lane holds the same value)
   double mass = 0.0;
   for (int c = 0; c < nch; ++c) mass = mass + __shfl_sync(kFull, c < 32 ? s_lo : s_hi, c & 31);
   int tok = -1;
+  if (lane == 0 && b == (int)blockIdx.x) gstamp(a, 15);  // diagnostics: the first round trip is in
   if (mass > 0.0) {
     double T = u * mass;
     // chunk level (left to right), then warp level of the chosen chunk
     double P = 0.0;
     int cc = -1, last_pos = -1;
-    for (int c = 0; c < nch; ++c) {
-      const double v = __shfl_sync(kFull, c < 32 ? s_lo : s_hi, c & 31);
+    auto step = [&](int c, double v) {
       if (v > 0.0) last_pos = c;
       if (cc < 0) {
         const double Pn = P + v;
@@ -287,11 +297,13 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
         }
         P = Pn;
       }
-    }
+    };
+    for (int c = 0; c < nch; ++c) step(c, __shfl_sync(kFull, c < 32 ? s_lo : s_hi, c & 31));
     if (cc < 0) {
       cc = last_pos;
       T = __longlong_as_double(0x7ff0000000000000ll);
     }
+    DESCENT_PROBE(2);
     // the 8 warp sums of the chosen chunk (from lane cc's registers, or lanes 0..7 load them, then broadcast)
     double Wc[kChunkWarps];
     if (one_trip) {
@@ -305,6 +317,7 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
       for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __shfl_sync(kFull, wl, w);
     }
     const int ww = seq_find(Wc, kChunkWarps, T);
+    DESCENT_PROBE(3);
     if (cc >= 0 && ww >= 0) {
       const int64_t e0 = (int64_t)cc * kChunkElems + ww * kWarpElems;
       const void* Pr = BF ? (const void*)(a.zp + prow * (int64_t)a.V) : (const void*)(a.p + prow * (int64_t)a.V);
@@ -314,6 +327,7 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
                 : descend_global<false, BF>(Pr, nullptr, e0, a.V, lane, T, lp, lq);
     }
   }
+  DESCENT_PROBE(7);
   if (tok < 0) bad |= TETRIS_ST_DEGENERATE;
   if (lane == 0) {
     a.out_idx[b] = tok;
@@ -353,12 +367,9 @@ __device__ __forceinline__ void issue_item(const StreamArgs& a, PersistShared& s
 // Deeper producer schedule for the logits form (its items are half as many bytes, so the claim / row-lookup round
 // trips must overlap more): C claims on the work counter and L row lookups in flight, kept in shift registers.
 // req(i) -> request of item i; rows(b, prow, qrow, lse_p, lse_q).  Returns the next stage index.
-// gate != nullptr (fused step): the claims go out first, then the row lookups wait until every CTA has published
-// its rows (*gate == gridDim.x).
 template <bool BF, int L, int C, typename Req, typename Rows>
 __device__ int stream_deep(const StreamArgs& a, PersistShared& sh, uint8_t* stage_mem, int t, long long total,
-                           unsigned long long* work, int phase, uint64_t pol, Req req, Rows rows,
-                           const int* gate = nullptr) {
+                           unsigned long long* work, int phase, uint64_t pol, Req req, Rows rows) {
   constexpr int D = L + C;
   long long ci[D], pr[D], qr[D];
   float lp[D], lq[D];
@@ -368,10 +379,6 @@ __device__ int stream_deep(const StreamArgs& a, PersistShared& sh, uint8_t* stag
     pr[d] = 0;
     qr[d] = -1;
     lp[d] = lq[d] = 0.f;
-  }
-  if (gate) {
-    spin_acquire_geq(gate, (int)gridDim.x);
-    gstamp(a, 7);
   }
 #pragma unroll
   for (int d = 0; d < L; ++d)
@@ -426,85 +433,146 @@ __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stag
 // rejection among the selected positions (accept_model.py:309-313, sim_engine.py:397-401) from verdicts gathered in
 // the selection's first round trip, the row to resample from, and — in the last CTA to publish — the compaction
 // offsets.  The producers wait for every CTA's rows (ctl[0] == G), the descents for the scans (ctl[1]).
-// An own cell's accept-test inputs, loaded raw in one phase and turned into the verdict in a later one, so the
-// dependent gathers overlap the key and rank phases instead of stalling the first.
-struct FusedCell {
-  int t;        // drafted token
-  double u;     // accept uniform
-  float pv, qv; // p[lr][j][t], q[lr][j][t] (fp32 form) / lse of those rows (logits form)
-  uint32_t zz;  // logits form: the two bf16 logits (p low, q high)
-};
-constexpr int kFusedCellsPerThread = 4;  // own cells <= B_sel * k <= kFusedMaxCells <= 4 * 576
+// A request's ready word (fused step): bits 63..44 the launch's epoch (low 20 bits), 43..22 its p row, 21..0 its q row
+// + 1 (0: bonus row).  Rows < 2^22 hold: R * (k + 1) <= 2 * kFusedMaxCells.  Epochs make the words self-resetting:
+// a word from an earlier launch never carries this launch's epoch.
+__device__ __forceinline__ unsigned long long fused_ready_word(uint32_t epoch, long long prow, long long qrow) {
+  return ((unsigned long long)(epoch & 0xFFFFFu) << 44) | ((unsigned long long)prow << 22) |
+         (unsigned long long)(qrow + 1);
+}
+__device__ __forceinline__ bool fused_ready(unsigned long long w, uint32_t epoch) {
+  return (uint32_t)(w >> 44) == (epoch & 0xFFFFFu);
+}
+__device__ __forceinline__ unsigned long long fused_wait_ready(const unsigned long long* p, uint32_t epoch) {
+  for (;;) {
+    const unsigned long long w = __ldcg(p);
+    if (fused_ready(w, epoch)) return w;
+    __nanosleep(32);
+  }
+}
+
+// The last CTA to count itself in (ctl[0]) writes win_offsets / PolicyStats (selector.py:150-170) and the compaction
+// offsets from every CTA's published rows, then raises ctl[1] (the descents wait for it).  Run by the 16 consumer
+// warps after the producer has started streaming, so it reads global memory only (the prologue's shared scratch is
+// the stage ring by then).
+template <bool BF>
+__device__ void fused_scans(const StreamArgs& a, int pt, int nt) {
+  const FusedSel& f = a.fs;
+  __shared__ int s_last;
+  __shared__ long long s_tmp[33];
+  if (fused_publish(f, pt, nt, &s_last)) {
+    if (pt == 0) gstamp(a, 11);
+    int wr[kFusedMaxRpt], nr[kFusedMaxRpt];
+    fused_load_windows(f, pt, nt, wr);  // both scans' inputs in one round trip
+    const int R = a.R, rpl = (R + nt - 1) / nt, l0 = pt * rpl;
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) {
+      const int lr = l0 + i;
+      nr[i] = (i < rpl && lr < R) ? __ldcg(f.accepted + lr) + 1 : 0;
+      if (f.cap && i < rpl && lr < R) nr[i] = min(nr[i], max(__ldg(f.cap + lr), 0));
+    }
+    fused_win_scan(f, a.k, pt, nt, s_tmp, wr);
+    long long my = 0;
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) my += nr[i];
+    long long etot;
+    long long eex = fused_excl_scan<long long>(my, s_tmp, etot, pt, nt);
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) {
+      const int lr = l0 + i;
+      if (i < rpl && lr < R) {
+        f.offsets[lr] = (int32_t)eex;
+        eex += nr[i];
+      }
+    }
+    if (pt == 0) f.offsets[R] = (int32_t)etot;
+    fused_release_done(f, pt, nt);
+    if (pt == 0) gstamp(a, 12);
+  }
+}
+
+// The own cells' accept verdicts (verify_token, accept_model.py:309-313) by ONE warp — the publisher's, idle until
+// streaming starts — while the other 17 warps build keys and ranks: its two dependent round trips (drafted tokens
+// and uniforms, then the p / q gathers) overlap the selection instead of stalling it.  Verdict byte: bit0 accept,
+// bit1 drafted token outside the vocabulary, bit2 uniform outside [0, 1).  4 cells per lane per round.
+template <bool BF>
+__device__ void fused_verdicts(const StreamArgs& a, const FusedView& v, int lane) {
+  const FusedSel& f = a.fs;
+  const int k = a.k, G = gridDim.x, g = blockIdx.x;
+  for (int c0 = 0; c0 < v.ncell; c0 += 128) {
+    int64_t ce[4];
+    int t[4];
+    double u[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int c = c0 + lane + 32 * x;
+      ce[x] = -1;
+      if (c < v.ncell) {
+        const int oi = c / k, j = c - oi * k, lr = g + oi * G - f.row0;
+        if (lr >= 0 && lr < a.R) ce[x] = (int64_t)lr * k + j;
+      }
+      t[x] = ce[x] >= 0 ? __ldg(a.d + ce[x]) : 0;
+      u[x] = ce[x] >= 0 ? __ldg(f.u_acc + ce[x]) : 0.0;
+    }
+    double m[4], sq[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      m[x] = sq[x] = 0.0;
+      if (ce[x] >= 0 && t[x] >= 0 && t[x] < a.V) {
+        const int64_t e = ce[x], lr = e / k, prow = lr * (k + 1) + (e - lr * k);
+        m[x] = gather_p(a, prow, t[x]);
+        sq[x] = gather_q(a, e, t[x]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int c = c0 + lane + 32 * x;
+      if (c >= v.ncell) continue;
+      uint8_t vb = 0;
+      if (ce[x] >= 0) {
+        vb = (u[x] >= 0.0 && u[x] < 1.0) ? 0 : 4;
+        if (t[x] < 0 || t[x] >= a.V)
+          vb |= 2;
+        else
+          vb |= ((sq[x] <= m[x]) || (u[x] < m[x] / sq[x])) ? 1 : 0;
+      }
+      v.verd[c] = vb;
+    }
+  }
+}
 
 template <bool BF>
 __device__ void fused_select(const StreamArgs& a, uint8_t* smem) {
   const FusedSel& f = a.fs;
   const int tid = threadIdx.x, NT = blockDim.x, G = gridDim.x, g = blockIdx.x, k = a.k;
+  const int NP = NT - 32;  // the selection's participants: warps 0 .. 16; warp 17 gathers the verdicts
   const FusedView v = fused_view(f, k, smem);
-  __shared__ int s_last;
-  __shared__ long long s_tmp[33];
-  // phase 0: scores + lengths (shared), the own cells' drafted tokens and uniforms (registers)
-  FusedCell cell[kFusedCellsPerThread];
-  int64_t ce[kFusedCellsPerThread];  // (lr * k + j) of the cell, -1: not a local drafted cell
-#pragma unroll
-  for (int x = 0; x < kFusedCellsPerThread; ++x) {
-    const int c = tid + x * NT;
-    ce[x] = -1;
-    if (c < v.ncell) {
-      const int oi = c / k, j = c - oi * k, lr = g + oi * G - f.row0;
-      if (lr >= 0 && lr < a.R) ce[x] = (int64_t)lr * k + j;
-    }
-    cell[x].t = ce[x] >= 0 ? __ldg(a.d + ce[x]) : 0;
-    cell[x].u = ce[x] >= 0 ? __ldg(f.u_acc + ce[x]) : 0.0;
+  __shared__ uint32_t s_epoch;
+  if (tid == 0) s_epoch = (uint32_t)__ldcg(f.ctl + 2) + 1u;  // this launch's epoch (the previous grid is complete)
+  if (tid >= NP) {
+    fused_verdicts<BF>(a, v, tid & 31);
+  } else {
+    fused_stage(f, k, v, tid, NP);
+    fused_bar(NP);
+    if (tid == 0) gstamp(a, 8);
+    fused_keys(f, k, v, tid, NP, a.status);
+    fused_bar(NP);
+    if (tid == 0) gstamp(a, 9);
+    fused_ranks(k, v, tid, NP);
+#ifdef TETRIS_FUSED_TWICE  // A/B timing only (wrong results): each phase again, warm, stamped into slots 11 / 12
+    fused_bar(NP);
+    if (tid == 0) gstamp(a, 10);
+    fused_keys(f, k, v, tid, NP, a.status);
+    fused_bar(NP);
+    if (tid == 0) gstamp(a, 11);
+    fused_ranks(k, v, tid, NP);
+    fused_bar(NP);
+    if (tid == 0) gstamp(a, 12);
+#endif
   }
-  fused_stage(f, k, v, tid, NT);
-  fused_bar(NT);
-  if (tid == 0) gstamp(a, 8);
-  // phase 1: the gathers p[lr][j][t], q[lr][j][t] go out, then the keys are built while they are in flight
-#pragma unroll
-  for (int x = 0; x < kFusedCellsPerThread; ++x) {
-    const int t = cell[x].t;
-    cell[x].zz = 0u;
-    cell[x].pv = cell[x].qv = 0.f;
-    if (ce[x] >= 0 && t >= 0 && t < a.V) {
-      const int64_t e = ce[x], lr = e / k, prow = lr * (k + 1) + (e - lr * k);
-      if (BF) {
-        cell[x].zz = (uint32_t)__ldg(a.zp + prow * a.V + t) | ((uint32_t)__ldg(a.zq + e * a.V + t) << 16);
-        cell[x].pv = __ldg(a.lse_p + prow);
-        cell[x].qv = __ldg(a.lse_q + e);
-      } else {
-        cell[x].pv = __ldg(a.p + prow * a.V + t);
-        cell[x].qv = __ldg(a.q + e * a.V + t);
-      }
-    }
-  }
-  fused_keys(f, k, v, tid, NT, a.status);
-  fused_bar(NT);
-  if (tid == 0) gstamp(a, 9);
-  // phase 2: ranks; then the verdicts (verify_token, accept_model.py:309-313) of the own cells.  Verdict byte: bit0
-  // accept, bit1 drafted token outside the vocabulary, bit2 uniform outside [0, 1)
-  fused_ranks(k, v, tid, NT);
-#pragma unroll
-  for (int x = 0; x < kFusedCellsPerThread; ++x) {
-    const int c = tid + x * NT;
-    if (c >= v.ncell) continue;
-    uint8_t vb = 0;
-    if (ce[x] >= 0) {
-      const double u = cell[x].u;
-      const int t = cell[x].t;
-      vb = (u >= 0.0 && u < 1.0) ? 0 : 4;
-      if (t < 0 || t >= a.V) {
-        vb |= 2;
-      } else {
-        const double m = BF ? (double)prob_from_logit(cell[x].zz & 0xffffu, cell[x].pv) : (double)cell[x].pv;
-        const double s = BF ? (double)prob_from_logit(cell[x].zz >> 16, cell[x].qv) : (double)cell[x].qv;
-        vb |= ((s <= m) || (u < m / s)) ? 1 : 0;
-      }
-    }
-    v.verd[c] = vb;
-  }
-  fused_bar(NT);
+  __syncthreads();
   if (tid == 0) gstamp(a, 10);
+  const uint32_t epoch = s_epoch;
   // phase 3: the own rows' windows, first rejection (sim_engine.py:397-401), row to resample from
   for (int oi = tid; oi < v.nown; oi += NT) {
     const int r = g + oi * G;
@@ -529,39 +597,10 @@ __device__ void fused_select(const StreamArgs& a, uint8_t* smem) {
         f.rowlse[2 * (int64_t)lr] = __ldg(a.lse_p + (int64_t)lr * (k + 1) + acc);
         f.rowlse[2 * (int64_t)lr + 1] = acc < w ? __ldg(a.lse_q + (int64_t)lr * k + acc) : 0.f;
       }
+      // the request's ready word: this launch's epoch + both rows, in one 8-byte store the producers poll
+      __stcg(f.ready + lr, fused_ready_word(epoch, (long long)lr * (k + 1) + acc, acc < w ? (long long)lr * k + acc : -1));
       set_status(a.status, vbad);
     }
-  }
-  if (fused_publish(f, tid, NT, &s_last)) {
-    if (tid == 0) gstamp(a, 11);
-    // the last CTA to publish: windows -> win_offsets + PolicyStats; emitted counts -> offsets (compact's contract);
-    // both scans' inputs in one round trip
-    int wr[kFusedMaxRpt], nr[kFusedMaxRpt];
-    fused_load_windows(f, tid, NT, wr);
-    const int R = a.R, rpl = (R + NT - 1) / NT, l0 = tid * rpl;
-#pragma unroll
-    for (int i = 0; i < kFusedMaxRpt; ++i) {
-      const int lr = l0 + i;
-      nr[i] = (i < rpl && lr < R) ? __ldcg(f.accepted + lr) + 1 : 0;
-      if (f.cap && i < rpl && lr < R) nr[i] = min(nr[i], max(__ldg(f.cap + lr), 0));
-    }
-    fused_win_scan(f, v, tid, NT, s_tmp, wr);
-    long long my = 0;
-#pragma unroll
-    for (int i = 0; i < kFusedMaxRpt; ++i) my += nr[i];
-    long long etot;
-    long long eex = fused_excl_scan<long long>(my, s_tmp, etot, tid, NT);
-#pragma unroll
-    for (int i = 0; i < kFusedMaxRpt; ++i) {
-      const int lr = l0 + i;
-      if (i < rpl && lr < R) {
-        f.offsets[lr] = (int32_t)eex;
-        eex += nr[i];
-      }
-    }
-    if (tid == 0) f.offsets[R] = (int32_t)etot;
-    fused_release_done(f, tid, NT);
-    if (tid == 0) gstamp(a, 12);
   }
   // the stage ring is written by the TMA engine (async proxy) after these generic shared-memory accesses
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -657,7 +696,39 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
 
   if (warp == kProducerWarp) {
     // ---------------------------------------------------------------- producer
-    if (SPEC) {
+    if (FUSED) {
+      if (lane == 0) {
+        // items in order from the work counter, as the plain producer; each item's rows come from its request's ready
+        // word (polled until it carries this launch's epoch — no wait for the other CTAs' selection work), the next
+        // item's word read while the current copy waits for its stage
+        const uint64_t pol = l2_evict_normal_policy();
+        const uint32_t epoch = (uint32_t)__ldcg(a.fs.ctl + 2) + 1u;
+        long long i = (long long)atomicAdd(work, 1ull), i1 = (long long)atomicAdd(work, 1ull);
+        unsigned long long w = i < total ? fused_wait_ready(a.fs.ready + i / nch, epoch) : 0ull;
+        gstamp(a, 7);
+        int t = 0;
+        while (i < total) {
+          const long long i2 = (long long)atomicAdd(work, 1ull);
+          const unsigned long long w1 = i1 < total ? __ldcg(a.fs.ready + i1 / nch) : 0ull;
+          const long long prow = (long long)((w >> 22) & 0x3FFFFFull), qrow = (long long)(w & 0x3FFFFFull) - 1;
+          float lp = 0.f, lq = 0.f;
+          if (BF) {
+            lp = __ldg(a.lse_p + prow);
+            lq = qrow >= 0 ? __ldg(a.lse_q + qrow) : 0.f;
+          }
+          if (t == 0) gstamp(a, 2);
+          issue_item<BF>(a, sh, stage_mem, t++, (int)(i / nch), (int)(i % nch), prow, qrow, 0, pol, lp, lq);
+          i = i1;
+          i1 = i2;
+          if (i < total) w = fused_ready(w1, epoch) ? w1 : fused_wait_ready(a.fs.ready + i / nch, epoch);
+        }
+        const int st = t % kStages;  // end of stream: a sentinel stage without data
+        if (t >= kStages) mbar_wait(&sh.empty[st], (uint32_t)(((t / kStages) & 1) ^ 1u));
+        sh.meta[st] = StageMeta{-1, 0, 0, 0};
+        mbar_arrive(&sh.full[st]);
+        gstamp(a, 3);
+      }
+    } else if (SPEC) {
       if (lane == 0) {
         const uint64_t pol = l2_evict_first_policy();
         // phase A: residual rows at position 0 of the listed requests, item i = (entry i / nch, chunk i % nch),
@@ -749,7 +820,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
                                       qr = a.qrow ? __ldcg(a.qrow + (int64_t)b * a.row_stride) : -1;
                                       lp = __ldcg(a.rowlse + 2 * (int64_t)b);
                                       lq = __ldcg(a.rowlse + 2 * (int64_t)b + 1);
-                                    }, FUSED ? a.fs.ctl : nullptr);
+                                    });
       const int s = t % kStages;  // end of stream: a sentinel stage without data
       if (t >= kStages) mbar_wait(&sh.empty[s], (uint32_t)(((t / kStages) & 1) ^ 1u));
       sh.meta[s] = StageMeta{-1, 0, 0, 0};
@@ -760,10 +831,6 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       // two items of look-ahead on the counter and the row info, so neither round trip stalls the copies
       long long i_next = (long long)atomicAdd(work, 1ull);
       long long i_next2 = (long long)atomicAdd(work, 1ull);
-      if (FUSED) {  // the claims are out; the row lookups need every CTA's rows published
-        spin_acquire_geq(a.fs.ctl, G);
-        gstamp(a, 7);
-      }
       long long pn = 0, qn = -1;
       float lpn = 0.f, lqn = 0.f;
       auto rows = [&](long long ii) {
@@ -800,6 +867,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
     __syncwarp();
   } else if (warp < kConsumerWarps) {
     // ---------------------------------------------------------------- consumers
+    if (FUSED) fused_scans<BF>(a, tid, kConsumerWarps * 32);
     for (int t = 0;; ++t) {
       const int s = t % kStages;
       mbar_wait(&sh.full[s], (uint32_t)((t / kStages) & 1));
@@ -940,6 +1008,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
           __nanosleep(64);
         }
         *cnt = 0;  // every arrival is in: ready for the next launch
+        if (warp == 0 && b == (int)blockIdx.x) gstamp(a, 13);
         if (inA && !doneA) {  // phase A streamed this request for nothing: drain its counter too
           for (;;) {
             asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.req_cnt_spec + b) : "memory");
@@ -952,6 +1021,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       __syncwarp();
       finalize_request<BF>(a, b, qrow >= 0, lane, doneA ? a.chunk_sums_spec : a.chunk_sums,
                            doneA ? a.warp_sums_spec : a.warp_sums);
+      if (warp == 0 && lane == 0 && b == (int)blockIdx.x) gstamp(a, 14);
     }
     // the last CTA out resets the work counters and the phase-A list (every producer is done with them)
     __syncthreads();
@@ -966,6 +1036,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         if (FUSED) {
           a.fs.ctl[0] = 0;
           a.fs.ctl[1] = 0;
+          a.fs.ctl[2] = a.fs.ctl[2] + 1;  // the epoch this launch used (every CTA has read it)
         }
         *done = 0u;
       }
@@ -1098,7 +1169,7 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
              (spec && !a.spec_lse)))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "logits form: zq / lse_p / lse_q and the fused descent are required");
   const bool fused = a.fs.conf != nullptr;
-  if (fused && (spec || a.req_cnt == nullptr || !a.accepted || !a.fs.ctl || !a.fs.u_acc || !a.d ||
+  if (fused && (spec || a.req_cnt == nullptr || !a.accepted || !a.fs.ctl || !a.fs.ready || !a.fs.u_acc || !a.d ||
                 (long long)a.fs.B_sel * a.k > kFusedMaxCells || (bf && !a.fs.rowlse)))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "fused step: B_sel * k > %d or missing buffers", kFusedMaxCells);
   const void* fn = fused ? (bf ? (const void*)persist_stream_kernel<false, true, true>

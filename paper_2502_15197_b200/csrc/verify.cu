@@ -734,6 +734,7 @@ static int fused_step_impl(const double* conf, const int32_t* len, int32_t B_sel
   f.rowlse = rowlse;
   f.offsets = offsets;
   f.ctl = cnt + abi::kSlotFusedCtl;
+  f.ready = reinterpret_cast<unsigned long long*>(cnt + abi::kSlotFusedReady);
   if (k == 0) a.d = d ? d : (const int32_t*)&kNoScores;
   return launch_persist_stream(a, st);
 }

@@ -34,8 +34,9 @@ d = dbg[64:64 + 16 * nsm].view(nsm, 16).cpu()
 cyc = dbg[64 + 16 * nsm:].view(nsm, 16).cpu()
 t0 = int(d[:, 0][d[:, 0] > 0].min())
 names = ["entry", "after wait", "first copy", "last copy", "first consumed", "publisher done", "descents done",
-         "spec prologue / fused: all rows published (producer)", "fused: scores loaded", "fused: keys built",
-         "fused: ranks done", "fused: last CTA publishes", "fused: scans released"]
+         "spec prologue / fused: first item ready (producer)", "fused: scores loaded", "fused: keys built",
+         "fused: ranks done", "fused: last CTA publishes", "fused: scans released",
+         "descent (warp 0): request's chunks counted", "descent (warp 0): done", "descent (warp 0): sums in"]
 for s, nme in enumerate(names):
     col = d[:, s]
     col = col[col > 0]
@@ -47,9 +48,10 @@ for s, nme in enumerate(names):
 # in-CTA phase lengths in SM cycles (clock64 beside each stamp): consecutive slots of the fused prologue
 for a_, b_, nme in ((1, 8, "wait -> scores loaded"), (8, 9, "scores -> keys"), (9, 10, "keys -> ranks+verdicts"),
                     (10, 11, "ranks -> published (last CTA)"), (11, 12, "published -> scans released (last CTA)"),
-                    (1, 7, "wait -> producer sees all rows"), (7, 2, "all rows -> first copy"),
+                    (1, 7, "wait -> first item ready"), (7, 2, "ready -> first copy"),
                     (2, 3, "first -> last copy"), (3, 5, "last copy -> publisher done"),
-                    (5, 6, "publisher done -> descents done")):
+                    (5, 6, "publisher done -> descents done"), (5, 13, "publisher done -> warp 0 request counted"),
+                    (13, 15, "counted -> descent sums in"), (15, 14, "sums in -> descent done")):
     m = (cyc[:, a_] > 0) & (cyc[:, b_] > 0)
     if m.sum() == 0:
         continue
