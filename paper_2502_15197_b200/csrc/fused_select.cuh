@@ -327,6 +327,24 @@ __device__ __forceinline__ void fused_release_done(const FusedSel& f, int pt, in
   }
 }
 
+// A request's ready word (one-launch step): bits 63..44 the launch's epoch (low 20 bits), 43..22 its p row (greedy: its
+// window), 21..0 its q row + 1 (0: bonus row).  Rows < 2^22 hold: R * (k + 1) <= 2 * kFusedMaxCells.  Epochs make the words self-resetting:
+// a word from an earlier launch never carries this launch's epoch.
+__device__ __forceinline__ unsigned long long fused_ready_word(uint32_t epoch, long long prow, long long qrow) {
+  return ((unsigned long long)(epoch & 0xFFFFFu) << 44) | ((unsigned long long)prow << 22) |
+         (unsigned long long)(qrow + 1);
+}
+__device__ __forceinline__ bool fused_ready(unsigned long long w, uint32_t epoch) {
+  return (uint32_t)(w >> 44) == (epoch & 0xFFFFFu);
+}
+__device__ __forceinline__ unsigned long long fused_wait_ready(const unsigned long long* p, uint32_t epoch) {
+  for (;;) {
+    const unsigned long long w = __ldcg(p);
+    if (fused_ready(w, epoch)) return w;
+    __nanosleep(32);
+  }
+}
+
 __device__ __forceinline__ void spin_acquire_geq(const int* p, int v) {
   int seen;
   for (;;) {

@@ -23,6 +23,7 @@
 // chunks, reads the w_b + 1 keys and writes accepted / out_tok; the last CTA out runs the compaction (offsets and
 // tokens, compact_kernel's contract) when asked to.
 #include "common.cuh"
+#include "fused_select.cuh"
 #include "launch.h"
 
 namespace tetris {
@@ -169,11 +170,18 @@ __global__ void __launch_bounds__(1024, 1)
   if (tid == 0) rowmap[0] = (int32_t)total;
 }
 
+// FUSED (the one-launch greedy step, B_sel * k <= kFusedMaxCells): the selection runs as a prologue on the consumer
+// and publisher warps (fused_select.cuh) while the producer already streams row 0 of every request; the ring is 5
+// stages and the 6th stage's 32 KB holds the selection's scratch.  The row list becomes per-request ready words (epoch
+// | window): phase B claims every (request, row 1..k, chunk) item in order and skips the rows past the window.
+template <bool FUSED>
 __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const GreedyArgs a) {
+  constexpr int kGStages = FUSED ? 5 : 6;
   extern __shared__ __align__(128) uint8_t stage_mem[];
   __shared__ GreedyShared sh;
   __shared__ long long s_tmp[33];
   __shared__ int s_last;
+  __shared__ uint32_t s_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nch = a.nch, V = a.V, k = a.k;
   const int G = gridDim.x;
@@ -191,7 +199,35 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
     }
     mbar_fence_init();
   }
+  if (FUSED) {
+    // the previous launch on the stream may have written the inputs: wait for it before the first read; the epoch
+    // of this launch (the previous one's + 1, set by its last CTA out)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0) s_epoch = (uint32_t)__ldcg(a.fs.ctl + 2) + 1u;
+  }
   __syncthreads();
+
+  if (FUSED && warp != kGProducer) {
+    // the selection prologue on warps 0..15 and 17 (participant index: warp 17 -> 512..543)
+    const int NP = kGThreads - 32, pt = warp < kGProducer ? tid : tid - 32;
+    const FusedSel& f = a.fs;
+    const FusedView v = fused_view(f, k, stage_mem + kGStages * kGStageBytes);
+    fused_stage(f, k, v, pt, NP);
+    fused_bar(NP);
+    fused_keys(f, k, v, pt, NP, a.status);
+    fused_bar(NP);
+    fused_ranks(k, v, pt, NP);
+    fused_bar(NP);
+    const uint32_t epoch = s_epoch;
+    for (int oi = pt; oi < v.nown; oi += NP) {
+      const int r = blockIdx.x + oi * G;
+      const int w = fused_window(f, k, v, oi);
+      f.windows[r] = w;
+      const int lr = r - f.row0;
+      if (lr >= 0 && lr < a.B) __stcg(f.ready + lr, fused_ready_word(epoch, w, -1));  // epoch | window
+    }
+    if (pt == 0) gtime(a, 5);
+  }
 
   if (warp == kGProducer) {
     const uint64_t pol = l2_evict_first_policy();
@@ -236,11 +272,35 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       }
     }
     __syncwarp();
+    if (FUSED) {
+      // Phase B of the one-launch step: items (request b, row j = 1..k, chunk c) in order from the work counter; a
+      // request's window comes from its ready word (polled until it carries this launch's epoch), rows past it are
+      // skipped without a copy
+      if (lane == 0) {
+        const uint32_t epoch = s_epoch;
+        const long long per_b = (long long)k * nch, total = (long long)a.B * per_b;
+        long long i = (long long)atomicAdd(work, 1ull), i1 = (long long)atomicAdd(work, 1ull);
+        int bcur = -1, wb = 0;
+        while (i < total) {
+          const long long i2 = (long long)atomicAdd(work, 1ull);
+          const int b = (int)(i / per_b), rem = (int)(i - (long long)b * per_b), j = 1 + rem / nch, cc = rem % nch;
+          if (b != bcur) {
+            wb = (int)((fused_wait_ready(a.fs.ready + b, epoch) >> 22) & 0x3FFFFFull);
+            bcur = b;
+          }
+          if (j <= wb) issue(b, b * (k + 1) + j, cc, 0);
+          i = i1;
+          i1 = i2;
+        }
+        gtime(a, 2);
+      }
+    }
     // Phase B: the listed rows 1..w_b, once the selection (and its row list) is complete
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (lane == 0) gtime(a, 2);
-    const long long total = (long long)__ldcg(a.rowmap) * nch;
-    if (lane == 0 && total <= (long long)kStaticItems * gridDim.x) {
+    if (!FUSED) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (lane == 0 && !FUSED) gtime(a, 2);
+    const long long total = FUSED ? 0 : (long long)__ldcg(a.rowmap) * nch;
+    if (FUSED) {
+    } else if (lane == 0 && total <= (long long)kStaticItems * gridDim.x) {
       // small calls: a static schedule (items blockIdx.x + x * G) with every row lookup issued up front
       int rm[kStaticItems];
 #pragma unroll
@@ -339,7 +399,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.ring_free[slot]);
       key = warp_max_u64(key);
-      if (m.pad == 0 && !waited) {  // the row list's keys were zeroed by the selection: wait for it once
+      if (!FUSED && m.pad == 0 && !waited) {  // the row list's keys were zeroed by the selection: wait for it once
         asm volatile("griddepcontrol.wait;" ::: "memory");
         waited = true;
       }
@@ -356,7 +416,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's selector may be scheduled
   constexpr int kWarps = kGThreads / 32;
   for (int b = warp * G + blockIdx.x; b < a.B; b += G * kWarps) {
-    int w = a.windows[b];
+    int w = FUSED ? (int)((fused_wait_ready(a.fs.ready + b, s_epoch) >> 22) & 0x3FFFFFull) : a.windows[b];
     uint32_t bad = (w < 0 || w > k) ? TETRIS_ST_BAD_WINDOW : 0u;
     w = w < 0 ? 0 : (w > k ? k : w);
     if (lane == 0) {
@@ -370,7 +430,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       a.req_cnt[b] = 0;  // every arrival is in: ready for the next launch
     }
     __syncwarp();
-    const unsigned long long* kb = a.keys + (int64_t)b * (k + 1);
+    unsigned long long* kb = a.keys + (int64_t)b * (k + 1);
     int acc = w, tok = -1;
     for (int j0 = 0; j0 <= w; j0 += 32) {
       const int j = j0 + lane;
@@ -387,6 +447,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       }
       if (w < j0 + 32) tok = __shfl_sync(kFull, am, w - j0);  // all accepted: the bonus position's argmax
     }
+    for (int j = 1 + lane; j <= w; j += 32) kb[j] = 0ull;  // read: left at zero for the next launch
     if (lane == 0) {
       a.key0[b] = 0ull;  // read above (lane 0, j = 0): ready for the next launch
       a.accepted[b] = acc;
@@ -406,12 +467,19 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       *work = 0ull;
       *reinterpret_cast<unsigned long long*>(a.grid_bar2) = 0ull;
       *done = 0u;
+      if (FUSED) a.fs.ctl[2] = (int)s_epoch;  // the epoch this launch used (every CTA has read it)
       __threadfence();
     }
     s_last = last;
   }
   __syncthreads();
-  if (!s_last || a.offsets == nullptr) return;
+  if (!s_last) return;
+  if (FUSED) {  // the one-launch step: win_offsets and PolicyStats over every selected row's window
+    int wr[kFusedMaxRpt];
+    fused_load_windows(a.fs, tid, blockDim.x, wr);
+    fused_win_scan(a.fs, k, tid, blockDim.x, s_tmp, wr);
+  }
+  if (a.offsets == nullptr) return;
   // compact_kernel's contract: n_b = accepted[b] + 1 (capped), offsets = exclusive scan, tokens = d[b][0..a) ++ [x]
   const int B = a.B;
   const int R = (B + blockDim.x - 1) / blockDim.x;
@@ -443,6 +511,9 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
 
 namespace tetris {
 
+// the one-launch greedy step keeps the selection's scratch in the 6th stage (32 KB)
+bool greedy_fused_fits(int B_sel, int k) { return fused_scratch_bytes(B_sel, k, abi::device_sm_count()) <= kGStageBytes; }
+
 bool persist_greedy_eligible(const float* p, int V) {
   return (V % kLaneElems == 0) && (((uintptr_t)p & 15u) == 0);
 }
@@ -471,15 +542,22 @@ int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, 
 
 int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st) {
   const int num_sms = abi::device_sm_count();
-  cudaError_t e = abi::ensure_smem((const void*)persist_greedy_kernel, kGSmem);
+  const bool fused = a.fs.conf != nullptr;
+  if (fused && ((long long)a.fs.B_sel * a.k > kFusedMaxCells || !a.fs.ctl || !a.fs.ready ||
+                fused_scratch_bytes(a.fs.B_sel, a.k, num_sms) > kGStageBytes))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "one-launch greedy step: B_sel * k > %d or missing buffers",
+                     kFusedMaxCells);
+  const void* fn = fused ? (const void*)persist_greedy_kernel<true> : (const void*)persist_greedy_kernel<false>;
+  cudaError_t e = abi::ensure_smem(fn, kGSmem);
   if (e != cudaSuccess) return abi::cuda_fail(e);
-  // the listed-row count lives on the device; the bound B * (k + 1) * nch caps the useful grid
+  // the listed-row count lives on the device; the bound B * (k + 1) * nch caps the useful grid (fused: every SM,
+  // the selection's rank work is spread over the CTAs)
   const long long items = (long long)a.B * (a.k + 1) * a.nch;
-  const int grid = (int)(items < num_sms ? items : num_sms);
+  const int grid = fused ? num_sms : (int)(items < num_sms ? items : num_sms);
   GreedyArgs copy = a;
   copy.dbg = debug_buffer();
   void* args[] = {(void*)&copy};
-  return launch_pdl((const void*)persist_greedy_kernel, dim3(grid), dim3(kGThreads), kGSmem, st, args);
+  return launch_pdl(fn, dim3(grid), dim3(kGThreads), kGSmem, st, args);
 }
 
 }  // namespace tetris

@@ -136,6 +136,7 @@ struct GreedyArgs {
   int32_t* offsets;           // [B+1] nullable: fused compaction off
   int32_t* tokens;
   uint32_t* status;
+  FusedSel fs;                // one-launch step (fs.conf != nullptr): the selection as the kernel's prologue
 };
 
 int launch_select(const SelectArgs& a, cudaStream_t st);
@@ -146,6 +147,7 @@ size_t gselect_scratch_bytes();
 int launch_persist_stream(const StreamArgs& a, cudaStream_t st);
 bool persist_eligible(const float* p, const float* q, int V);
 bool persist_greedy_eligible(const float* p, int V);
+bool greedy_fused_fits(int B_sel, int k);
 int launch_greedy_rowmap(const int32_t* windows, int B, int k, int32_t* rowmap, unsigned long long* keys, int j0,
                          cudaStream_t st);
 int launch_persist_greedy(const GreedyArgs& a, cudaStream_t st);

@@ -433,24 +433,6 @@ __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stag
 // rejection among the selected positions (accept_model.py:309-313, sim_engine.py:397-401) from verdicts gathered in
 // the selection's first round trip, the row to resample from, and — in the last CTA to publish — the compaction
 // offsets.  The producers wait for every CTA's rows (ctl[0] == G), the descents for the scans (ctl[1]).
-// A request's ready word (fused step): bits 63..44 the launch's epoch (low 20 bits), 43..22 its p row, 21..0 its q row
-// + 1 (0: bonus row).  Rows < 2^22 hold: R * (k + 1) <= 2 * kFusedMaxCells.  Epochs make the words self-resetting:
-// a word from an earlier launch never carries this launch's epoch.
-__device__ __forceinline__ unsigned long long fused_ready_word(uint32_t epoch, long long prow, long long qrow) {
-  return ((unsigned long long)(epoch & 0xFFFFFu) << 44) | ((unsigned long long)prow << 22) |
-         (unsigned long long)(qrow + 1);
-}
-__device__ __forceinline__ bool fused_ready(unsigned long long w, uint32_t epoch) {
-  return (uint32_t)(w >> 44) == (epoch & 0xFFFFFu);
-}
-__device__ __forceinline__ unsigned long long fused_wait_ready(const unsigned long long* p, uint32_t epoch) {
-  for (;;) {
-    const unsigned long long w = __ldcg(p);
-    if (fused_ready(w, epoch)) return w;
-    __nanosleep(32);
-  }
-}
-
 // The last CTA to count itself in (ctl[0]) writes win_offsets / PolicyStats (selector.py:150-170) and the compaction
 // offsets from every CTA's published rows, then raises ctl[1] (the descents wait for it).  Run by the 16 consumer
 // warps after the producer has started streaming, so it reads global memory only (the prologue's shared scratch is

@@ -1046,26 +1046,6 @@ extern "C" int tetris_step_greedy_f32(const double* conf, const int32_t* len, in
   int* cnt = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS);
   unsigned long long* keys = (unsigned long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ARG_VAL);
   int32_t* rowmap = (int32_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWMAP);
-  SelectArgs sa = {};
-  sa.vals = conf;
-  sa.len = len;
-  sa.B = B_sel;
-  sa.k = k;
-  sa.C = (long long)C;
-  sa.windows = windows;
-  sa.win_offsets = win_offsets;
-  sa.stats = (long long*)stats4;
-  sa.status = status;
-  sa.ep_row0 = row0;
-  sa.ep_rows = B;
-  sa.gscratch = abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_GSEL);
-  const bool fused_rows = select1_eligible(B_sel, k);
-  if (fused_rows) {
-    sa.rowmap = rowmap;
-    sa.gkeys = keys;
-  }
-  if ((rc = launch_select(sa, st))) return rc;
-  if (!fused_rows && (rc = launch_greedy_rowmap(windows + row0, B, k, rowmap, keys, 1, st))) return rc;
   GreedyArgs a = {};
   a.p = p;
   a.d = d;
@@ -1086,6 +1066,43 @@ extern "C" int tetris_step_greedy_f32(const double* conf, const int32_t* len, in
   a.offsets = offsets;
   a.tokens = tokens;
   a.status = status;
+  if (fused_step_eligible(B_sel, k, 0) && greedy_fused_fits(B_sel, k)) {
+    // small batch: ONE launch — the selection as the argmax stream's prologue (greedy.cu, FUSED)
+    FusedSel& f = a.fs;
+    static const double kNoScores = 0.0;  // k == 0: nothing is read through it
+    f.conf = conf ? conf : &kNoScores;
+    f.len = len;
+    f.B_sel = B_sel;
+    f.row0 = row0;
+    f.C = (long long)C;
+    f.windows = windows;
+    f.win_offsets = win_offsets;
+    f.stats = (long long*)stats4;
+    f.ctl = cnt + abi::kSlotFusedCtl;
+    f.ready = reinterpret_cast<unsigned long long*>(cnt + abi::kSlotFusedReady);
+    if (k == 0 && !d) a.d = (const int32_t*)&kNoScores;
+    return launch_persist_greedy(a, st);
+  }
+  SelectArgs sa = {};
+  sa.vals = conf;
+  sa.len = len;
+  sa.B = B_sel;
+  sa.k = k;
+  sa.C = (long long)C;
+  sa.windows = windows;
+  sa.win_offsets = win_offsets;
+  sa.stats = (long long*)stats4;
+  sa.status = status;
+  sa.ep_row0 = row0;
+  sa.ep_rows = B;
+  sa.gscratch = abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_GSEL);
+  const bool fused_rows = select1_eligible(B_sel, k);
+  if (fused_rows) {
+    sa.rowmap = rowmap;
+    sa.gkeys = keys;
+  }
+  if ((rc = launch_select(sa, st))) return rc;
+  if (!fused_rows && (rc = launch_greedy_rowmap(windows + row0, B, k, rowmap, keys, 1, st))) return rc;
   return launch_persist_greedy(a, st);
 }
 

@@ -676,6 +676,8 @@ class TetrisStep:
             if self.V % 8 != 0:
                 return 3  # select, verify (one sample_kernel), compact
             return 1 if self.fused else 2
+        if self.Bg * self.k <= FUSED_MAX_CELLS and self.V % 8 == 0 and not _NO_FUSED:
+            return 1  # the one-launch greedy step (selection as the argmax stream's prologue)
         return 2 if self.Bg * self.k <= 16384 and self.Bg <= 4096 else 3
 
 

@@ -196,3 +196,86 @@ def test_logits_one_launch():
     assert torch.equal(s32.tokens[:n], step.tokens[:n])
     w_ref, _, _ = O.select(_np(lb.conf), C, _np(lb.lengths))
     assert np.array_equal(_np(step.windows_all), w_ref)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# the one-launch GREEDY step (persist_greedy_kernel<FUSED>): the selection as the argmax stream's prologue while row 0
+# of every request streams; against the stage-by-stage path (tetris_select_f64 + tetris_verify_greedy_compact_f32)
+# and the oracle
+def _greedy_step(conf, ln, Bsel, k, C, row0, B, p, d, V, cap):
+    lib, s = N.load(), torch.cuda.current_stream().cuda_stream
+    o = _Out(Bsel, B, k)
+    ws = ops.Workspace(DEV, N.OP_ALL, Bsel, k, V)
+    cp = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    rc = lib.tetris_step_greedy_f32(conf.data_ptr(), cp(ln), Bsel, k, C, row0, B, p.data_ptr(), d.data_ptr(), cp(cap),
+                                    V, o.windows.data_ptr(), o.woff.data_ptr(), o.acc.data_ptr(), o.tok.data_ptr(),
+                                    o.offs.data_ptr(), o.toks.data_ptr(), o.stats.data_ptr(), o.status.data_ptr(),
+                                    ws.ptr, ws.nbytes, s)
+    assert rc == N.OK, lib.tetris_last_error()
+    torch.cuda.synchronize()
+    return o, ws
+
+
+def _check_greedy(B, k, V, C, seed, *, conf=None, lengths=None, cap=False, world=1, rank=0, repeat=1):
+    bt = make_batch(B, k, V, seed=seed, mode="greedy")
+    if conf is None:
+        conf, lengths = bt.conf, bt.lengths
+    Bsel = B * world
+    if world > 1:
+        others = [make_batch(B, k, 8, seed=seed + 1000 + r).conf for r in range(world)]
+        others[rank] = conf
+        conf = torch.cat(others).contiguous()
+        lengths = None if lengths is None else torch.cat([lengths] * world).contiguous()
+    g = torch.Generator(DEV).manual_seed(seed + 7)
+    capt = torch.randint(0, k + 3, (B,), dtype=torch.int32, device=DEV, generator=g) if cap else None
+    o, ws = _greedy_step(conf, lengths, Bsel, k, C, rank * B, B, bt.p, bt.d, V, capt)
+    lib = N.load()
+    for _ in range(repeat - 1):  # the same workspace again: ready words / keys / counters left clean
+        rc = lib.tetris_step_greedy_f32(conf.data_ptr(), None if lengths is None else lengths.data_ptr(), Bsel, k, C,
+                                        rank * B, B, bt.p.data_ptr(), bt.d.data_ptr(),
+                                        None if capt is None else capt.data_ptr(), V, o.windows.data_ptr(),
+                                        o.woff.data_ptr(), o.acc.data_ptr(), o.tok.data_ptr(), o.offs.data_ptr(),
+                                        o.toks.data_ptr(), o.stats.data_ptr(), o.status.data_ptr(), ws.ptr, ws.nbytes,
+                                        torch.cuda.current_stream().cuda_stream)
+        assert rc == N.OK
+    torch.cuda.synchronize()
+    ops.raise_for_status(o.status)
+    r = o.results()
+    w_ref, _, st_ref = O.select(_np(conf), C, None if lengths is None else _np(lengths))
+    assert np.array_equal(r["windows"], w_ref)
+    assert list(r["stats"]) == list(st_ref[:3])
+    assert np.array_equal(r["win_offsets"], np.concatenate([[0], np.cumsum(w_ref)]))
+    wl = w_ref[rank * B:(rank + 1) * B]
+    acc_ref, tok_ref = O.verify_greedy(_np(bt.p), _np(bt.d), wl, nthreads=8)
+    assert np.array_equal(r["accepted"], acc_ref)
+    assert np.array_equal(r["out_tok"], tok_ref)
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None if capt is None else _np(capt))
+    assert np.array_equal(r["offsets"], off_ref)
+    assert np.array_equal(r["tokens"], toks_ref)
+
+
+@pytest.mark.parametrize("B,k,V,C", [(16, 5, 32000, 48), (256, 8, 32000, 1024), (1, 1, 8, 1), (37, 11, 4096, 200),
+                                     (2048, 1, 1024, 700), (100, 20, 8200, 900), (128, 16, 128256, 999)])
+def test_greedy_one_launch_parity(B, k, V, C):
+    _check_greedy(B, k, V, C, seed=B * 7 + k)
+
+
+@pytest.mark.parametrize("C", [0, 1, 79, 80, 500])
+def test_greedy_capacity_edges_and_cap(C):
+    _check_greedy(16, 5, 32000, C, seed=C, cap=True)
+
+
+@pytest.mark.parametrize("kind", ["quantized", "ties", "zeros", "ragged"])
+def test_greedy_adversarial_selection(kind):
+    conf, ln = selection_instance(256, 8, kind, seed=13)
+    _check_greedy(256, 8, 8192, 1000, seed=3, conf=conf.contiguous(), lengths=ln.contiguous())
+
+
+def test_greedy_shard_and_repeats():
+    _check_greedy(64, 8, 8192, 1200, seed=4, world=4, rank=2)
+    _check_greedy(64, 8, 8192, 300, seed=5, repeat=4)
+
+
+def test_greedy_step_launch_count():
+    step = ops.TetrisStep(16, 5, 32000, 48, mode="greedy")
+    assert step.launches_per_step == 1
