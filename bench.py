@@ -108,7 +108,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------------------------------
-def _setup_dist(n_gpus: int):
+def _setup_dist(n_gpus: int, force_nccl: bool = False):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -117,11 +117,13 @@ def _setup_dist(n_gpus: int):
     if n_gpus > 1 and world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch with torchrun --nproc-per-node {n_gpus}")
     group = None
-    if world > 1:
+    if world > 1 or force_nccl:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        for key, val in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_PORT", "29531")):  # --nccl without torchrun
+            os.environ.setdefault(key, val)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
     else:
@@ -189,7 +191,7 @@ def run_tetris(args):
     from paper_2502_15197_b200 import ops
     from paper_2502_15197_b200.synthetic import make_batch, make_logit_batch
 
-    world, rank, local, group = _setup_dist(args.gpus)
+    world, rank, local, group = _setup_dist(args.gpus, args.nccl)
     logits = args.input == "logits"
     if logits and (cfg_mode := CONFIGS[args.config]["mode"]) != "stochastic":
         raise SystemExit(f"--input logits is the stochastic step ({args.config} is {cfg_mode})")
@@ -221,7 +223,7 @@ def run_tetris(args):
     else:
         sets = [make_batch(B_local, k, V, mode=mode, seed=args.seed + 7919 * rank + 104729 * s, device=dev)
                 for s in range(nsets)]
-    step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group if world > 1 else None,
+    step = ops.TetrisStep(B_local, k, V, C, mode=mode, device=dev, group=group,
                           policy=args.policy, shard=(sim_w, 0) if sim_w else None)
     if sim_w:
         # one rank's share of a sharded step on one GPU: this rank's requests (rank 0) + the other ranks' scores as
@@ -261,7 +263,8 @@ def run_tetris(args):
     graphs = []
     multi = None
     M = 1
-    use_graph = args.graph and world == 1
+    # (NCCL groups: the native sharded step issues its all-gather on the current stream, so it captures too)
+    use_graph = args.graph and (world == 1 or step._comm is not None)
     if use_graph:
         cs = torch.cuda.Stream()
         cs.wait_stream(torch.cuda.current_stream())
@@ -461,14 +464,14 @@ def _e2e(args, cfg, step_dev, bt, B, k, V, C, mode, group, world, dev):
     return {"value": toks / (ms / 1e3), "unit": "tokens/s", "steps": steps, "ms_per_step": ms / steps,
             "h2d_bytes_per_step": hs.h2d_bytes() + zero_copy, "d2h_bytes_per_step": hs.d2h_bytes(),
             "h2d_mode": ("explicit copies of conf/lengths/draft tokens/uniforms (%d B) + " % hs.h2d_bytes()) + (
-                "DMA copies of the needed p/q rows from pinned host memory after the selection (%d B; the selector's "
+                "gather-kernel copies of the needed p/q rows from pinned host memory after the selection (%d B; the selector's "
                 "accept test reads its scalars through the mapping)" % zero_copy if hs.transfer == "staged" else
                 "zero-copy kernel reads of the needed p/q rows from pinned host memory (%d B)" % zero_copy)}
 
 
 def _e2e_logits(args, cfg, lb, B, k, V, C, dev):
     """The logits form through the host-buffer API (ops.HostLogitStep): bf16 logits + lse in pinned host memory, the
-    needed rows staged by DMA after the selection, results copied back, every step."""
+    needed rows gathered into device memory after the selection, results copied back, every step."""
     import torch
 
     from paper_2502_15197_b200 import ops
@@ -499,7 +502,7 @@ def _e2e_logits(args, cfg, lb, B, k, V, C, dev):
     staged = rows * V * 2 + rows * 4
     return {"value": toks / (ms / 1e3), "unit": "tokens/s", "steps": steps, "ms_per_step": ms / steps,
             "h2d_bytes_per_step": hs.h2d_bytes() + staged, "d2h_bytes_per_step": hs.d2h_bytes(),
-            "h2d_mode": "explicit copies of conf/lengths/draft tokens/uniforms (%d B) + DMA copies of the needed bf16 "
+            "h2d_mode": "explicit copies of conf/lengths/draft tokens/uniforms (%d B) + gather-kernel copies of the needed bf16 "
                         "logit rows and their lse after the selection (%d B)" % (hs.h2d_bytes(), staged)}
 
 
@@ -775,6 +778,8 @@ def main():
                     help="--impl reference: about this many seconds for the K timed steps (sets the per-step sample)")
     ap.add_argument("--graph-steps", type=int, default=8, help="steps captured per CUDA graph (rounded up to a "
                     "multiple of the input-set count)")
+    ap.add_argument("--nccl", action="store_true", help="run the NCCL-sharded step even at world size 1 (measures "
+                    "the exchange's fixed cost on one GPU)")
     ap.add_argument("--simulate-world", type=int, default=0,
                     help="on 1 GPU: time rank 0's share of a step sharded over this many ranks (the other ranks' "
                          "gathered scores are this rank's rows reshuffled; no NCCL exchange in the timed region)")

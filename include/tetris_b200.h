@@ -11,10 +11,9 @@
  *   - All pointers are DEVICE pointers (or host pointers registered/mapped for device access) owned by the caller;
  *     the library allocates nothing persistent.  Scratch space comes from a caller-provided workspace that must be
  *     zeroed once with tetris_workspace_init() (kernels leave their arrival counters at zero after every call).
- *   - Everything is stream-ordered on the caller's `stream`; no entry point synchronises the host, except the two
- *     host-buffer steps (tetris_step_*_staged_f32), which wait for the selection mid-call to learn which host rows to
- *     copy.  The ABI is reentrant: no mutable globals besides the thread-local last-error string and write-once
- *     per-device caches (SM count, kernel shared-memory attributes, the staged steps' per-thread copy streams).
+ *   - Everything is stream-ordered on the caller's `stream`; no entry point synchronises the host.  The ABI is
+ *     reentrant: no mutable globals besides the thread-local last-error string and write-once per-device caches (SM
+ *     count, kernel shared-memory attributes), and the NCCL symbol table of the sharded entry points (resolved once).
  *   - Host-checkable argument errors return TETRIS_INVALID_ARGUMENT immediately.  Data-dependent errors found on the
  *     device are OR-ed into the caller's device word `status` (TETRIS_ST_* bits); the host adapter reads it when it
  *     materialises results and raises the reference's exception.
@@ -38,6 +37,7 @@ typedef struct CUstream_st* tetris_stream_t; /* == cudaStream_t */
 #define TETRIS_INVALID_ARGUMENT 1   /* -> ValueError (selector.py:145-146, accept_model.py:284-288, :304-308) */
 #define TETRIS_DEGENERATE_RESIDUAL 2 /* -> DegenerateResidualError (accept_model.py:28-29, :323-326)           */
 #define TETRIS_CUDA_ERROR 3
+#define TETRIS_NCCL_ERROR 4         /* NCCL missing or a collective failed (tetris_dist_*)                       */
 
 /* ---- device status bits (OR-ed into *status by kernels) ----------------------------------------------------- */
 #define TETRIS_ST_BAD_VALUE 1u     /* alpha / cum NaN or (conf mode) outside [0,1]  (accept_model.py:55-59)       */
@@ -249,41 +249,42 @@ int tetris_verify_greedy_compact_f32(const float* p, const int32_t* d, const int
                                      int32_t* offsets, int32_t* tokens, uint32_t* status, void* ws, size_t ws_bytes,
                                      tetris_stream_t stream);
 
-/* The stochastic step for HOST-resident p ([B][k+1][V]) and q ([B][k][V]) in pinned, device-mapped memory (the
- * end-to-end path): selection + accept test reading the scalars it needs through the mapping, then (host waits for
- * it) one DMA copy per needed row into the device buffer `staging` (>= 2*B rows of V floats) on the copy engines,
- * then the sampler on device memory.  rowinfo_host: pinned host scratch of 2*B int64.  Same results as
- * tetris_step_stochastic_f32 with dense uniforms. */
+/* The stochastic step for HOST-resident p / q (the end-to-end path): p_host [B][k+1][V], q_host [B][k][V] pinned and
+ * device-mapped (tetris_map_host), 16-byte aligned, V % 8 == 0.  The selector's accept test gathers its scalars through
+ * the mapping; then one gather kernel copies the row each request resamples from (residual: p[b][a_b] and q[b][a_b];
+ * bonus: p[b][w_b]) from host memory into the device buffer `staging` (>= 2*B rows of V; request b uses rows 2b, 2b+1)
+ * with 16-byte SM loads over the host link (51 GB/s measured, vs 37 GB/s for one DMA copy per row), then the sampler
+ * runs on device memory.  No host synchronisation (capturable).  Same results as tetris_step_stochastic_f32 with dense
+ * uniforms. */
 int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
                                       const float* p_host, const float* q_host, const int32_t* d,
                                       const double* u_acc, const double* u_res, const int32_t* cap, int32_t V,
-                                      float* staging, int64_t* rowinfo_host, int32_t* windows, int32_t* win_offsets,
-                                      int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
-                                      int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                      float* staging, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
+                                      int32_t* out_tok, double* mass_out, int32_t* offsets, int32_t* tokens,
+                                      int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
                                       tetris_stream_t stream);
 
 /* tetris_step_stochastic_staged_f32 for HOST-resident LOGITS: zp_host / zq_host bf16 and lse_p_host / lse_q_host f32,
- * all pinned and device-mapped; staging [2B][V] bf16 and lse_staging [2B] f32 on the device, lse_host_scratch [2B]
- * f32 pinned.  Same results as tetris_step_stochastic_bf16 on device copies; half the host-link bytes of the fp32
- * form. */
+ * all pinned and device-mapped; staging [2B][V] bf16 and lse_staging [2B] f32 on the device.  Same results as
+ * tetris_step_stochastic_bf16 on device copies; half the host-link bytes of the fp32 form. */
 int tetris_step_stochastic_staged_bf16(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
                                        const uint16_t* zp_host, const float* lse_p_host, const uint16_t* zq_host,
                                        const float* lse_q_host, const int32_t* d, const double* u_acc,
                                        const double* u_res, const int32_t* cap, int32_t V, uint16_t* staging,
-                                       float* lse_staging, float* lse_host_scratch, int64_t* rowinfo_host,
-                                       int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
-                                       double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4,
-                                       uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+                                       float* lse_staging, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
+                                       int32_t* out_tok, double* mass_out, int32_t* offsets, int32_t* tokens,
+                                       int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                       tetris_stream_t stream);
 
-/* The greedy step for HOST-resident p ([B][k+1][V], pinned and device-mapped): the selection, then (host waits for it)
- * one DMA copy per request of its verified rows p[b][0 .. windows[b]] (contiguous in host memory) into the same
- * place of the device buffer p_dev ([B][k+1][V]; rows not needed are left untouched), then the greedy verification +
- * compaction on p_dev.  windows_host: pinned host scratch of B int32.  Same results as tetris_step_greedy_f32. */
+/* The greedy step for HOST-resident p ([B][k+1][V], pinned and device-mapped, 16-byte aligned, V % 4 == 0): the
+ * selection, then a gather kernel copies each request's verified rows p[b][0 .. windows[b]] from host memory into the
+ * same place of the device buffer p_dev ([B][k+1][V]; rows not needed are left untouched), then the greedy
+ * verification + compaction on p_dev.  No host synchronisation.  Same results as tetris_step_greedy_f32. */
 int tetris_step_greedy_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
                                   const float* p_host, const int32_t* d, const int32_t* cap, int32_t V, float* p_dev,
-                                  int32_t* windows_host, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
-                                  int32_t* out_tok, int32_t* offsets, int32_t* tokens, int64_t* stats4,
-                                  uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream);
+                                  int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                                  int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws,
+                                  size_t ws_bytes, tetris_stream_t stream);
 
 /* The greedy step in 2 launches (select1 with the row-list epilogue, then the persistent argmax stream with the
  * verdicts and the compaction; V % 8 == 0 and 16-byte aligned p, else the stage-by-stage fallback): the selection of
@@ -339,6 +340,48 @@ int tetris_sim_step(const double* truth, const int32_t* truth_len, int32_t B, in
                     int32_t* served, int32_t* arrival, double* alpha_hat, int64_t* counters, int32_t* accepted,
                     int32_t* credited, double* expected, int64_t* done_ids, int32_t* done_arrival,
                     int32_t* next_depths, uint32_t* status, tetris_stream_t stream);
+
+/* ---- request-sharded steps over NCCL (north_star: "allgather of per-shard candidates + local select")
+ * One process per GPU; rank g of W owns requests [g*B_local, (g+1)*B_local).  `nccl_comm` is the caller's ncclComm_t
+ * (cast to void*; e.g. torch ProcessGroupNCCL's, or ncclCommInitRank's); the library resolves ncclAllGather /
+ * ncclGroupStart / ncclGroupEnd / ncclCommCount / ncclCommUserRank from the libnccl.so.2 already loaded in the process
+ * (else dlopen("libnccl.so.2") or $TETRIS_NCCL_LIB) and links no NCCL itself.  The exchange is ONE NCCL group of two
+ * all-gathers on `stream`: every rank's conf [B_local][k] f64 and len [B_local] i32 into conf_all [W*B_local][k] /
+ * len_all [W*B_local] (caller-owned; len_local == NULL: all rows k, nothing gathered, and every rank must pass NULL).
+ * The selection then runs over the gathered W*B_local rows with the GLOBAL capacity C on every rank (identical
+ * inputs => identical windows_all [W*B_local] and win_offsets_all [W*B_local+1] on all ranks, equal to the
+ * single-device selection); verification, resampling and compaction cover the local rows only: p, q, zp, zq, d,
+ * u_acc (dense [B_local][k]), u_res, cap, accepted, out_tok, mass_out, offsets, tokens are the shard's.  The workspace
+ * is sized for B = W*B_local.  Capturable in a CUDA graph (NCCL supports stream capture).  The python replacement
+ * for the reference's global selection call (selector.py:133-176 over all requests) is paper_2502_15197_b200.dist. */
+int tetris_nccl_comm_info(void* nccl_comm, int32_t* rank, int32_t* world);
+int tetris_dist_gather_scores(const double* conf_local, const int32_t* len_local, int32_t B_local, int32_t k,
+                              void* nccl_comm, double* conf_all, int32_t* len_all, tetris_stream_t stream);
+int tetris_dist_select_f64(const double* vals_local, const int32_t* len_local, int32_t B_local, int32_t k, int64_t C,
+                           int32_t vals_are_cum, void* nccl_comm, double* vals_all, int32_t* len_all,
+                           int32_t* windows_all, int32_t* win_offsets_all, int64_t* stats4, uint32_t* status, void* ws,
+                           size_t ws_bytes, tetris_stream_t stream);
+int tetris_dist_step_stochastic_f32(const double* conf_local, const int32_t* len_local, int32_t B_local, int32_t k,
+                                    int64_t C, const float* p, const float* q, const int32_t* d, const double* u_acc,
+                                    const double* u_res, const int32_t* cap, int32_t V, void* nccl_comm,
+                                    double* conf_all, int32_t* len_all, int32_t* windows_all, int32_t* win_offsets_all,
+                                    int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
+                                    int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                    tetris_stream_t stream);
+int tetris_dist_step_stochastic_bf16(const double* conf_local, const int32_t* len_local, int32_t B_local, int32_t k,
+                                     int64_t C, const uint16_t* zp, const float* lse_p, const uint16_t* zq,
+                                     const float* lse_q, const int32_t* d, const double* u_acc, const double* u_res,
+                                     const int32_t* cap, int32_t V, void* nccl_comm, double* conf_all, int32_t* len_all,
+                                     int32_t* windows_all, int32_t* win_offsets_all, int32_t* accepted,
+                                     int32_t* out_tok, double* mass_out, int32_t* offsets, int32_t* tokens,
+                                     int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                     tetris_stream_t stream);
+int tetris_dist_step_greedy_f32(const double* conf_local, const int32_t* len_local, int32_t B_local, int32_t k,
+                                int64_t C, const float* p, const int32_t* d, const int32_t* cap, int32_t V,
+                                void* nccl_comm, double* conf_all, int32_t* len_all, int32_t* windows_all,
+                                int32_t* win_offsets_all, int32_t* accepted, int32_t* out_tok, int32_t* offsets,
+                                int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
+                                tetris_stream_t stream);
 
 #ifdef __cplusplus
 }

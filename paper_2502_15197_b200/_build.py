@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC",
     "-I", str(INCLUDE),
 ]
-SOURCES = ["abi.cu", "select.cu", "select1.cu", "gselect.cu", "verify.cu", "stream.cu", "greedy.cu", "compact.cu", "sim.cu"]
+SOURCES = ["abi.cu", "select.cu", "select1.cu", "gselect.cu", "verify.cu", "stream.cu", "greedy.cu", "compact.cu", "sim.cu", "dist.cu"]
 
 
 def _nvcc() -> str:
@@ -70,7 +70,7 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         objs = list(ex.map(compile_one, SOURCES))
     if force or not _newer(LIB_PATH, objs):
         tmp = LIB_PATH.with_suffix(".so.tmp")
-        cmd = [nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(tmp), *map(str, objs)]
+        cmd = [nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(tmp), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

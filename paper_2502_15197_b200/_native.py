@@ -17,6 +17,7 @@ OK = 0
 INVALID_ARGUMENT = 1
 DEGENERATE_RESIDUAL = 2
 CUDA_ERROR = 3
+NCCL_ERROR = 4
 
 ST_BAD_VALUE = 1
 ST_DEGENERATE = 2
@@ -90,12 +91,12 @@ _SIGNATURES = {
     "tetris_verify_greedy_f32": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _sz, _p]),
     "tetris_step_stochastic_staged_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
-                  _p, _sz, _p]),
+                  _sz, _p]),
     "tetris_step_stochastic_staged_bf16": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p,
-                  _p, _p, _p, _p, _p, _sz, _p]),
+                  _p, _p, _p, _sz, _p]),
     "tetris_step_greedy_staged_f32": (
-        C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+        C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "tetris_step_greedy_f32": (
         C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _i32, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz,
                   _p]),
@@ -109,6 +110,19 @@ _SIGNATURES = {
     "tetris_sim_step": (
         C.c_int, [_p, _p, _i32, _i32, _i32, _i32, _i64, C.c_double, _p, _i64, _p, _i64, _p, _p, _p, _p, _p, _p, _p,
                   _p, _p, _p, _p, _p, _p, _p, _p]),
+    "tetris_nccl_comm_info": (C.c_int, [_p, _p, _p]),
+    "tetris_dist_gather_scores": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _p, _p]),
+    "tetris_dist_select_f64": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "tetris_dist_step_stochastic_f32": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                  _p, _p, _sz, _p]),
+    "tetris_dist_step_stochastic_bf16": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                  _p, _p, _p, _p, _sz, _p]),
+    "tetris_dist_step_greedy_f32": (
+        C.c_int, [_p, _p, _i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz,
+                  _p]),
 }
 EXPORTS = tuple(_SIGNATURES)
 

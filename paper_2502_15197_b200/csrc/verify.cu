@@ -850,92 +850,81 @@ static int verify_greedy_impl(const float* p, const int32_t* d, const int32_t* w
   return offsets ? tetris_compact(accepted, out_tok, d, cap, B, k, offsets, tokens, st) : TETRIS_OK;
 }
 
+// ---- host-buffer steps: the needed host rows are gathered by SM loads of the mapped host memory ----------------
 // The stochastic step for HOST-resident p / q (the end-to-end path): the selector's accept test gathers its scalars
-// from the mapped host memory; then the row each request resamples from (rowinfo, 16 B per request) comes back to
-// the host, the host queues one DMA copy per needed row into `staging` on the copy engines (which read host memory
-// at ~55 GB/s on this box, vs ~50 for SM-issued zero-copy reads), rewrites rowinfo as staging rows, and the sampler
-// runs on device memory.  Blocking: the host waits for the selection (one stream synchronize).
-// ---- host-buffer steps: the needed host rows are copied by the DMA engines --------------------------------------
-// The copies are spread over kCopyStreams streams (forked from / joined to the caller's stream with events) so several
-// copy engines work at once and each copy's set-up overlaps the others' transfers.  The streams and events are created
-// once per (host thread, device): a thread that later drives another GPU gets that device's own set.
-constexpr int kCopyStreams = 8;
-constexpr int kMaxDevices = 64;
-struct CopyLanes {
-  cudaStream_t cs[kCopyStreams];
-  cudaEvent_t ev[kCopyStreams + 1];
-  bool ready;
-};
-
-static int copy_lanes(CopyLanes** out) {
-  static thread_local CopyLanes lanes[kMaxDevices] = {};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return abi::cuda_fail(e);
-  if (dev < 0 || dev >= kMaxDevices) return abi::fail(TETRIS_INVALID_ARGUMENT, "device %d >= %d", dev, kMaxDevices);
-  CopyLanes& L = lanes[dev];
-  if (!L.ready) {
-    for (int i = 0; i < kCopyStreams; ++i)
-      if ((e = cudaStreamCreateWithFlags(&L.cs[i], cudaStreamNonBlocking)) != cudaSuccess) return abi::cuda_fail(e);
-    for (int i = 0; i <= kCopyStreams; ++i)
-      if ((e = cudaEventCreateWithFlags(&L.ev[i], cudaEventDisableTiming)) != cudaSuccess) return abi::cuda_fail(e);
-    L.ready = true;
+// from the mapped host memory; then stage_rows_kernel copies the row each request resamples from (rowinfo, left in the
+// workspace by the selector epilogue) from the mapped host tensors into `staging` (request b: rows 2b, 2b+1) and
+// rewrites rowinfo as staging rows, and the sampler runs on device memory.  Everything stays stream-ordered: no host
+// synchronisation, capturable in a CUDA graph.  Measured on this box (tools/micro/h2d_rows.cu, 1800 rows of 513 KB):
+// SM gather 51 GB/s, one cudaMemcpyAsync per row 37 GB/s (a ~4.5 us fixed cost per copy on the copy engine, whatever
+// the stream count), one contiguous copy 55 GB/s (the link's ceiling, not reachable for scattered rows).
+__device__ __forceinline__ void copy_row_h2d(const int4* __restrict__ src, int4* __restrict__ dst, long long words) {
+  constexpr int U = 4;  // 16-byte loads in flight per thread
+  for (long long i = threadIdx.x; i < words; i += U * blockDim.x) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * blockDim.x < words) v[u] = __ldcv(src + i + u * blockDim.x);  // host memory: never a stale line
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * blockDim.x < words) dst[i + u * blockDim.x] = v[u];
   }
-  *out = &L;
-  return TETRIS_OK;
 }
 
-static int copy_h2d_batched(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<size_t>& sizes,
-                            cudaStream_t st) {
-  CopyLanes* L = nullptr;
-  int rc = copy_lanes(&L);
-  if (rc) return rc;
-  cudaError_t e;
-  if ((e = cudaEventRecord(L->ev[kCopyStreams], st)) != cudaSuccess) return abi::cuda_fail(e);
-  const size_t n = dsts.size();
-  for (int i = 0; i < kCopyStreams; ++i) {
-    if ((e = cudaStreamWaitEvent(L->cs[i], L->ev[kCopyStreams], 0)) != cudaSuccess) return abi::cuda_fail(e);
-    const size_t lo = n * i / kCopyStreams, hi = n * (i + 1) / kCopyStreams;
-    if (hi > lo) {
-      cudaMemcpyAttributes attr = {};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t attr_idx = 0, fail_idx = 0;
-      e = cudaMemcpyBatchAsync(dsts.data() + lo, srcs.data() + lo, sizes.data() + lo, hi - lo, &attr, &attr_idx, 1,
-                               &fail_idx, L->cs[i]);
-      if (e != cudaSuccess) {  // older driver: one copy at a time
-        cudaGetLastError();
-        for (size_t j = lo; j < hi; ++j)
-          if ((e = cudaMemcpyAsync(dsts[j], srcs[j], sizes[j], cudaMemcpyHostToDevice, L->cs[i])) != cudaSuccess)
-            return abi::cuda_fail(e);
-      }
+// item 2b + t: request b's p row (t = 0) or q row (t = 1, absent for a bonus row) into staging row 2b + t
+__global__ void __launch_bounds__(512) stage_rows_kernel(const char* __restrict__ p_map, const char* __restrict__ q_map,
+                                                         const float* __restrict__ lsep_map,
+                                                         const float* __restrict__ lseq_map, long long* rowinfo,
+                                                         int B, long long row_bytes, char* staging,
+                                                         float* lse_staging) {
+  for (int it = blockIdx.x; it < 2 * B; it += gridDim.x) {
+    const int b = it >> 1, t = it & 1;
+    const long long r = rowinfo[2 * b + t];
+    if (r < 0) continue;  // bonus: no q row
+    copy_row_h2d((const int4*)((t ? q_map : p_map) + r * row_bytes), (int4*)(staging + (long long)it * row_bytes),
+                 row_bytes / 16);
+    __syncthreads();  // every thread has read rowinfo[it] before it is rewritten
+    if (threadIdx.x == 0) {
+      if (lse_staging) lse_staging[it] = (t ? lseq_map : lsep_map)[r];
+      rowinfo[2 * b + t] = it;
     }
-    if ((e = cudaEventRecord(L->ev[i], L->cs[i])) != cudaSuccess) return abi::cuda_fail(e);
-    if ((e = cudaStreamWaitEvent(st, L->ev[i], 0)) != cudaSuccess) return abi::cuda_fail(e);
   }
-  return TETRIS_OK;
 }
 
-// The host-buffer stochastic step, either input form (T = float probabilities, or uint16_t bf16 logits with their
-// host-resident lse): selection + accept test reading the scalars through the mapping, then (host waits for it) one DMA
-// copy per needed row into `staging`, then the sampler on device memory.  Logits form: the staged rows' lse go to
-// lse_staging (device, [2B]) through the pinned lse_host_scratch ([2B]); the producer's per-request lse pairs were
-// already written by the selector epilogue (values, so the row renumbering does not touch them).
+// greedy: item b*(k+1) + j copies p[b][j] for j <= windows[b] into the same place of p_dev
+__global__ void __launch_bounds__(512) stage_greedy_rows_kernel(const char* __restrict__ p_map,
+                                                                const int32_t* __restrict__ windows, int B, int k,
+                                                                long long row_bytes, char* p_dev) {
+  const int n = B * (k + 1);
+  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+    const int b = it / (k + 1), j = it - b * (k + 1);
+    if (j > windows[b]) continue;
+    copy_row_h2d((const int4*)(p_map + (long long)it * row_bytes), (int4*)(p_dev + (long long)it * row_bytes),
+                 row_bytes / 16);
+  }
+}
+
+static int stage_grid(long long items) {
+  const long long g = 4LL * abi::device_sm_count();
+  return (int)(items < g ? (items > 0 ? items : 1) : g);
+}
+
 template <typename T>
 static int staged_impl(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C, const T* p_host,
                        const T* q_host, const float* lsep_host, const float* lseq_host, const int32_t* d,
                        const double* u_acc, const double* u_res, const int32_t* cap, int32_t V, T* staging,
-                       float* lse_staging, float* lse_host_scratch, int64_t* rowinfo_host, int32_t* windows,
-                       int32_t* win_offsets, int32_t* accepted, int32_t* out_tok, double* mass_out, int32_t* offsets,
-                       int32_t* tokens, int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
-                       tetris_stream_t stream) {
+                       float* lse_staging, int32_t* windows, int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                       double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status,
+                       void* ws, size_t ws_bytes, tetris_stream_t stream) {
   constexpr bool kLogits = sizeof(T) == 2;
   int rc = check_shape(B, k, V);
   if (rc) return rc;
-  if (!p_host || (k > 0 && !q_host) || !staging || !rowinfo_host ||
-      (kLogits && (!lsep_host || (k > 0 && !lseq_host) || !lse_staging || !lse_host_scratch)))
+  if (!p_host || (k > 0 && !q_host) || !staging ||
+      (kLogits && (!lsep_host || (k > 0 && !lseq_host) || !lse_staging)))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
-  if (V % 8 != 0 || !aligned16(staging))
-    return abi::fail(TETRIS_INVALID_ARGUMENT, "staged step needs V %% 8 == 0 and a 16-byte aligned staging buffer");
+  if (V % 8 != 0 || !aligned16(staging) || !aligned16(p_host) || (q_host && !aligned16(q_host)))
+    return abi::fail(TETRIS_INVALID_ARGUMENT,
+                     "staged step needs V %% 8 == 0 and 16-byte aligned host tensors and staging buffer");
   cudaStream_t st = (cudaStream_t)stream;
   void *p_map = nullptr, *q_map = nullptr, *lp_map = nullptr, *lq_map = nullptr;
   cudaError_t e = cudaHostGetDevicePointer(&p_map, (void*)p_host, 0);
@@ -949,39 +938,13 @@ static int staged_impl(const double* conf, const int32_t* len, int32_t B, int32_
   if ((rc = select_accept_impl(conf, len, B, k, C, 0, B, mapped, d, u_acc, 0, cap, V, windows, win_offsets, accepted,
                                offsets, tokens, stats4, status, ws, ws_bytes, stream)))
     return rc;
+  // the rows the selection chose, host -> staging (request b: rows 2b, 2b+1), rowinfo rewritten as staging rows
   long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
-  const size_t ri_bytes = (size_t)B * 2 * sizeof(long long);
-  if ((e = cudaMemcpyAsync(rowinfo_host, rowinfo, ri_bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-      (e = cudaStreamSynchronize(st)) != cudaSuccess)
-    return abi::cuda_fail(e);
-  // one copy per needed row, in request order; rowinfo rewritten as staging rows
-  const size_t row_bytes = (size_t)V * sizeof(T);
-  std::vector<void*> dsts, srcs;
-  std::vector<size_t> sizes;
-  dsts.reserve(2 * (size_t)B);
-  srcs.reserve(2 * (size_t)B);
-  long long s = 0;
-  for (int b = 0; b < B; ++b) {
-    const long long pr = rowinfo_host[2 * b], qr = rowinfo_host[2 * b + 1];
-    dsts.push_back(staging + s * V);
-    srcs.push_back((void*)(p_host + pr * V));
-    if (kLogits) lse_host_scratch[s] = lsep_host[pr];
-    rowinfo_host[2 * b] = s++;
-    if (qr >= 0) {
-      dsts.push_back(staging + s * V);
-      srcs.push_back((void*)(q_host + qr * V));
-      if (kLogits) lse_host_scratch[s] = lseq_host[qr];
-      rowinfo_host[2 * b + 1] = s++;
-    }
-  }
-  sizes.assign(dsts.size(), row_bytes);
-  if ((rc = copy_h2d_batched(dsts, srcs, sizes, st))) return rc;
-  if ((e = cudaMemcpyAsync(rowinfo, rowinfo_host, ri_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
-    return abi::cuda_fail(e);
-  if (kLogits &&
-      (e = cudaMemcpyAsync(lse_staging, lse_host_scratch, (size_t)s * sizeof(float), cudaMemcpyHostToDevice, st)) !=
-          cudaSuccess)
-    return abi::cuda_fail(e);
+  stage_rows_kernel<<<stage_grid(2LL * B), 512, 0, st>>>((const char*)p_map, (const char*)q_map,
+                                                         (const float*)lp_map, (const float*)lq_map, rowinfo, B,
+                                                         (long long)V * sizeof(T), (char*)staging,
+                                                         kLogits ? lse_staging : nullptr);
+  if ((rc = abi::launch_check())) return rc;
   const ProbIn staged = kLogits ? ProbIn{nullptr, nullptr, (const uint16_t*)staging, (const uint16_t*)staging,
                                          lse_staging, lse_staging}
                                 : ProbIn{(const float*)staging, (const float*)staging, nullptr, nullptr, nullptr,
@@ -993,30 +956,28 @@ static int staged_impl(const double* conf, const int32_t* len, int32_t B, int32_
 extern "C" int tetris_step_stochastic_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k,
                                                  int64_t C, const float* p_host, const float* q_host,
                                                  const int32_t* d, const double* u_acc, const double* u_res,
-                                                 const int32_t* cap, int32_t V, float* staging,
-                                                 int64_t* rowinfo_host, int32_t* windows, int32_t* win_offsets,
-                                                 int32_t* accepted, int32_t* out_tok, double* mass_out,
-                                                 int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                                 const int32_t* cap, int32_t V, float* staging, int32_t* windows,
+                                                 int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
+                                                 double* mass_out, int32_t* offsets, int32_t* tokens, int64_t* stats4,
                                                  uint32_t* status, void* ws, size_t ws_bytes,
                                                  tetris_stream_t stream) {
   return staged_impl<float>(conf, len, B, k, C, p_host, q_host, nullptr, nullptr, d, u_acc, u_res, cap, V, staging,
-                            nullptr, nullptr, rowinfo_host, windows, win_offsets, accepted, out_tok, mass_out,
-                            offsets, tokens, stats4, status, ws, ws_bytes, stream);
+                            nullptr, windows, win_offsets, accepted, out_tok, mass_out, offsets, tokens, stats4,
+                            status, ws, ws_bytes, stream);
 }
 
 extern "C" int tetris_step_stochastic_staged_bf16(const double* conf, const int32_t* len, int32_t B, int32_t k,
                                                   int64_t C, const uint16_t* zp_host, const float* lse_p_host,
                                                   const uint16_t* zq_host, const float* lse_q_host, const int32_t* d,
                                                   const double* u_acc, const double* u_res, const int32_t* cap,
-                                                  int32_t V, uint16_t* staging, float* lse_staging,
-                                                  float* lse_host_scratch, int64_t* rowinfo_host, int32_t* windows,
+                                                  int32_t V, uint16_t* staging, float* lse_staging, int32_t* windows,
                                                   int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
                                                   double* mass_out, int32_t* offsets, int32_t* tokens,
                                                   int64_t* stats4, uint32_t* status, void* ws, size_t ws_bytes,
                                                   tetris_stream_t stream) {
   return staged_impl<uint16_t>(conf, len, B, k, C, zp_host, zq_host, lse_p_host, lse_q_host, d, u_acc, u_res, cap, V,
-                               staging, lse_staging, lse_host_scratch, rowinfo_host, windows, win_offsets, accepted,
-                               out_tok, mass_out, offsets, tokens, stats4, status, ws, ws_bytes, stream);
+                               staging, lse_staging, windows, win_offsets, accepted, out_tok, mass_out, offsets,
+                               tokens, stats4, status, ws, ws_bytes, stream);
 }
 
 // The greedy step (select -> greedy verification -> compaction) in 2 launches when the selector is the single-CTA one
@@ -1184,46 +1145,34 @@ extern "C" int tetris_residual_f64(const double* p_draft, const double* p_target
   return abi::launch_check();
 }
 
-// The greedy step for host-resident p: selection, then one DMA copy per request of its verified rows p[b][0..w_b]
-// (contiguous in host memory) into the same place of p_dev, then the greedy verification + compaction on p_dev.
+// The greedy step for host-resident p: selection, then stage_greedy_rows_kernel copies each request's verified rows
+// p[b][0..w_b] from the mapped host tensor into the same place of p_dev, then the greedy verification + compaction
+// on p_dev.  Stream-ordered, no host synchronisation.
 extern "C" int tetris_step_greedy_staged_f32(const double* conf, const int32_t* len, int32_t B, int32_t k, int64_t C,
                                              const float* p_host, const int32_t* d, const int32_t* cap, int32_t V,
-                                             float* p_dev, int32_t* windows_host, int32_t* windows,
-                                             int32_t* win_offsets, int32_t* accepted, int32_t* out_tok,
-                                             int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status,
-                                             void* ws, size_t ws_bytes, tetris_stream_t stream) {
+                                             float* p_dev, int32_t* windows, int32_t* win_offsets, int32_t* accepted,
+                                             int32_t* out_tok, int32_t* offsets, int32_t* tokens, int64_t* stats4,
+                                             uint32_t* status, void* ws, size_t ws_bytes, tetris_stream_t stream) {
   using namespace tetris;
   int rc = check_shape(B, k, V);
   if (rc) return rc;
   if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
   if (B == 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "empty batch");
-  if ((k > 0 && (!conf || !d)) || !p_host || !p_dev || !windows_host || !windows || !accepted || !out_tok ||
-      !offsets || !tokens)
+  if ((k > 0 && (!conf || !d)) || !p_host || !p_dev || !windows || !accepted || !out_tok || !offsets || !tokens)
     return abi::fail(TETRIS_INVALID_ARGUMENT, "null argument");
+  if (V % 4 != 0 || !aligned16(p_dev) || !aligned16(p_host))
+    return abi::fail(TETRIS_INVALID_ARGUMENT, "staged greedy step needs V %% 4 == 0 and 16-byte aligned p_host, p_dev");
   if ((rc = check_verify_ws(B, k, V, ws, ws_bytes))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  void* p_map = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&p_map, (void*)p_host, 0);
+  if (e != cudaSuccess) return abi::cuda_fail(e);
   if ((rc = tetris_select_f64(conf, len, B, k, C, 0, windows, win_offsets, nullptr, stats4, status, ws, ws_bytes,
                               stream)))
     return rc;
-  cudaError_t e;
-  if ((e = cudaMemcpyAsync(windows_host, windows, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToHost, st)) !=
-          cudaSuccess ||
-      (e = cudaStreamSynchronize(st)) != cudaSuccess)
-    return abi::cuda_fail(e);
-  const size_t req_elems = (size_t)(k + 1) * V;
-  std::vector<void*> dsts, srcs;
-  std::vector<size_t> sizes;
-  dsts.reserve(B);
-  srcs.reserve(B);
-  sizes.reserve(B);
-  for (int b = 0; b < B; ++b) {
-    int w = windows_host[b];
-    w = w < 0 ? 0 : (w > k ? k : w);
-    dsts.push_back(p_dev + (size_t)b * req_elems);
-    srcs.push_back((void*)(p_host + (size_t)b * req_elems));
-    sizes.push_back((size_t)(w + 1) * V * sizeof(float));
-  }
-  if ((rc = copy_h2d_batched(dsts, srcs, sizes, st))) return rc;
+  stage_greedy_rows_kernel<<<stage_grid((long long)B * (k + 1)), 512, 0, st>>>(
+      (const char*)p_map, windows, B, k, (long long)V * sizeof(float), (char*)p_dev);
+  if ((rc = abi::launch_check())) return rc;
   return verify_greedy_impl(p_dev, d, windows, cap, B, k, V, accepted, out_tok, offsets, tokens, status, ws, ws_bytes,
                             st);
 }

@@ -427,7 +427,14 @@ class TetrisStep:
                 raise ValueError(f"shard rank {self.rank} outside world {self.world}")
         Bg = B * self.world
         self.Bg = Bg
-        if self.world > 1:
+        # NCCL groups: the exchange and the step are ONE native call (tetris_dist_step_*, csrc/dist.cu) on the
+        # torch communicator; other backends (gloo tests) gather in Python (dist.gather_scores)
+        self._comm = None
+        if group is not None:
+            from .dist import nccl_comm
+
+            self._comm = nccl_comm(group, dev)
+        if self.world > 1 or self._comm is not None:
             if u_layout != "dense":
                 raise ValueError("sharded steps use the dense uniform layout")
             self.conf_all = torch.zeros(Bg, k, dtype=_F64, device=dev)
@@ -458,9 +465,10 @@ class TetrisStep:
         if self.policy == "fixed":
             self._run_fixed(lengths, p, q, d, u_acc, u_res, cap, events, window)
             return
+        if self._comm is not None and events is None and self._dist_native(p, q):
+            self._run_dist(conf, lengths, p, q, d, u_acc, u_res, cap)
+            return
         if self.world > 1 and self.group is not None:
-            import torch.distributed as dist
-
             from .dist import gather_scores
 
             gather_scores(self.conf_all, self.len_all, conf, lengths, self.group)  # one coalesced NCCL exchange
@@ -554,6 +562,34 @@ class TetrisStep:
             self.status.data_ptr(), ws.ptr, ws.nbytes, s)
         self._check(rc)
 
+    def _dist_native(self, p, q) -> bool:
+        """The native sharded step serves the dense-uniform TETRIS step; the stochastic form needs the TMA sampler's
+        V % 8 == 0 and 16-byte aligned p / q (the greedy step falls back inside the library)."""
+        if self.u_layout != "dense" or self.policy != "tetris":
+            return False
+        return self.mode == "greedy" or (self.V % 8 == 0 and p.data_ptr() % 16 == 0 and q.data_ptr() % 16 == 0)
+
+    def _run_dist(self, conf, lengths, p, q, d, u_acc, u_res, cap) -> None:
+        """Request-sharded step over NCCL in one library call: the score all-gather (one NCCL group on the current
+        stream), the global selection over the gathered rows, this rank's verification and compaction."""
+        lib, ws, s = self._lib, self.ws, torch.cuda.current_stream().cuda_stream
+        B, k, V = self.B, self.k, self.V
+        len_all = None if lengths is None else self.len_all
+        if self.mode == "stochastic":
+            rc = lib.tetris_dist_step_stochastic_f32(
+                conf.data_ptr(), _ptr(lengths), B, k, self.C, p.data_ptr(), q.data_ptr(), d.data_ptr(),
+                u_acc.data_ptr(), u_res.data_ptr(), _ptr(cap), V, self._comm, self.conf_all.data_ptr(), _ptr(len_all),
+                self.windows_all.data_ptr(), self.win_offsets.data_ptr(), self.accepted.data_ptr(),
+                self.out_tok.data_ptr(), self.mass.data_ptr(), self.offsets.data_ptr(), self.tokens.data_ptr(),
+                self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        else:
+            rc = lib.tetris_dist_step_greedy_f32(
+                conf.data_ptr(), _ptr(lengths), B, k, self.C, p.data_ptr(), _ptr(d), _ptr(cap), V, self._comm,
+                self.conf_all.data_ptr(), _ptr(len_all), self.windows_all.data_ptr(), self.win_offsets.data_ptr(),
+                self.accepted.data_ptr(), self.out_tok.data_ptr(), self.offsets.data_ptr(), self.tokens.data_ptr(),
+                self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s)
+        self._check(rc)
+
     def run_logits(self, conf, lengths, zp, lse_p, zq, lse_q, d, u_acc, u_res, cap=None, events=None) -> None:
         """The stochastic step on LOGITS: zp [B, k+1, V] / zq [B, k, V] bf16 logits with their row
         log-sum-exp lse_p [B, k+1] / lse_q [B, k] f32 (the LM head's softmax normaliser); every probability is the
@@ -574,6 +610,15 @@ class TetrisStep:
         lib, ws, s = self._lib, self.ws, torch.cuda.current_stream().cuda_stream
         if events is not None:
             events[0].record()
+        if self._comm is not None and events is None and self.u_layout == "dense":
+            len_all = None if lengths is None else self.len_all
+            self._check(lib.tetris_dist_step_stochastic_bf16(
+                conf.data_ptr(), _ptr(lengths), B, k, self.C, zp.data_ptr(), lse_p.data_ptr(), zq.data_ptr(),
+                lse_q.data_ptr(), d.data_ptr(), u_acc.data_ptr(), u_res.data_ptr(), _ptr(cap), V, self._comm,
+                self.conf_all.data_ptr(), _ptr(len_all), self.windows_all.data_ptr(), self.win_offsets.data_ptr(),
+                self.accepted.data_ptr(), self.out_tok.data_ptr(), self.mass.data_ptr(), self.offsets.data_ptr(),
+                self.tokens.data_ptr(), self.stats.data_ptr(), self.status.data_ptr(), ws.ptr, ws.nbytes, s))
+            return
         if self.world > 1 and self.group is not None:
             from .dist import gather_scores
 
@@ -711,19 +756,20 @@ class HostTetrisStep:
 
     def __init__(self, B: int, k: int, V: int, capacity: int, p_host: torch.Tensor, q_host: Optional[torch.Tensor],
                  mode: str = "stochastic", device="cuda", transfer: str = "staged"):
-        """transfer: "staged" (after the selection the needed rows are copied host->device by the DMA engines --
-        tetris_step_stochastic_staged_f32: the residual / bonus row of each request into a [2B, V] staging buffer;
-        tetris_step_greedy_staged_f32: rows 0..w_b of each request into their place of a [B, k+1, V] device copy;
-        the host waits for the selection) or "zero-copy" (the kernels read the rows from pinned host memory; no host
-        wait).  q_host may be None (or empty) when k == 0 or mode == "greedy"."""
+        """transfer: "staged" (after the selection a gather kernel copies the needed rows host->device over the
+        mapping -- tetris_step_stochastic_staged_f32: the residual / bonus row of each request into a [2B, V] staging
+        buffer; tetris_step_greedy_staged_f32: rows 0..w_b of each request into their place of a [B, k+1, V] device
+        copy) or "zero-copy" (the streaming kernels read the rows from pinned host memory themselves).  Neither waits
+        on the host.  q_host may be None (or empty) when k == 0 or mode == "greedy"."""
         if transfer not in ("staged", "zero-copy"):
             raise ValueError(f"transfer must be 'staged' or 'zero-copy', got {transfer!r}")
         self.step = TetrisStep(B, k, V, capacity, mode=mode, device=device)
         dev = self.step.device
         self.mode = mode
-        # the staged stochastic path feeds the TMA sampler (32-byte rows): other vocabulary sizes read through the
-        # mapping
-        self.transfer = transfer if (mode == "greedy" or V % 8 == 0) else "zero-copy"
+        # the staged paths copy 16-byte words and the stochastic one feeds the TMA sampler (32-byte rows): other
+        # vocabulary sizes and misaligned views read through the mapping
+        aligned = p_host.data_ptr() % 16 == 0 and (q_host is None or q_host.numel() == 0 or q_host.data_ptr() % 16 == 0)
+        self.transfer = transfer if aligned and V % (4 if mode == "greedy" else 8) == 0 else "zero-copy"
         if q_host is not None and q_host.numel() == 0:
             q_host = None
         if mode == "stochastic" and k > 0 and q_host is None:
@@ -734,10 +780,8 @@ class HostTetrisStep:
         self.q = _MappedTensor(q_host) if q_host is not None else torch.empty(B, 0, V, dtype=_F32, device=dev)
         if self.transfer == "staged" and mode == "stochastic":
             self.staging = torch.empty(2 * B, V, dtype=torch.float32, device=dev)
-            self.rowinfo_host = torch.empty(2 * B, dtype=_I64).pin_memory()
         elif self.transfer == "staged":
             self.p_dev = torch.empty(B, k + 1, V, dtype=torch.float32, device=dev)
-            self.windows_host = torch.empty(B, dtype=_I32).pin_memory()
         self.conf = torch.empty(B, k, dtype=_F64, device=dev)
         self.lengths = torch.empty(B, dtype=_I32, device=dev)
         self.d = torch.empty(B, k, dtype=_I32, device=dev)
@@ -770,15 +814,14 @@ class HostTetrisStep:
             st._check(st._lib.tetris_step_stochastic_staged_f32(
                 self.conf.data_ptr(), self.lengths.data_ptr(), self.B, self.k, st.C, self.p_host.data_ptr(),
                 _ptr(self.q_host), self.d.data_ptr(), self.u_acc.data_ptr(), self.u_res.data_ptr(), None,
-                self.V, self.staging.data_ptr(), self.rowinfo_host.data_ptr(), st.windows_all.data_ptr(),
+                self.V, self.staging.data_ptr(), st.windows_all.data_ptr(),
                 st.win_offsets.data_ptr(), st.accepted.data_ptr(), st.out_tok.data_ptr(), st.mass.data_ptr(),
                 st.offsets.data_ptr(), st.tokens.data_ptr(), st.stats.data_ptr(), st.status.data_ptr(), st.ws.ptr,
                 st.ws.nbytes, s))
         elif self.transfer == "staged" and st.group is None:
             st._check(st._lib.tetris_step_greedy_staged_f32(
                 self.conf.data_ptr(), self.lengths.data_ptr(), self.B, self.k, st.C, self.p_host.data_ptr(),
-                self.d.data_ptr(), None, self.V, self.p_dev.data_ptr(), self.windows_host.data_ptr(),
-                st.windows_all.data_ptr(), st.win_offsets.data_ptr(), st.accepted.data_ptr(), st.out_tok.data_ptr(),
+                self.d.data_ptr(), None, self.V, self.p_dev.data_ptr(), st.windows_all.data_ptr(), st.win_offsets.data_ptr(), st.accepted.data_ptr(), st.out_tok.data_ptr(),
                 st.offsets.data_ptr(), st.tokens.data_ptr(), st.stats.data_ptr(), st.status.data_ptr(), st.ws.ptr,
                 st.ws.nbytes, s))
         else:
@@ -790,8 +833,8 @@ class HostTetrisStep:
 
 class HostLogitStep:
     """HostTetrisStep for LOGITS: zp_host [B, k+1, V] / zq_host [B, k, V] bf16 and lse_p_host [B, k+1] / lse_q_host
-    [B, k] f32 in pinned host memory (tetris_step_stochastic_staged_bf16: after the selection the needed bf16 rows are
-    copied host->device by the DMA engines -- half the host-link bytes of the fp32 form)."""
+    [B, k] f32 in pinned host memory (tetris_step_stochastic_staged_bf16: after the selection a gather kernel copies
+    the needed bf16 rows host->device -- half the host-link bytes of the fp32 form)."""
 
     def __init__(self, B: int, k: int, V: int, capacity: int, zp_host: torch.Tensor, lse_p_host: torch.Tensor,
                  zq_host: torch.Tensor, lse_q_host: torch.Tensor, device="cuda"):
@@ -808,8 +851,6 @@ class HostLogitStep:
         self.host = (zp_host, lse_p_host, zq_host, lse_q_host)
         self.staging = torch.empty(2 * B, V, dtype=torch.bfloat16, device=dev)
         self.lse_staging = torch.empty(2 * B, dtype=_F32, device=dev)
-        self.lse_scratch = torch.empty(2 * B, dtype=_F32).pin_memory()
-        self.rowinfo_host = torch.empty(2 * B, dtype=_I64).pin_memory()
         self.conf = torch.empty(B, k, dtype=_F64, device=dev)
         self.lengths = torch.empty(B, dtype=_I32, device=dev)
         self.d = torch.empty(B, k, dtype=_I32, device=dev)
@@ -836,8 +877,7 @@ class HostLogitStep:
         st._check(st._lib.tetris_step_stochastic_staged_bf16(
             self.conf.data_ptr(), self.lengths.data_ptr(), self.B, self.k, st.C, zp.data_ptr(), lp.data_ptr(),
             zq.data_ptr(), lq.data_ptr(), self.d.data_ptr(), self.u_acc.data_ptr(), self.u_res.data_ptr(), None,
-            self.V, self.staging.data_ptr(), self.lse_staging.data_ptr(), self.lse_scratch.data_ptr(),
-            self.rowinfo_host.data_ptr(), st.windows_all.data_ptr(), st.win_offsets.data_ptr(), st.accepted.data_ptr(),
+            self.V, self.staging.data_ptr(), self.lse_staging.data_ptr(), st.windows_all.data_ptr(), st.win_offsets.data_ptr(), st.accepted.data_ptr(),
             st.out_tok.data_ptr(), st.mass.data_ptr(), st.offsets.data_ptr(), st.tokens.data_ptr(),
             st.stats.data_ptr(), st.status.data_ptr(), st.ws.ptr, st.ws.nbytes, torch.cuda.current_stream().cuda_stream))
         self.offsets_host.copy_(st.offsets, non_blocking=True)

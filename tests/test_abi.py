@@ -25,6 +25,24 @@ def test_library_loads_and_exports_header_symbols():
     assert lib.tetris_abi_version() == 1
 
 
+def test_ctypes_signatures_match_header_prototypes():
+    """Every argument of every prototype has the ctypes type of its C type (a wrong arity or width would pass garbage
+    through ctypes silently)."""
+    import ctypes as C
+
+    txt = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    kinds = {"int32_t": C.c_int32, "int64_t": C.c_int64, "size_t": C.c_size_t, "int": C.c_int, "double": C.c_double,
+             "tetris_stream_t": C.c_void_p}
+    n = 0
+    for m in re.finditer(r"\b(?:int|size_t|const char\*)\s+(tetris_\w+)\s*\(([^)]*)\)\s*;", txt):
+        name, args = m.group(1), m.group(2).strip()
+        params = [] if args in ("", "void") else [a.strip() for a in args.split(",")]
+        want = [C.POINTER(C.c_void_p) if "**" in a else C.c_void_p if "*" in a else kinds[a.rsplit(None, 1)[0].replace("const ", "")] for a in params]
+        assert list(N._SIGNATURES[name][1]) == want, name
+        n += 1
+    assert n == len(N.EXPORTS)
+
+
 def test_cubin_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", str(N.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
@@ -97,7 +115,24 @@ def test_batched_entry_points_reject_bad_arguments_without_gpu():
         lambda: N.call("tetris_resample_spec_f32", 1, 1, 1, None, None, 4, 2, 128, None, None, None, 1, None, None,
                        None, None, 0, None),
         lambda: N.call("tetris_step_stochastic_staged_f32", None, None, 4, 2, 3, None, None, None, None, None, None,
-                       128, None, None, None, None, None, None, None, None, None, None, None, None, 0, None),
+                       128, None, None, None, None, None, None, None, None, None, None, None, 0, None),
+        lambda: N.call("tetris_step_greedy_staged_f32", None, None, 4, 2, 3, None, None, None, 128, None, None, None,
+                       None, None, None, None, None, None, None, 0, None),
     ):
         with pytest.raises(ValueError):
             call()
+
+
+def test_nccl_binding_resolves_without_gpu():
+    """The sharded entry points resolve NCCL at run time (no link-time dependency): with the process's libnccl found,
+    a null communicator is an argument error, not a load failure."""
+    import ctypes as C
+
+    import torch  # noqa: F401  (loads torch's libnccl.so.2 into the process, as under Python on the GPU box)
+
+    lib = N.load()
+    r, w = C.c_int32(), C.c_int32()
+    assert lib.tetris_nccl_comm_info(None, C.byref(r), C.byref(w)) == N.INVALID_ARGUMENT
+    assert b"communicator" in lib.tetris_last_error()
+    assert lib.tetris_dist_select_f64(None, None, 0, 4, 8, 0, None, None, None, None, None, None, None, None, 0,
+                                      None) == N.INVALID_ARGUMENT

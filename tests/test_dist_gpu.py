@@ -111,3 +111,94 @@ def test_nccl_coalesced_score_exchange():
     p.join(240)
     assert p.exitcode == 0
     assert q.get(timeout=5) is True
+
+
+def _native_dist_worker(port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        import ctypes as C
+
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+        from paper_2502_15197_b200 import _native as N
+        from paper_2502_15197_b200 import ops
+        from paper_2502_15197_b200.dist import dist_select, nccl_comm
+        from paper_2502_15197_b200.synthetic import make_batch, make_logit_batch
+
+        grp = dist.group.WORLD
+        comm = nccl_comm(grp, "cuda:0")
+        r, w = C.c_int32(-1), C.c_int32(-1)
+        N.call("tetris_nccl_comm_info", comm, C.byref(r), C.byref(w))
+        fails = [] if (r.value, w.value) == (0, 1) else [f"comm info {(r.value, w.value)}"]
+        names = ("windows_all", "win_offsets", "accepted", "out_tok", "offsets", "tokens", "stats", "status")
+        # fused one-launch (small), two-launch + speculative (mid), the grid selector (B*k > 16384), greedy
+        for B, k, V, C_, mode in ((16, 5, 32000, 48, "greedy"), (256, 8, 32000, 1024, "stochastic"),
+                                  (1024, 16, 16384, 8192, "stochastic"), (2048, 16, 8192, 16384, "stochastic"),
+                                  (300, 8, 4096, 1200, "greedy")):
+            bt = make_batch(B, k, V, mode=mode, seed=B + k, ragged=True, device="cuda:0")
+            ref = ops.TetrisStep(B, k, V, C_, mode=mode, device="cuda:0")
+            nat = ops.TetrisStep(B, k, V, C_, mode=mode, device="cuda:0", group=grp)
+            args = (bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+            ref.run(*args)
+            nat.run(*args)
+            torch.cuda.synchronize()
+            for n in names:
+                if not torch.equal(getattr(ref, n), getattr(nat, n)):
+                    fails.append(f"{mode} B={B} k={k}: {n}")
+            # the same native sharded step captured in a CUDA graph (NCCL under stream capture), replayed
+            for n in names:
+                getattr(nat, n).zero_()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                nat.run(*args)
+            torch.cuda.current_stream().wait_stream(cs)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                nat.run(*args)
+            for n in names:
+                getattr(nat, n).zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            for n in names:
+                if not torch.equal(getattr(ref, n), getattr(nat, n)):
+                    fails.append(f"graph {mode} B={B} k={k}: {n}")
+        # logits form
+        lb = make_logit_batch(256, 8, 32000, seed=3, device="cuda:0")
+        ref = ops.TetrisStep(256, 8, 32000, 1024, device="cuda:0")
+        nat = ops.TetrisStep(256, 8, 32000, 1024, device="cuda:0", group=grp)
+        for s in (ref, nat):
+            s.run_logits(lb.conf, lb.lengths, lb.zp, lb.lse_p, lb.zq, lb.lse_q, lb.d, lb.u_acc, lb.u_res)
+        torch.cuda.synchronize()
+        fails += [f"logits: {n}" for n in names if not torch.equal(getattr(ref, n), getattr(nat, n))]
+        # the selection alone
+        bt = make_batch(4096, 16, 64, seed=9, ragged=True, device="cuda:0")
+        sel = dist_select(bt.conf, 20000, bt.lengths, group=grp)
+        want = ops.select(bt.conf, 20000, bt.lengths).windows
+        torch.cuda.synchronize()
+        if not torch.equal(sel.global_windows, want):
+            fails.append("dist_select")
+        q.put(fails)
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported through the queue
+        import traceback
+
+        q.put([traceback.format_exc()])
+
+
+def test_native_nccl_sharded_step_world1():
+    """The native sharded entry points (tetris_dist_*: NCCL all-gather of the scores on the torch communicator, then
+    the step) at world 1 -- eager and captured in a CUDA graph -- give the single-device step's results bit for bit
+    (stochastic fused / two-launch / grid-selector sizes, greedy, logits, the selection alone)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_native_dist_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=400)
+    p.join(60)
+    assert res == [], res

@@ -1,6 +1,6 @@
-"""GPU: the end-to-end host-buffer API (ops.HostTetrisStep) — p / q in pinned host memory, the needed rows moved by
-DMA after the selection (staged) or read by the kernels through the mapping (zero-copy) — gives the device step's
-results bit for bit, and the CPU oracle's."""
+"""GPU: the end-to-end host-buffer API (ops.HostTetrisStep) — p / q in pinned host memory, the needed rows gathered
+over the mapping into device memory after the selection (staged) or read by the streaming kernels through the mapping
+(zero-copy) — gives the device step's results bit for bit, and the CPU oracle's."""
 import numpy as np
 import pytest
 import torch
@@ -86,3 +86,36 @@ def test_pageable_host_inputs_are_registered_and_released():
     dptr = N.map_host(ptr, p_h.numel() * 4)
     assert dptr != 0
     N.unmap_host(ptr)
+
+
+@pytest.mark.parametrize("mode", ["stochastic", "greedy"])
+def test_staged_host_step_in_cuda_graph(mode):
+    """The staged host steps never synchronise the host, so a whole end-to-end step (H2D of the small inputs, the
+    selection, the row gather, the verification, D2H of the results) replays from one CUDA graph."""
+    B, k, V, C = 128, 8, 16384, 600
+    bt = make_batch(B, k, V, seed=11, mode=mode, ragged=True)
+    dev_step = ops.TetrisStep(B, k, V, C, mode=mode)
+    dev_step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    p_h = bt.p.cpu().pin_memory()
+    q_h = bt.q.cpu().pin_memory() if mode == "stochastic" else None
+    small = [t.cpu().pin_memory() for t in (bt.conf, bt.lengths, bt.d, bt.u_acc, bt.u_res)]
+    args = small if mode == "stochastic" else small[:3]
+    hs = ops.HostTetrisStep(B, k, V, C, p_h, q_h, mode=mode, transfer="staged")
+    assert hs.transfer == "staged"
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        hs.run(*args)
+    torch.cuda.current_stream().wait_stream(cs)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        hs.run(*args)
+    hs.offsets_host.zero_()
+    hs.tokens_host.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    n = int(hs.offsets_host[-1])
+    assert n > 0 and np.array_equal(hs.offsets_host.numpy(), _np(dev_step.offsets))
+    assert np.array_equal(hs.tokens_host.numpy()[:n], _np(dev_step.tokens)[:n])
