@@ -564,8 +564,20 @@ __device__ void sift_up(HeapItem* h, int n, int pos, long long& cmp) {
   sift_down(h, start, pos, cmp);
 }
 
-__global__ void heap_stats_kernel(const double* __restrict__ cum, const int32_t* __restrict__ len, int B, int k,
-                                  long long C, long long* stats, HeapItem* heap) {
+// The replay is one dependent chain of heap accesses, so their latency is the cost: the heap (16 B per row) and, when
+// they fit too, the cum values live in shared memory (staged by the whole CTA first); otherwise in the workspace.
+__global__ void heap_stats_kernel(const double* __restrict__ cum_g, const int32_t* __restrict__ len, int B, int k,
+                                  long long C, long long* stats, HeapItem* heap_g, int heap_in_smem,
+                                  int cum_in_smem) {
+  extern __shared__ __align__(16) uint8_t hs_smem[];
+  HeapItem* heap = heap_in_smem ? (HeapItem*)hs_smem : heap_g;
+  const double* cum = cum_g;
+  if (cum_in_smem) {
+    double* cs = (double*)(hs_smem + (size_t)B * sizeof(HeapItem));
+    for (long long i = threadIdx.x; i < (long long)B * k; i += blockDim.x) cs[i] = cum_g[i];
+    cum = cs;
+  }
+  __syncthreads();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   long long cmp = 0, extracts = 0, inserts = 0, peak = 0;
   if (C > 0) {
@@ -776,9 +788,15 @@ extern "C" int tetris_heap_stats_f64(const double* cum, const int32_t* len, int3
   const size_t need = tetris_workspace_bytes(TETRIS_OP_SELECT, B, k, 0);
   if (B > 0 && (!ws || ws_bytes < need))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "workspace too small: %zu < %zu", ws_bytes, need);
-  heap_stats_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
+  constexpr size_t kMaxSmem = 200 * 1024;
+  const size_t heap_b = (size_t)B * sizeof(HeapItem), cum_b = (size_t)B * k * sizeof(double);
+  const int heap_in = heap_b <= kMaxSmem, cum_in = heap_in && heap_b + cum_b <= kMaxSmem;
+  const size_t smem = (heap_in ? heap_b : 0) + (cum_in ? cum_b : 0);
+  cudaError_t e = abi::ensure_smem(heap_stats_kernel, smem);
+  if (e != cudaSuccess) return abi::cuda_fail(e);
+  heap_stats_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(
       cum, len, B, k, (long long)C, (long long*)stats4,
-      (HeapItem*)abi::ws_region(ws, TETRIS_OP_SELECT, B, k, 0, abi::WS_KEYS));
+      (HeapItem*)abi::ws_region(ws, TETRIS_OP_SELECT, B, k, 0, abi::WS_KEYS), heap_in, cum_in);
   return abi::launch_check();
 }
 

@@ -94,7 +94,7 @@ class GpuSimulator:
     def __init__(self, batch_size: int, k: int, capacity: int, *, extra: int = 0, policy: str = "tetris",
                  dsd_decay: float = 0.9, dsd_initial_estimate: float = 0.5, uniforms=None, lengths=None, device=None,
                  pipeline: str = "sequential", draft_time_per_token: float = 0.0025,
-                 selection_overhead: float = 0.0003, verify_time: float = 0.025):
+                 selection_overhead: float = 0.0003, verify_time: float = 0.025, exact_stats: bool = True):
         if pipeline not in ("sequential", "parallel"):
             raise ValueError(f"pipeline must be 'sequential' or 'parallel', got {pipeline!r}")
         self.pipeline, self.draft_time_per_token = pipeline, draft_time_per_token
@@ -129,10 +129,22 @@ class GpuSimulator:
         self.depths_dev = torch.clamp(self.target, max=self.K).to(torch.int32)
         self.status = ops.new_status(dev)
         self.device = dev
+        # exact_stats: PolicyStats.comparisons from the exact heapq replay (tetris_heap_stats_f64, one thread: the
+        # count is a property of the sequential schedule); False takes the selection's closed forms and reports
+        # comparisons = -1, which keeps the whole step parallel
+        self.exact_stats = bool(exact_stats)
+        # every per-step result comes back in ONE round of async copies into pinned buffers, then one stream sync
+        self._host = {name: torch.empty(t.shape, dtype=t.dtype).pin_memory() for name, t in (
+            ("counters", self.counters), ("windows", self.windows), ("accepted", self.accepted),
+            ("credited", self.credited), ("expected", self.expected), ("alpha_hat", self.alpha_hat),
+            ("done_ids", self.done_ids), ("done_arrival", self.done_arrival), ("depths", self.depths_dev),
+            ("stats", torch.zeros(4, dtype=torch.int64)), ("status", self.status))}
+        self._host["depths"].copy_(self.depths_dev)
 
     def depths(self) -> tuple:
-        """Draft depths of the next step, min(k + extra, remaining) per active request (sim_engine.py:343)."""
-        return tuple(int(x) for x in self.depths_dev.cpu().numpy())
+        """Draft depths of the next step, min(k + extra, remaining) per active request (sim_engine.py:343); fetched
+        with the previous step's results (no extra device round trip)."""
+        return tuple(int(x) for x in self._host["depths"].numpy())
 
     def step(self, truth, surrogate=None) -> GpuStepOutcome:
         """One simulator step given the draft phase's truth (and surrogate) rows, ragged lists or [B, K] arrays whose
@@ -141,12 +153,13 @@ class GpuSimulator:
         depths = self.depths()
         tr = self._pack(truth, depths)
         lens = torch.tensor(depths, dtype=torch.int32, device=dev)
-        stats = None
+        stats_t = None
         if self.policy == "tetris":
             sg = self._pack(truth if surrogate is None else surrogate, depths)
-            res = ops.select(sg, self.C, lens, want_cum=True)
+            res = ops.select(sg, self.C, lens, want_cum=self.exact_stats)
             self.windows.copy_(res.windows)
-            stats_t = ops.heap_stats(res.cum, self.C, lens)  # exact PolicyStats incl. heapq comparisons
+            # exact PolicyStats incl. heapq comparisons, or the selection's closed forms (comparisons -1)
+            stats_t = ops.heap_stats(res.cum, self.C, lens) if self.exact_stats else res.stats
         N.call("tetris_sim_step", tr.data_ptr(), lens.data_ptr(), B, K, POLICY_CODES[self.policy], self.k, self.C,
                self.dsd_decay, self.uniforms.data_ptr(), self.uniforms.numel(), self.lengths.data_ptr(),
                self.n_lengths, self.windows.data_ptr(), self.ids.data_ptr(), self.target.data_ptr(),
@@ -154,27 +167,37 @@ class GpuSimulator:
                self.accepted.data_ptr(), self.credited.data_ptr(), self.expected.data_ptr(), self.done_ids.data_ptr(),
                self.done_arrival.data_ptr(), self.depths_dev.data_ptr(), self.status.data_ptr(),
                torch.cuda.current_stream(dev).cuda_stream)
-        ops.raise_for_status(self.status, "sim step")
-        cnt = self.counters.cpu().numpy()
+        h = self._host
+        for name, t in (("counters", self.counters), ("windows", self.windows), ("accepted", self.accepted),
+                        ("credited", self.credited), ("expected", self.expected), ("alpha_hat", self.alpha_hat),
+                        ("done_ids", self.done_ids), ("done_arrival", self.done_arrival), ("depths", self.depths_dev),
+                        ("status", self.status)):
+            h[name].copy_(t, non_blocking=True)
+        if stats_t is not None:
+            h["stats"].copy_(stats_t, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        ops.raise_for_status(h["status"], "sim step")
+        cnt = h["counters"].numpy()
         n_done = int(cnt[4])
+        stats = None
         if self.policy == "tetris":
             from .selector import PolicyStats
 
-            st = stats_t.cpu().numpy()
+            st = h["stats"].numpy()
             stats = PolicyStats(int(st[0]), int(st[1]), int(st[2]), int(st[3]))
-        comps = tuple(zip((int(x) for x in self.done_ids[:n_done].cpu().numpy()),
-                          (int(x) for x in self.done_arrival[:n_done].cpu().numpy())))
+        comps = tuple(zip((int(x) for x in h["done_ids"].numpy()[:n_done]),
+                          (int(x) for x in h["done_arrival"].numpy()[:n_done])))
         return GpuStepOutcome(
             tau=self.step_time(depths),
             step=int(cnt[3]) - 1,
-            windows=tuple(int(x) for x in self.windows.cpu().numpy()),
-            accepted=tuple(int(x) for x in self.accepted.cpu().numpy()),
-            credited=tuple(int(x) for x in self.credited.cpu().numpy()),
+            windows=tuple(int(x) for x in h["windows"].numpy()),
+            accepted=tuple(int(x) for x in h["accepted"].numpy()),
+            credited=tuple(int(x) for x in h["credited"].numpy()),
             bonus=B,
-            expected_accepted=float(self.expected.item()),
+            expected_accepted=float(h["expected"].numpy()[0]),
             stats=stats,
             completions=comps,
-            alpha_hat=float(self.alpha_hat.item()),
+            alpha_hat=float(h["alpha_hat"].numpy()[0]),
         )
 
     def step_time(self, drafted_depths) -> float:

@@ -589,3 +589,28 @@ def test_spec_max_requests_follows_the_device():
 
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     assert N2.spec_max_requests() == min(4096, 32 * sms)
+
+
+@pytest.mark.parametrize("kind", ["random", "ties", "ragged"])
+@pytest.mark.parametrize("B,k", [(2048, 16), (4096, 16), (1500, 40), (3000, 7)])
+def test_select_cluster_kernel_without_workspace(kind, B, k):
+    """tetris_select_f64 with NO workspace takes the thread-block-cluster selector (select_kernel, DSMEM histograms)
+    for batches above the single-CTA selector's 16384 cells: same windows / stats / cum bits as the oracle."""
+    a, ln = selection_instance(B, k, kind, seed=B * k)
+    a, ln = a.to(DEV).contiguous(), ln.to(DEV).contiguous()
+    for C in (1, B, B * k // 3, B * k - 1):
+        windows = torch.zeros(B, dtype=torch.int32, device=DEV)
+        offs = torch.zeros(B + 1, dtype=torch.int32, device=DEV)
+        cum = torch.zeros(B, k, dtype=torch.float64, device=DEV)
+        stats = torch.zeros(4, dtype=torch.int64, device=DEV)
+        status = ops.new_status(DEV)
+        N.call("tetris_select_f64", a.data_ptr(), ln.data_ptr(), B, k, C, 0, windows.data_ptr(), offs.data_ptr(),
+               cum.data_ptr(), stats.data_ptr(), status.data_ptr(), None, 0, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        ops.raise_for_status(status)
+        w_ref, cum_ref, st_ref = O.select(_np(a), C, _np(ln))
+        assert np.array_equal(_np(windows), w_ref), (kind, B, k, C)
+        assert np.array_equal(_np(stats)[:3], st_ref[:3])
+        assert np.array_equal(np.diff(_np(offs)), w_ref)
+        mask = np.arange(k)[None, :] < _np(ln)[:, None]
+        assert np.array_equal(_np(cum)[mask].view(np.uint64), cum_ref[mask].view(np.uint64))

@@ -47,3 +47,17 @@ def test_gpu_sim_rejects_wrong_depths():
     bad = [r[:-1] if len(r) > 1 else r for r in s["truth_rows"]]
     with pytest.raises(ValueError):
         sim.step(bad, bad)
+
+
+@pytest.mark.parametrize("run", [r for r in RUNS if r["policy"] == "tetris"][:2], ids=lambda r: r["tag"])
+def test_gpu_sim_closed_form_stats(run):
+    """exact_stats=False: the same trace with PolicyStats from the selection's closed forms (comparisons = -1), i.e.
+    without the one-thread heapq replay."""
+    sim = GpuSimulator(run["batch_size"], run["k"], run["capacity"], extra=run["extra"], policy=run["policy"],
+                       dsd_decay=run["dsd_decay"], dsd_initial_estimate=run["dsd_initial_estimate"],
+                       uniforms=run["uniforms"], lengths=run["lengths"], device="cuda", exact_stats=False)
+    for i, s in enumerate(run["steps"]):
+        out = sim.step(s["truth_rows"], s["surrogate_rows"])
+        assert list(out.windows) == s["windows"] and list(out.credited) == s["credited"], i
+        st = out.stats
+        assert [st.extracts, st.inserts, st.peak_queue] == s["stats"][:3] and st.comparisons == -1, i

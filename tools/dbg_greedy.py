@@ -33,9 +33,12 @@ for _ in range(3):
     g.replay()
 torch.cuda.synchronize()
 d = dbg.cpu()
-t0 = int(d[48])
-st = d[64:].view(nsm, 8)
-print("select %.2f -> %.2f us" % (0.0, (int(d[49]) - t0) / 1e3))
+st = d[64:64 + 8 * nsm].view(nsm, 8)
+if int(d[48]):  # a separate selector launch stamped its CTA 0
+    t0 = int(d[48])
+    print("select %.2f -> %.2f us" % (0.0, (int(d[49]) - t0) / 1e3))
+else:  # the one-launch step: the selection is the stream kernel's prologue
+    t0 = int(st[:, 0][st[:, 0] > 0].min())
 for j, name in enumerate(["entry", "first copy", "after wait", "last copy", "tail done"]):
     col = st[:, j][st[:, j] > 0]
     if len(col):
