@@ -614,3 +614,32 @@ def test_select_cluster_kernel_without_workspace(kind, B, k):
         assert np.array_equal(np.diff(_np(offs)), w_ref)
         mask = np.arange(k)[None, :] < _np(ln)[:, None]
         assert np.array_equal(_np(cum)[mask].view(np.uint64), cum_ref[mask].view(np.uint64))
+
+
+@pytest.mark.parametrize("B,k,V,C", [(64, 4, 16384, 160), (1024, 16, 8192, 8192)])
+def test_step_adversarial_rows_through_the_stream_kernel(B, k, V, C):
+    """The product sampler (persist_stream_kernel: the fused one-launch step at the small size, the speculative
+    two-launch step at the large one) on rows with exact zeros, subnormals, NaN, p == q ties and huge dynamic range
+    mixed with ordinary rows: the consumers' integer-widening fast path and their F2F path give the oracle's tokens."""
+    bt = make_batch(B, k, V, seed=B + V)
+    rng = np.random.default_rng(5)
+    p = bt.p.cpu().numpy()
+    q = bt.q.cpu().numpy()
+    adv = _adversarial_rows(V, rng)
+    nan_row = rng.random(V).astype(np.float32)
+    nan_row[rng.integers(0, V, 5)] = np.nan
+    adv.append(nan_row)
+    for b in range(0, B, 3):  # every third request: all its rows adversarial
+        for j in range(k + 1):
+            p[b, j] = adv[(b + j) % len(adv)]
+            if j < k:
+                q[b, j] = np.roll(adv[(b + 2 * j + 1) % len(adv)], j + 1)
+    pt, qt = torch.from_numpy(p).to(DEV), torch.from_numpy(q).to(DEV)
+    step = ops.TetrisStep(B, k, V, C)
+    step.run(bt.conf, bt.lengths, pt, qt, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    w_ref, _, _ = O.select(_np(bt.conf), C, _np(bt.lengths))
+    acc_ref, tok_ref, _ = O.verify_stochastic(p, q, _np(bt.d), w_ref, _np(bt.u_acc), _np(bt.u_res), nthreads=8)
+    assert np.array_equal(_np(step.windows), w_ref)
+    assert np.array_equal(_np(step.accepted), acc_ref)
+    assert np.array_equal(_np(step.out_tok), tok_ref)
