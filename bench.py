@@ -108,12 +108,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------------------------------
-def _setup_dist(n_gpus: int, force_nccl: bool = False):
+def _setup_dist(n_gpus: int, force_nccl: bool = False, backend: str = "nccl"):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) if backend == "nccl" else 0
     if n_gpus > 1 and world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch with torchrun --nproc-per-node {n_gpus}")
     group = None
@@ -124,7 +124,10 @@ def _setup_dist(n_gpus: int, force_nccl: bool = False):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         for key, val in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_PORT", "29531")):  # --nccl without torchrun
             os.environ.setdefault(key, val)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # gloo: the N > 1 flow of this script with several ranks on ONE GPU (tests/test_bench_contract.py)
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     else:
         torch.cuda.set_device(local)
@@ -191,7 +194,7 @@ def run_tetris(args):
     from paper_2502_15197_b200 import ops
     from paper_2502_15197_b200.synthetic import make_batch, make_logit_batch
 
-    world, rank, local, group = _setup_dist(args.gpus, args.nccl)
+    world, rank, local, group = _setup_dist(args.gpus, args.nccl, args.dist_backend)
     logits = args.input == "logits"
     if logits and (cfg_mode := CONFIGS[args.config]["mode"]) != "stochastic":
         raise SystemExit(f"--input logits is the stochastic step ({args.config} is {cfg_mode})")
@@ -265,6 +268,29 @@ def run_tetris(args):
     M = 1
     # (NCCL groups: the native sharded step issues its all-gather on the current stream, so it captures too)
     use_graph = args.graph and (world == 1 or step._comm is not None)
+    if use_graph and world > 1:
+        # the sharded step's NCCL group under stream capture: verified at world 1 on this pool's one-GPU boxes; should a
+        # multi-GPU driver refuse to capture it, every rank falls back to eager launches together
+        try:
+            _probe = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                run(0)
+            torch.cuda.current_stream().wait_stream(cs)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(_probe):
+                run(0)
+            ok = 1.0
+        except Exception as e:  # noqa: BLE001 - any capture failure means eager launches
+            print(f"[bench] rank {rank}: CUDA graph capture of the sharded step failed ({e!r:.200}); eager launches",
+                  file=sys.stderr)
+            ok = 0.0
+        use_graph = _max_over_ranks(-ok, group) == -1.0  # every rank captured (nothing captured runs before this)
+        if use_graph:
+            _probe.replay()  # all ranks together
+            torch.cuda.synchronize()
+        del _probe
     if use_graph:
         cs = torch.cuda.Stream()
         cs.wait_stream(torch.cuda.current_stream())
@@ -778,6 +804,8 @@ def main():
                     help="--impl reference: about this many seconds for the K timed steps (sets the per-step sample)")
     ap.add_argument("--graph-steps", type=int, default=8, help="steps captured per CUDA graph (rounded up to a "
                     "multiple of the input-set count)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: several ranks on one GPU (tests of the N > 1 flow; not a measurement)")
     ap.add_argument("--nccl", action="store_true", help="run the NCCL-sharded step even at world size 1 (measures "
                     "the exchange's fixed cost on one GPU)")
     ap.add_argument("--simulate-world", type=int, default=0,

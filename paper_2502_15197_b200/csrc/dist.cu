@@ -17,7 +17,8 @@
 // against one all-gather plus a ~20 us replicated selection that the speculative sampler already overlaps.
 //
 // NCCL binding: the library does not link NCCL.  The communicator comes from the caller (ncclComm_t as void*), and
-// the four NCCL functions used are resolved at first use from the libnccl.so.2 ALREADY LOADED in the process (the
+// the NCCL functions used (ncclAllGather, ncclGroupStart / End, ncclCommCount, ncclCommUserRank, and
+// ncclCommGetAsyncError for non-blocking communicators) are resolved at first use from the libnccl.so.2 ALREADY LOADED in the process (the
 // one that created the communicator: torch's bundled NCCL under Python, the host's own otherwise), falling back to
 // dlopen("libnccl.so.2") -- or $TETRIS_NCCL_LIB when set.  Using a communicator with a different NCCL build than
 // the one that created it is undefined, hence RTLD_NOLOAD first.
@@ -36,13 +37,16 @@ typedef int (*AllGatherFn)(const void*, void*, size_t, int, void*, cudaStream_t)
 typedef int (*GroupFn)(void);
 typedef int (*CommIntFn)(const void*, int*);
 typedef const char* (*ErrStrFn)(int);
-constexpr int kInt8 = 0;  // ncclInt8
+typedef int (*AsyncErrFn)(void*, int*);
+constexpr int kInt8 = 0;        // ncclInt8
+constexpr int kInProgress = 7;  // ncclInProgress: a non-blocking communicator is still working on the call
 
 struct Api {
   AllGatherFn all_gather = nullptr;
   GroupFn group_start = nullptr, group_end = nullptr;
   CommIntFn comm_count = nullptr, comm_rank = nullptr;
   ErrStrFn err_str = nullptr;
+  AsyncErrFn async_err = nullptr;
   char why[256] = {0};
   bool ok = false;
 };
@@ -69,6 +73,7 @@ static const Api& api() {
     a.comm_count = (CommIntFn)dlsym(h, "ncclCommCount");
     a.comm_rank = (CommIntFn)dlsym(h, "ncclCommUserRank");
     a.err_str = (ErrStrFn)dlsym(h, "ncclGetErrorString");
+    a.async_err = (AsyncErrFn)dlsym(h, "ncclCommGetAsyncError");
     a.ok = a.all_gather && a.group_start && a.group_end && a.comm_count && a.comm_rank;
     if (!a.ok) snprintf(a.why, sizeof a.why, "libnccl.so.2 lacks the NCCL collective API");
   });
@@ -79,14 +84,25 @@ static int nccl_fail(const Api& a, int r, const char* what) {
   return abi::fail(TETRIS_NCCL_ERROR, "NCCL %s failed: %s (%d)", what, a.err_str ? a.err_str(r) : "?", r);
 }
 
+// A communicator created non-blocking (ncclConfig_t.blocking = 0) may answer ncclInProgress: wait for the call's
+// completion the way NCCL prescribes (poll ncclCommGetAsyncError), then report its final state.
+static int settle(const Api& a, void* comm, int r) {
+  if (r != kInProgress || !a.async_err) return r;
+  int st = kInProgress;
+  do {
+    if (a.async_err(comm, &st) != 0) return st == 0 ? kInProgress : st;
+  } while (st == kInProgress);
+  return st;
+}
+
 // rank / world of the communicator
 static int comm_info(void* comm, int* rank, int* world) {
   const Api& a = api();
   if (!a.ok) return abi::fail(TETRIS_NCCL_ERROR, "%s", a.why);
   if (!comm) return abi::fail(TETRIS_INVALID_ARGUMENT, "null NCCL communicator");
   int r;
-  if ((r = a.comm_count(comm, world)) != 0) return nccl_fail(a, r, "ncclCommCount");
-  if ((r = a.comm_rank(comm, rank)) != 0) return nccl_fail(a, r, "ncclCommUserRank");
+  if ((r = settle(a, comm, a.comm_count(comm, world))) != 0) return nccl_fail(a, r, "ncclCommCount");
+  if ((r = settle(a, comm, a.comm_rank(comm, rank))) != 0) return nccl_fail(a, r, "ncclCommUserRank");
   return TETRIS_OK;
 }
 
@@ -100,9 +116,9 @@ static int gather_scores(const double* conf, const int32_t* len, int B_local, in
   if ((r = a.group_start()) != 0) return nccl_fail(a, r, "ncclGroupStart");
   int r1 = cb ? a.all_gather(conf, conf_all, cb, kInt8, comm, st) : 0;
   int r2 = len ? a.all_gather(len, len_all, lb, kInt8, comm, st) : 0;
-  if ((r = a.group_end()) != 0) return nccl_fail(a, r, "ncclGroupEnd");
-  if (r1) return nccl_fail(a, r1, "ncclAllGather(conf)");
-  if (r2) return nccl_fail(a, r2, "ncclAllGather(len)");
+  if ((r = settle(a, comm, a.group_end())) != 0) return nccl_fail(a, r, "ncclGroupEnd");
+  if (r1 && r1 != kInProgress) return nccl_fail(a, r1, "ncclAllGather(conf)");
+  if (r2 && r2 != kInProgress) return nccl_fail(a, r2, "ncclAllGather(len)");
   return TETRIS_OK;
 }
 

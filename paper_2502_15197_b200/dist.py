@@ -63,7 +63,8 @@ def nccl_comm(group, device) -> Optional[int]:
 
     def ptr():
         try:
-            return int(backend._comm_ptr())
+            with torch.cuda.device(dev):  # the communicator of this device
+                return int(backend._comm_ptr())
         except RuntimeError:
             return 0
 

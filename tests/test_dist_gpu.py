@@ -202,3 +202,25 @@ def test_native_nccl_sharded_step_world1():
     res = q.get(timeout=400)
     p.join(60)
     assert res == [], res
+
+
+def test_bench_multi_rank_flow_on_one_gpu():
+    """bench.py's N > 1 flow (torchrun, one rank per process, barriers, max-over-ranks timing, whole-job sums, the e2e
+    leg, rank 0 printing one JSON line) with two ranks on ONE GPU exchanging over gloo -- the NCCL exchange itself is
+    covered at world 1 above."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--config", "cfg2", "--steps",
+           "20", "--warmup", "3", "--dist-backend", "gloo", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 20
+    assert "B=512" in d["config"]["workload"] and d["e2e"]["value"] > 0
