@@ -30,10 +30,13 @@ namespace tetris {
 // Element form of the streamed rows: fp32 probabilities (3 stages of 64 KB), or bf16 logits + per-row lse (the logits
 // contract, tetris_b200.h; 6 stages of 32 KB: the same bytes in flight per SM)
 template <bool BF>
+#ifndef TETRIS_F32_STAGES  // A/B experiments only
+#define TETRIS_F32_STAGES 3
+#endif
 struct Elem {
   using T = float;
   static constexpr int kBytes = 4;
-  static constexpr int kStages = 3;
+  static constexpr int kStages = TETRIS_F32_STAGES;
 };
 template <>
 struct Elem<true> {
@@ -54,7 +57,7 @@ template <bool BF>
 __host__ __device__ constexpr size_t stage_row_bytes() { return (size_t)kChunkElems * Elem<BF>::kBytes; }
 template <bool BF>
 __host__ __device__ constexpr size_t stage_bytes() { return 2 * stage_row_bytes<BF>(); }
-static_assert(Elem<false>::kStages * stage_bytes<false>() == kPersistSmem, "fp32 ring");
+static_assert(Elem<false>::kStages * stage_bytes<false>() <= kPersistSmem, "fp32 ring");
 static_assert(Elem<true>::kStages * stage_bytes<true>() == kPersistSmem, "bf16 ring");
 
 
