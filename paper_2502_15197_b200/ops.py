@@ -430,6 +430,7 @@ class TetrisStep:
         # NCCL groups: the exchange and the step are ONE native call (tetris_dist_step_*, csrc/dist.cu) on the
         # torch communicator; other backends (gloo tests) gather in Python (dist.gather_scores)
         self._comm = None
+        self._gathered_len = False
         if group is not None:
             from .dist import nccl_comm
 
@@ -454,10 +455,32 @@ class TetrisStep:
         with torch.cuda.device(dev):
             self.spec_max = min(SPEC_MAX_REQUESTS, N.spec_max_requests())
 
-    def run(self, conf, lengths, p, q, d, u_acc=None, u_res=None, cap=None, events=None, window=None) -> None:
+    def exchange(self, conf, lengths=None) -> None:
+        """Issue the sharded step's only exchange -- every rank's scores and drafted depths all-gathered into this
+        step's conf_all / len_all -- NOW, on the current stream; then call run(..., gathered=True), which skips it.
+        The exchange needs only the draft phase's confidences, so a serving loop issues it as soon as drafting ends
+        (e.g. on a side stream, before the target model's forward pass that produces p) and takes it off the
+        verification step's critical path.  NCCL: tetris_dist_gather_scores on the torch communicator."""
+        if self.group is None:
+            raise ValueError("exchange() needs the step's process group")
+        self._gathered_len = lengths is not None
+        if self._comm is not None:
+            self._check(self._lib.tetris_dist_gather_scores(
+                conf.data_ptr(), _ptr(lengths), self.B, self.k, self._comm, self.conf_all.data_ptr(),
+                _ptr(self.len_all if lengths is not None else None), torch.cuda.current_stream().cuda_stream))
+        else:
+            from .dist import gather_scores
+
+            ln = lengths if lengths is not None else torch.full((self.B,), self.k, dtype=_I32, device=conf.device)
+            gather_scores(self.conf_all, self.len_all, conf, ln, self.group)
+            self._gathered_len = True
+
+    def run(self, conf, lengths, p, q, d, u_acc=None, u_res=None, cap=None, events=None, window=None,
+            gathered: bool = False) -> None:
         """events: optional 4 torch.cuda.Events recorded around select / verify / compact (kernel timing).  The
         stochastic step is two launches (select+accept+compaction offsets, then the streaming sampler), so its
-        events bracket [select kernel | sampler | nothing]."""
+        events bracket [select kernel | sampler | nothing].  gathered=True: exchange() already gathered the scores
+        (conf / lengths are then not read)."""
         lib, ws, s = self._lib, self.ws, torch.cuda.current_stream().cuda_stream
         B, k, V = self.B, self.k, self.V
         if events is not None:
@@ -465,10 +488,14 @@ class TetrisStep:
         if self.policy == "fixed":
             self._run_fixed(lengths, p, q, d, u_acc, u_res, cap, events, window)
             return
-        if self._comm is not None and events is None and self._dist_native(p, q):
+        if gathered:  # exchange() already issued the all-gather on this stream
+            if self.group is None:
+                raise ValueError("gathered=True needs the step's process group and a prior exchange()")
+            sel_conf, sel_len = self.conf_all, (self.len_all if self._gathered_len else None)
+        elif self._comm is not None and events is None and self._dist_native(p, q):
             self._run_dist(conf, lengths, p, q, d, u_acc, u_res, cap)
             return
-        if self.world > 1 and self.group is not None:
+        elif self.world > 1 and self.group is not None:
             from .dist import gather_scores
 
             gather_scores(self.conf_all, self.len_all, conf, lengths, self.group)  # one coalesced NCCL exchange

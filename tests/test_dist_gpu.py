@@ -168,6 +168,19 @@ def _native_dist_worker(port, q):
             for n in names:
                 if not torch.equal(getattr(ref, n), getattr(nat, n)):
                     fails.append(f"graph {mode} B={B} k={k}: {n}")
+        # the exchange issued early on a side stream, then the step with gathered=True (serving-loop overlap)
+        bt = make_batch(1024, 16, 16384, seed=21, ragged=True, device="cuda:0")
+        ref = ops.TetrisStep(1024, 16, 16384, 8192, device="cuda:0")
+        nat = ops.TetrisStep(1024, 16, 16384, 8192, device="cuda:0", group=grp)
+        ref.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            nat.exchange(bt.conf, bt.lengths)
+        torch.cuda.current_stream().wait_stream(side)
+        nat.run(None, None, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res, gathered=True)
+        torch.cuda.synchronize()
+        fails += [f"early exchange: {n}" for n in names if not torch.equal(getattr(ref, n), getattr(nat, n))]
         # logits form
         lb = make_logit_batch(256, 8, 32000, seed=3, device="cuda:0")
         ref = ops.TetrisStep(256, 8, 32000, 1024, device="cuda:0")
