@@ -45,9 +45,13 @@ for i, d in enumerate(dbgs):
     d = d.cpu()
     sel0, sel1 = int(d[48]), int(d[49])
     st = d[64:64 + 16 * nsm].view(nsm, 16)
+    if sel0 == 0:  # the one-launch step (the selection is the sampler's prologue): time from the first CTA entry
+        sel0 = sel1 = int(st[:, 0][st[:, 0] > 0].min())
     t0 = sel0 if t0 is None else t0
     rel = lambda x: (x - t0) / 1e3  # noqa: E731
     col = lambda j: st[:, j][st[:, j] > 0]  # noqa: E731
-    print("step %d: select %.2f -> %.2f us | sampler entry %.2f (median %.2f) | first copy %.2f | last descent %.2f"
+    print("step %d: select %.2f -> %.2f us | sampler entry %.2f (median %.2f, max %.2f) | first copy %.2f | last "
+          "descent %.2f (median CTA %.2f)"
           % (i, rel(sel0), rel(sel1), rel(int(col(0).min())), rel(float(col(0).double().median())),
-             rel(float(col(2).double().median())), rel(int(col(6).max()))))
+             rel(int(col(0).max())), rel(float(col(2).double().median())), rel(int(col(6).max())),
+             rel(float(col(6).double().median()))))
