@@ -102,6 +102,36 @@ __device__ __forceinline__ void cta_prefix(const long long* part, GShared& sh) {
   }
 }
 
+// Radix schedule.  Pass 0 is a CLAMPED digit of key bits 63..48: for a score in [2^-127, 1] those bits are its
+// exponent and the top 4 mantissa bits (desc_key maps 1.0 to 0x400F..), so probabilities get 16 bins per binade
+// instead of the 2 binades per bin a plain top-11-bit digit gives them (cfg4 data: one pass fewer); bin 0 collects
+// every key below 0x4010 << 48 (scores >= 1.0, any cum above 1 in vals_are_cum mode) and bin 2047 every key from
+// 0x480E << 48 up (scores below ~2^-127, zero, negative cums).  Every bin is an interval of keys, digits are monotone
+// in the key, so the row-wise run-length histograms and range updates still apply.  After a middle bin (an exact
+// 16-bit prefix) the passes refine bits 47..0 as 11/11/11/11/4; after an edge bin, bits 63..0 as 11/11/11/11/10/10.
+struct GDigit {
+  int shift;
+  uint32_t mask;
+  int clamp;
+};
+__device__ __forceinline__ uint32_t gdigit(uint64_t key, const GDigit& d) {
+  if (d.clamp) {
+    const long long x = (long long)(key >> 48) - 0x400F;
+    return x < 0 ? 0u : (x > 2047 ? 2047u : (uint32_t)x);
+  }
+  return (uint32_t)(key >> d.shift) & d.mask;
+}
+__device__ __forceinline__ GDigit gpass(int pass, bool edge) {
+  if (pass == 0) return GDigit{48, 2047u, 1};
+  if (!edge) {  // bits 47..0
+    const int sh = 48 - 11 * pass;
+    return sh >= 0 ? GDigit{sh, 2047u, 0} : GDigit{0, 15u, 0};
+  }
+  const int w = pass <= 4 ? 11 : 10, sh = 64 - (pass <= 4 ? 11 * pass : 44 + 10 * (pass - 4));
+  return GDigit{sh, (1u << w) - 1u, 0};
+}
+__device__ __forceinline__ int glast_pass(bool edge) { return edge ? 6 : 5; }
+
 struct GArgs {
   SelectArgs a;
   GScratch* gs;
@@ -174,7 +204,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
     }
   }
   __syncthreads();
-  constexpr int kShift0 = 53;
+  const GDigit d0 = gpass(0, false);
   uint32_t bad = 0;
   int L = 0, lo = 0, hi = 0;
   if (row) {
@@ -198,7 +228,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
       env = (j == 0 || cum < env) ? cum : env;
       const uint64_t key = desc_key(env);
       keys[(size_t)j * KS + tid] = key;
-      const uint32_t dg = (uint32_t)(key >> kShift0);
+      const uint32_t dg = gdigit(key, d0);
       if (dg == cur) {
         ++cnt;
       } else {
@@ -221,13 +251,11 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
   // ---- phase 1: radix passes; one grid barrier each --------------------------------------------------------------
   long long need = a.C, N = 0;
   int mode = 0;  // 0: nothing selected, 1: everything, 2: radix
-  bool done = false;
-  int shift = 64, npass = 0;
-  for (int pass = 0; pass < 6; ++pass) {
+  bool done = false, edge = false;
+  int npass = 0;
+  for (int pass = 0; pass < 7; ++pass) {
     ++npass;
-    const int width = pass < 4 ? 11 : 10;
-    shift -= width;
-    const uint32_t mask = (1u << width) - 1u;
+    const GDigit dg = gpass(pass, edge);
     // the global histogram, copied through L2 (other CTAs' atomics landed there before the barrier; L1 may hold a
     // stale line from an earlier pass)
     const uint32_t* H = gs->hist[pass % 3];
@@ -253,27 +281,27 @@ __global__ void __launch_bounds__(kGThreads, 1) gselect_kernel(const GArgs ga) {
     const uint32_t D = (uint32_t)sh.digit;
     need = sh.need;
     const bool take_all = sh.done != 0;
+    if (pass == 0) edge = D == 0u || D == 2047u;  // an edge bin is an interval, not a prefix: refine from bit 63
     if (row && lo < hi) {
       int l = lo;
-      while (l < hi && (((uint32_t)(keys[(size_t)l * KS + tid] >> shift) & mask) < D)) ++l;
+      while (l < hi && gdigit(keys[(size_t)l * KS + tid], dg) < D) ++l;
       int e = l;
-      while (e < hi && (((uint32_t)(keys[(size_t)e * KS + tid] >> shift) & mask) == D)) ++e;
+      while (e < hi && gdigit(keys[(size_t)e * KS + tid], dg) == D) ++e;
       lo = take_all ? e : l;
       hi = e;
     }
     done = take_all;
-    if (done || pass == 5) break;
+    if (done || pass == glast_pass(edge)) break;
     if (stamp) a.dbg[12 + 5 * pass] = clock64();
     // next digit's histogram of the still-undecided cells
-    const int nshift = shift - (pass + 1 < 4 ? 11 : 10);
-    const uint32_t nmask = (1u << (pass + 1 < 4 ? 11 : 10)) - 1u;
+    const GDigit nd = gpass(pass + 1, edge);
     __syncthreads();
     for (int i = tid; i < kGBins; i += kGThreads) sh.hist[i] = 0;
     __syncthreads();
     if (row && lo < hi) {
-      uint32_t cur = (uint32_t)(keys[(size_t)lo * KS + tid] >> nshift) & nmask, cnt = 1;
+      uint32_t cur = gdigit(keys[(size_t)lo * KS + tid], nd), cnt = 1;
       for (int j = lo + 1; j < hi; ++j) {
-        const uint32_t dg = (uint32_t)(keys[(size_t)j * KS + tid] >> nshift) & nmask;
+        const uint32_t dg = gdigit(keys[(size_t)j * KS + tid], nd);
         if (dg == cur) {
           ++cnt;
         } else {

@@ -643,3 +643,26 @@ def test_step_adversarial_rows_through_the_stream_kernel(B, k, V, C):
     assert np.array_equal(_np(step.windows), w_ref)
     assert np.array_equal(_np(step.accepted), acc_ref)
     assert np.array_equal(_np(step.out_tok), tok_ref)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_grid_selector_edge_bins(seed):
+    """The grid selector's first pass clamps keys outside [2^-127, 1] into its two edge bins (then refines them from
+    bit 63): candidate cums above 1, tiny, zero, -0.0 and negative values, with ties, at grid-selector sizes."""
+    rng = np.random.default_rng(seed)
+    B, k = 4096, 16
+    cum = np.sort(rng.random((B, k)), axis=1)[:, ::-1].copy()  # non-increasing rows
+    kind = seed % 3
+    if kind == 0:    # many scores above 1 (edge bin 0 holds the C-th)
+        cum[: B // 2] += rng.integers(1, 4, (B // 2, 1))
+    elif kind == 1:  # many tiny / zero / negative scores (edge bin 2047)
+        cum[B // 3:] *= 1e-300
+        cum[B // 2:, k // 2:] = 0.0
+        cum[-B // 8:, -2:] = -np.abs(cum[-B // 8:, -2:]) - 1.0
+        cum[B // 2: B // 2 + 50, -1] = -0.0
+    else:            # quantised ties spanning both edges
+        cum = np.round(cum * 8) / 8 * rng.choice([1e-200, 1.0, 3.0], (B, 1))
+    cum = np.minimum.accumulate(cum, axis=1)  # keep rows non-increasing (the candidate lists' envelope)
+    lens = rng.integers(1, k + 1, B).astype(np.int32)
+    for C in (1, 777, B * k // 4, B * k // 2, B * k - 3):
+        _check_select(torch.from_numpy(cum), torch.from_numpy(lens), C, vals_are_cum=True)
