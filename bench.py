@@ -194,6 +194,8 @@ def run_tetris(args):
     from paper_2502_15197_b200 import ops
     from paper_2502_15197_b200.synthetic import make_batch, make_logit_batch
 
+    if args.nccl and args.simulate_world:
+        raise SystemExit("--nccl and --simulate-world are exclusive (the simulated shard is handed the gathered scores)")
     world, rank, local, group = _setup_dist(args.gpus, args.nccl, args.dist_backend)
     logits = args.input == "logits"
     if logits and (cfg_mode := CONFIGS[args.config]["mode"]) != "stochastic":

@@ -430,7 +430,7 @@ class TetrisStep:
         # NCCL groups: the exchange and the step are ONE native call (tetris_dist_step_*, csrc/dist.cu) on the
         # torch communicator; other backends (gloo tests) gather in Python (dist.gather_scores)
         self._comm = None
-        self._gathered_len = False
+        self._gathered_len = self._exchanged = False
         if group is not None:
             from .dist import nccl_comm
 
@@ -464,6 +464,7 @@ class TetrisStep:
         if self.group is None:
             raise ValueError("exchange() needs the step's process group")
         self._gathered_len = lengths is not None
+        self._exchanged = True
         if self._comm is not None:
             self._check(self._lib.tetris_dist_gather_scores(
                 conf.data_ptr(), _ptr(lengths), self.B, self.k, self._comm, self.conf_all.data_ptr(),
@@ -489,8 +490,9 @@ class TetrisStep:
             self._run_fixed(lengths, p, q, d, u_acc, u_res, cap, events, window)
             return
         if gathered:  # exchange() already issued the all-gather on this stream
-            if self.group is None:
+            if self.group is None or not self._exchanged:
                 raise ValueError("gathered=True needs the step's process group and a prior exchange()")
+            self._exchanged = False  # one exchange per step
             sel_conf, sel_len = self.conf_all, (self.len_all if self._gathered_len else None)
         elif self._comm is not None and events is None and self._dist_native(p, q):
             self._run_dist(conf, lengths, p, q, d, u_acc, u_res, cap)

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+for t in memcheck synccheck racecheck; do
+  timeout -s KILL 1500 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize.py > gpurun_out/r2ad_$t.txt 2>&1
+  echo "== $t"; tail -4 gpurun_out/r2ad_$t.txt
+done

@@ -41,3 +41,41 @@ for _ in range(2):
 torch.cuda.synchronize()
 ops.raise_for_status(step.status)
 print("ok")
+# round 2: the logits form (fused one-launch and two-launch sizes), the host-buffer steps (row-gather kernels), the grid
+# selector's clamped first pass on a stochastic step, the GPU simulator step
+from paper_2502_15197_b200.synthetic import make_logit_batch  # noqa: E402
+
+for (B, k, V, C) in [(200, 8, 8192, 700), (600, 8, 8192, 2000)]:
+    lb = make_logit_batch(B, k, V, seed=3, ragged=True)
+    step = ops.TetrisStep(B, k, V, C)
+    for _ in range(2):
+        step.run_logits(lb.conf, lb.lengths, lb.zp, lb.lse_p, lb.zq, lb.lse_q, lb.d, lb.u_acc, lb.u_res)
+    torch.cuda.synchronize()
+    ops.raise_for_status(step.status)
+for mode in ("stochastic", "greedy"):
+    B, k, V, C = 96, 5, 8192, 300
+    bt = make_batch(B, k, V, seed=4, mode=mode, ragged=True)
+    hs = ops.HostTetrisStep(B, k, V, C, bt.p.cpu().pin_memory(),
+                            bt.q.cpu().pin_memory() if mode == "stochastic" else None, mode=mode)
+    small = [t.cpu().pin_memory() for t in (bt.conf, bt.lengths, bt.d, bt.u_acc, bt.u_res)]
+    for _ in range(2):
+        hs.run(*(small if mode == "stochastic" else small[:3]))
+    torch.cuda.synchronize()
+    ops.raise_for_status(hs.step.status)
+B, k, V, C = 2048, 16, 2048, 12000  # 32768 cells: grid selector + speculative sampler
+bt = make_batch(B, k, V, seed=5, ragged=True)
+step = ops.TetrisStep(B, k, V, C)
+for _ in range(2):
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+torch.cuda.synchronize()
+ops.raise_for_status(step.status)
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
+from _sim_golden import runs  # noqa: E402
+from paper_2502_15197_b200.sim_engine import GpuSimulator  # noqa: E402
+
+run = runs()[0]
+sim = GpuSimulator(run["batch_size"], run["k"], run["capacity"], extra=run["extra"], policy=run["policy"],
+                   uniforms=run["uniforms"], lengths=run["lengths"], device="cuda")
+for s_ in run["steps"][:3]:
+    sim.step(s_["truth_rows"], s_["surrogate_rows"])
+print("sanitize.py: all kernels ran")
