@@ -22,6 +22,8 @@
 // Then, in the same launch, one warp per request (strided over the CTAs) waits for the request's (w_b + 1) · nch
 // chunks, reads the w_b + 1 keys and writes accepted / out_tok; the last CTA out runs the compaction (offsets and
 // tokens, compact_kernel's contract) when asked to.
+#include <climits>
+
 #include "common.cuh"
 #include "fused_select.cuh"
 #include "launch.h"
@@ -474,10 +476,52 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   }
   __syncthreads();
   if (!s_last) return;
-  if (FUSED) {  // the one-launch step: win_offsets and PolicyStats over every selected row's window
+  if (tid == 0) gtime(a, 6);
+  if (FUSED) {
+    // the one-launch step (B <= kFusedMaxCells): win_offsets / PolicyStats over every selected row's window and the
+    // compaction, with every load of both in ONE round trip (windows; accepted, out_tok, cap of the thread's rows
+    // [r0, r0 + rpt); the drafted tokens d staged in the now idle stage ring), then on-chip scans and the writes
     int wr[kFusedMaxRpt];
     fused_load_windows(a.fs, tid, blockDim.x, wr);
-    fused_win_scan(a.fs, k, tid, blockDim.x, s_tmp, wr);
+    const int B = a.B, nt = blockDim.x, rpt = (B + nt - 1) / nt, r0 = tid * rpt;
+    int acc[kFusedMaxRpt], tok[kFusedMaxRpt], nn[kFusedMaxRpt];
+    int32_t* ds = reinterpret_cast<int32_t*>(stage_mem);
+    if (a.offsets != nullptr) {
+#pragma unroll
+      for (int i = 0; i < kFusedMaxRpt; ++i) {
+        const int r = r0 + i;
+        const bool in = i < rpt && r < B;
+        acc[i] = in ? __ldcg(a.accepted + r) : 0;
+        tok[i] = in ? __ldcg(a.out_tok + r) : 0;
+        nn[i] = in && a.cap ? __ldg(a.cap + r) : INT_MAX;
+      }
+      for (int e = tid; e < B * k; e += nt) ds[e] = __ldg(a.d + e);
+    }
+    fused_win_scan(a.fs, k, tid, nt, s_tmp, wr);  // (its barriers also publish ds)
+    if (a.offsets == nullptr) return;
+    __syncthreads();
+    long long local = 0;
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) {
+      nn[i] = (i < rpt && r0 + i < B) ? min(acc[i] + 1, max(nn[i], 0)) : 0;
+      local += nn[i];
+    }
+    long long total;
+    long long off = block_excl_scan<long long>(local, s_tmp, total);
+#pragma unroll
+    for (int i = 0; i < kFusedMaxRpt; ++i) {
+      const int r = r0 + i;
+      if (i < rpt && r < B) {
+        a.offsets[r] = (int32_t)off;
+        for (int j = 0; j < nn[i]; ++j) a.tokens[off + j] = j < acc[i] ? ds[r * k + j] : tok[i];
+        off += nn[i];
+      }
+    }
+    if (tid == 0) {
+      a.offsets[B] = (int32_t)total;
+      gtime(a, 7);
+    }
+    return;
   }
   if (a.offsets == nullptr) return;
   // compact_kernel's contract: n_b = accepted[b] + 1 (capped), offsets = exclusive scan, tokens = d[b][0..a) ++ [x]

@@ -1197,7 +1197,8 @@ int spec_max_requests() { return std::min(kSpecMaxR, 32 * abi::device_sm_count()
 
 bool fused_step_eligible(int B_sel, int k, int u_packed) {
   static const bool off = std::getenv("TETRIS_NO_FUSED") != nullptr;  // A/B timing switch: the two-launch step
-  return !u_packed && B_sel >= 1 && (long long)B_sel * k <= kFusedMaxCells && !off;
+  // (B_sel bounded too: with k = 0 every batch has 0 cells, but the scans hold at most kFusedMaxRpt rows per thread)
+  return !u_packed && B_sel >= 1 && B_sel <= kFusedMaxRpt * 512 && (long long)B_sel * k <= kFusedMaxCells && !off;
 }
 
 bool persist_eligible(const float* p, const float* q, int V) {

@@ -392,6 +392,7 @@ SPEC_MAX_REQUESTS = 4096  # tetris_resample_spec_f32's limit (per call, local ro
 SPEC_MIN_CHUNKS = int(os.environ.get("TETRIS_SPEC_MIN_CHUNKS", "4096"))
 _NO_SPEC = os.environ.get("TETRIS_NO_SPEC") == "1"  # A/B timing switch: the plain sampler
 FUSED_MAX_CELLS = 2048  # csrc/launch.h kFusedMaxCells: the one-launch stochastic step up to this many cells
+FUSED_MAX_ROWS = 4096   # ... and this many selected rows (kFusedMaxRpt * 512: the fused scans' rows per thread)
 _NO_FUSED = "TETRIS_NO_FUSED" in os.environ  # A/B timing switch: the two-launch step (read by the library too)
 
 
@@ -729,7 +730,7 @@ class TetrisStep:
         """True when the stochastic step is ONE launch: the selection runs as the sampler's prologue (small batches,
         Bg * k <= FUSED_MAX_CELLS, dense uniforms; csrc/stream.cu fused_select)."""
         return (self.mode == "stochastic" and self.policy == "tetris" and self.u_layout == "dense"
-                and self.Bg * self.k <= FUSED_MAX_CELLS and not _NO_FUSED)
+                and self.Bg * self.k <= FUSED_MAX_CELLS and self.Bg <= FUSED_MAX_ROWS and not _NO_FUSED)
 
     @property
     def uses_spec(self) -> bool:
@@ -750,7 +751,7 @@ class TetrisStep:
             if self.V % 8 != 0:
                 return 3  # select, verify (one sample_kernel), compact
             return 1 if self.fused else 2
-        if self.Bg * self.k <= FUSED_MAX_CELLS and self.V % 8 == 0 and not _NO_FUSED:
+        if self.Bg * self.k <= FUSED_MAX_CELLS and self.Bg <= FUSED_MAX_ROWS and self.V % 8 == 0 and not _NO_FUSED:
             return 1  # the one-launch greedy step (selection as the argmax stream's prologue)
         return 2 if self.Bg * self.k <= 16384 and self.Bg <= 4096 else 3
 

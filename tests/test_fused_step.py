@@ -279,3 +279,26 @@ def test_greedy_shard_and_repeats():
 def test_greedy_step_launch_count():
     step = ops.TetrisStep(16, 5, 32000, 48, mode="greedy")
     assert step.launches_per_step == 1
+
+
+@pytest.mark.parametrize("mode", ["stochastic", "greedy"])
+@pytest.mark.parametrize("B", [2500, 4096, 5000])
+def test_k0_large_batches(mode, B):
+    """k = 0 (nothing drafted) gives every batch 0 cells: the one-launch path still holds at most 4096 rows (its scans
+    keep 8 rows per thread); larger batches take the two-launch step.  Either way every request emits its bonus
+    token, as the oracle says."""
+    k, V, C = 0, 8192, 10
+    bt = make_batch(B, k, V, seed=B, mode=mode)
+    step = ops.TetrisStep(B, k, V, C, mode=mode)
+    step.run(bt.conf, bt.lengths, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+    torch.cuda.synchronize()
+    ops.raise_for_status(step.status)
+    w_ref = np.zeros(B, np.int32)
+    if mode == "stochastic":
+        acc_ref, tok_ref, _ = O.verify_stochastic(_np(bt.p), _np(bt.q), _np(bt.d), w_ref, _np(bt.u_acc),
+                                                  _np(bt.u_res), nthreads=8)
+    else:
+        acc_ref, tok_ref = O.verify_greedy(_np(bt.p), _np(bt.d), w_ref, nthreads=8)
+    off_ref, toks_ref = O.compact(acc_ref, tok_ref, _np(bt.d), None)
+    assert np.array_equal(_np(step.windows), w_ref) and np.array_equal(_np(step.out_tok), tok_ref)
+    assert np.array_equal(_np(step.offsets), off_ref) and np.array_equal(_np(step.tokens)[: off_ref[-1]], toks_ref)
