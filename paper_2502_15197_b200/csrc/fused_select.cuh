@@ -77,6 +77,13 @@ __device__ inline FusedView fused_view(const FusedSel& f, int k, uint8_t* smem) 
 // The kernel issues its own per-cell loads (accept-test gathers) around this call, so they share the round trip.
 __device__ inline void fused_stage(const FusedSel& f, int k, const FusedView& v, int pt, int nt) {
   const int N = f.B_sel * k, KS = v.KS;
+  // the lengths' loads go out with the first batch of scores (one round trip, not two)
+  int ln[kFusedMaxRpt];
+#pragma unroll
+  for (int i = 0; i < kFusedMaxRpt; ++i) {
+    const int r = pt + i * nt;
+    ln[i] = r < f.B_sel ? (f.len ? __ldg(f.len + r) : k) : 0;
+  }
   for (int e0 = 0; e0 < N; e0 += 4 * nt) {
     double x4[4];
 #pragma unroll
@@ -93,7 +100,9 @@ __device__ inline void fused_stage(const FusedSel& f, int k, const FusedView& v,
       }
     }
   }
-  for (int r = pt; r < f.B_sel; r += nt) v.lens[r] = f.len ? __ldg(f.len + r) : k;
+#pragma unroll
+  for (int i = 0; i < kFusedMaxRpt; ++i)
+    if (pt + i * nt < f.B_sel) v.lens[pt + i * nt] = ln[i];
   for (int c = pt; c < v.ncell; c += nt) v.rk[c] = 0u;
 }
 

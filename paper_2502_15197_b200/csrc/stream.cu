@@ -677,7 +677,16 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) gstamp(a, 1);
   }
-  if (FUSED) fused_select<BF>(a, stage_mem);
+  long long f_i0 = 0, f_i1 = 0;
+  if (FUSED) {
+    // the producer's first two claims go out before the selection, so their round trip overlaps it (the counter was
+    // reset by the previous launch, complete after griddepcontrol.wait)
+    if (warp == kProducerWarp && lane == 0) {
+      f_i0 = (long long)atomicAdd(work, 1ull);
+      f_i1 = (long long)atomicAdd(work, 1ull);
+    }
+    fused_select<BF>(a, stage_mem);
+  }
 
   if (warp == kProducerWarp) {
     // ---------------------------------------------------------------- producer
@@ -688,7 +697,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         // item's word read while the current copy waits for its stage
         const uint64_t pol = l2_evict_normal_policy();
         const uint32_t epoch = (uint32_t)__ldcg(a.fs.ctl + 2) + 1u;
-        long long i = (long long)atomicAdd(work, 1ull), i1 = (long long)atomicAdd(work, 1ull);
+        long long i = f_i0, i1 = f_i1;
         unsigned long long w = i < total ? fused_wait_ready(a.fs.ready + i / nch, epoch) : 0ull;
         gstamp(a, 7);
         int t = 0;

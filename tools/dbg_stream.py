@@ -57,3 +57,12 @@ for a_, b_, nme in ((1, 8, "wait -> scores loaded"), (8, 9, "scores -> keys"), (
         continue
     dc = (cyc[m, b_] - cyc[m, a_]).double()
     print("cycles %-40s min %8.0f  median %8.0f  max %8.0f (CTAs %d)" % (nme, dc.min(), dc.median(), dc.max(), int(m.sum())))
+
+# the latest CTAs (their descents end the step): every stamp, us from the first entry
+late = torch.argsort(d[:, 6], descending=True)[:6]
+print("latest CTAs (cta: entry, after wait, first copy, last copy, first consumed, publisher done, descents done, "
+      "warp-0 request counted / sums in / done):")
+for c in late.tolist():
+    row = d[c]
+    f = lambda s: "%.2f" % ((int(row[s]) - t0) / 1e3) if int(row[s]) > 0 else "-"  # noqa: E731
+    print("  %3d: %s" % (c, " ".join(f(s) for s in (0, 1, 2, 3, 4, 5, 6, 13, 15, 14))))
