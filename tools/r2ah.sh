@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+timeout -s KILL 500 python -m pytest tests/test_fused_step.py tests/test_logits_gpu.py tests/test_gpu_parity.py tests/test_dist_gpu.py -x -q > gpurun_out/r2ah_tests.log 2>&1
+tail -5 gpurun_out/r2ah_tests.log
+for r in 1 2 3; do for v in libhead.so libtetris_b200.so; do for c in cfg2; do
+  TETRIS_LIB_VARIANT=$v timeout -s KILL 120 python bench.py --config $c --steps 2000 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2ah_ab.json 2>/dev/null
+  python -c "import json;d=json.loads(open('gpurun_out/r2ah_ab.json').read().strip().splitlines()[-1]);print('$v $c',round(d['ms_per_step']*1000,2), d['select_verify_latency_us'])"
+  TETRIS_LIB_VARIANT=$v timeout -s KILL 120 python bench.py --config $c --input logits --steps 2000 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2ah_ab.json 2>/dev/null
+  python -c "import json;d=json.loads(open('gpurun_out/r2ah_ab.json').read().strip().splitlines()[-1]);print('$v $c logits',round(d['ms_per_step']*1000,2), d['select_verify_latency_us'])"
+done; done; done
+timeout -s KILL 300 python tools/dbg_graph.py 256 8 32000 1024
