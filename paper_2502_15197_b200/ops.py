@@ -436,7 +436,7 @@ class TetrisStep:
             from .dist import nccl_comm
 
             self._comm = nccl_comm(group, dev)
-        if self.world > 1 or self._comm is not None:
+        if self.world > 1 or group is not None:
             if u_layout != "dense":
                 raise ValueError("sharded steps use the dense uniform layout")
             self.conf_all = torch.zeros(Bg, k, dtype=_F64, device=dev)
