@@ -168,6 +168,14 @@ def _native_dist_worker(port, q):
             for n in names:
                 if not torch.equal(getattr(ref, n), getattr(nat, n)):
                     fails.append(f"graph {mode} B={B} k={k}: {n}")
+        # no lengths (every row drafted k deep): nothing but the scores is gathered
+        bt = make_batch(512, 8, 8192, seed=17, device="cuda:0")
+        ref = ops.TetrisStep(512, 8, 8192, 2000, device="cuda:0")
+        nat = ops.TetrisStep(512, 8, 8192, 2000, device="cuda:0", group=grp)
+        for st_ in (ref, nat):
+            st_.run(bt.conf, None, bt.p, bt.q, bt.d, bt.u_acc, bt.u_res)
+        torch.cuda.synchronize()
+        fails += [f"no lengths: {n}" for n in names if not torch.equal(getattr(ref, n), getattr(nat, n))]
         # the exchange issued early on a side stream, then the step with gathered=True (serving-loop overlap)
         bt = make_batch(1024, 16, 16384, seed=21, ragged=True, device="cuda:0")
         ref = ops.TetrisStep(1024, 16, 16384, 8192, device="cuda:0")
