@@ -38,6 +38,7 @@ constexpr int kSegsPerWarp = kChunkElems / kSegElems / kGConsumers;  // staged s
 constexpr int kGProducer = kGConsumers;
 constexpr int kGPublisher = kGConsumers + 1;
 constexpr int kGThreads = (kGConsumers + 2) * 32;
+constexpr int kFinRows = 36;  // one-launch batches up to this many requests: CTA 0 finishes them alone (2 per warp)
 constexpr int kGRing = 64;
 constexpr int kClaim = 4;  // work items (row chunks) per claim on the global counter
 constexpr int kStaticItems = 8;  // calls with at most this many items per CTA use a static schedule
@@ -356,6 +357,16 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
     }
     __syncwarp();
   } else if (warp < kGConsumers) {
+    if (FUSED) {
+      // the one-launch step: win_offsets / PolicyStats over every selected row's window, by the consumers of the last
+      // CTA to publish its rows' windows — now, while the stream runs, not in the last CTA out's tail
+      __shared__ int s_last_pub;
+      if (fused_publish(a.fs, tid, kGConsumers * 32, &s_last_pub)) {
+        int wr[kFusedMaxRpt];
+        fused_load_windows(a.fs, tid, kGConsumers * 32, wr);
+        fused_win_scan(a.fs, k, tid, kGConsumers * 32, s_tmp, wr);
+      }
+    }
     for (int t = 0;; ++t) {
       const int s = t % kGStages;
       mbar_wait(&sh.full[s], (uint32_t)((t / kGStages) & 1));
@@ -417,7 +428,15 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
   asm volatile("griddepcontrol.wait;" ::: "memory");  // windows (no-op by now)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next step's selector may be scheduled
   constexpr int kWarps = kGThreads / 32;
-  for (int b = warp * G + blockIdx.x; b < a.B; b += G * kWarps) {
+  // small one-launch batches: CTA 0 alone runs every request's descent (one round: B <= its warps x 2) and then the
+  // compaction from shared memory — no last-CTA election, no reload of the results; the other CTAs leave at once
+  const bool fin = FUSED && a.offsets != nullptr && a.B <= kFinRows;
+  __shared__ int s_acc[kFinRows], s_tok[kFinRows];
+  int32_t* ds = reinterpret_cast<int32_t*>(stage_mem);  // the stage ring is idle now: the drafted tokens
+  if (fin && blockIdx.x == 0)
+    for (int e = tid; e < a.B * k; e += kGThreads) ds[e] = __ldg(a.d + e);  // in flight while the counters fill
+  for (int b = fin ? (blockIdx.x == 0 ? warp : a.B) : warp * G + blockIdx.x; b < a.B;
+       b += fin ? kWarps : G * kWarps) {
     int w = FUSED ? (int)((fused_wait_ready(a.fs.ready + b, s_epoch) >> 22) & 0x3FFFFFull) : a.windows[b];
     uint32_t bad = (w < 0 || w > k) ? TETRIS_ST_BAD_WINDOW : 0u;
     w = w < 0 ? 0 : (w > k ? k : w);
@@ -454,7 +473,38 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       a.key0[b] = 0ull;  // read above (lane 0, j = 0): ready for the next launch
       a.accepted[b] = acc;
       a.out_tok[b] = tok;
+      if (fin) {
+        s_acc[b] = acc;
+        s_tok[b] = tok;
+      }
       set_status(a.status, bad);
+    }
+  }
+  if (fin && blockIdx.x == 0) {
+    __syncthreads();
+    if (warp == 0) {  // compact_kernel's contract over <= 64 requests: n_b = accepted + 1 (capped), one warp scan
+      int n[2], tot = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int b = lane + 32 * h;
+        n[h] = b < a.B ? min(s_acc[b] + 1, a.cap ? max(__ldg(a.cap + b), 0) : INT_MAX) : 0;
+      }
+      int off[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int incl = warp_incl_scan<int>(n[h], lane);
+        off[h] = tot + incl - n[h];
+        tot += __shfl_sync(kFull, incl, 31);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int b = lane + 32 * h;
+        if (b < a.B) {
+          a.offsets[b] = off[h];
+          for (int j = 0; j < n[h]; ++j) a.tokens[off[h] + j] = j < s_acc[b] ? ds[b * k + j] : s_tok[b];
+        }
+      }
+      if (lane == 0) a.offsets[a.B] = tot;
     }
   }
 
@@ -469,20 +519,21 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       *work = 0ull;
       *reinterpret_cast<unsigned long long*>(a.grid_bar2) = 0ull;
       *done = 0u;
-      if (FUSED) a.fs.ctl[2] = (int)s_epoch;  // the epoch this launch used (every CTA has read it)
+      if (FUSED) {
+        a.fs.ctl[0] = 0;                  // the CTAs counted in by fused_publish
+        a.fs.ctl[2] = (int)s_epoch;       // the epoch this launch used (every CTA has read it)
+      }
       __threadfence();
     }
     s_last = last;
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last || fin) return;
   if (tid == 0) gtime(a, 6);
   if (FUSED) {
-    // the one-launch step (B <= kFusedMaxCells): win_offsets / PolicyStats over every selected row's window and the
-    // compaction, with every load of both in ONE round trip (windows; accepted, out_tok, cap of the thread's rows
-    // [r0, r0 + rpt); the drafted tokens d staged in the now idle stage ring), then on-chip scans and the writes
-    int wr[kFusedMaxRpt];
-    fused_load_windows(a.fs, tid, blockDim.x, wr);
+    // the one-launch step (B <= kFusedMaxRows): the compaction with every load in ONE round trip (accepted, out_tok,
+    // cap of the thread's rows [r0, r0 + rpt); the drafted tokens d staged in the now idle stage ring), then the
+    // on-chip scan and the writes (win_offsets / PolicyStats were written during the stream)
     const int B = a.B, nt = blockDim.x, rpt = (B + nt - 1) / nt, r0 = tid * rpt;
     int acc[kFusedMaxRpt], tok[kFusedMaxRpt], nn[kFusedMaxRpt];
     int32_t* ds = reinterpret_cast<int32_t*>(stage_mem);
@@ -497,7 +548,6 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       }
       for (int e = tid; e < B * k; e += nt) ds[e] = __ldg(a.d + e);
     }
-    fused_win_scan(a.fs, k, tid, nt, s_tmp, wr);  // (its barriers also publish ds)
     if (a.offsets == nullptr) return;
     __syncthreads();
     long long local = 0;
@@ -556,7 +606,11 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
 namespace tetris {
 
 // the one-launch greedy step keeps the selection's scratch in the 6th stage (32 KB)
-bool greedy_fused_fits(int B_sel, int k) { return fused_scratch_bytes(B_sel, k, abi::device_sm_count()) <= kGStageBytes; }
+// (and every own row's window is written by a consumer thread, which the win scan's barrier orders: <= 512 own rows)
+bool greedy_fused_fits(int B_sel, int k) {
+  const int G = abi::device_sm_count();
+  return fused_scratch_bytes(B_sel, k, G) <= kGStageBytes && (B_sel + G - 1) / G <= kGConsumers * 32;
+}
 
 bool persist_greedy_eligible(const float* p, int V) {
   return (V % kLaneElems == 0) && (((uintptr_t)p & 15u) == 0);
