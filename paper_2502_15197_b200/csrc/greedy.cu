@@ -206,7 +206,6 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
     // the previous launch on the stream may have written the inputs: wait for it before the first read; the epoch
     // of this launch (the previous one's + 1, set by its last CTA out)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (tid == 0) s_epoch = (uint32_t)__ldcg(a.fs.ctl + 2) + 1u;
   }
   __syncthreads();
 
@@ -215,7 +214,11 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
     const int NP = kGThreads - 32, pt = warp < kGProducer ? tid : tid - 32;
     const FusedSel& f = a.fs;
     const FusedView v = fused_view(f, k, stage_mem + kGStages * kGStageBytes);
+    // this launch's epoch (the previous one's + 1, set by its last CTA out): loaded beside the scores, published in
+    // shared memory after them (the barriers before phase 3 and the descents make it visible)
+    const uint32_t ep = pt == 0 ? (uint32_t)__ldcg(a.fs.ctl + 2) : 0u;
     fused_stage(f, k, v, pt, NP);
+    if (pt == 0) s_epoch = ep + 1u;
     fused_bar(NP);
     fused_keys(f, k, v, pt, NP, a.status);
     fused_bar(NP);
@@ -234,6 +237,8 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
 
   if (warp == kGProducer) {
     const uint64_t pol = l2_evict_first_policy();
+    // the producer's own copy of this launch's epoch (it takes no part in the prologue's barriers); phase B needs it
+    const uint32_t p_epoch = FUSED ? (uint32_t)__ldcg(a.fs.ctl + 2) + 1u : 0u;
     int t = 0;
     // one item (request b, listed row `row`, chunk c) into the next stage; phase 1: a row-0 item
     auto issue = [&](int b, int row, int cc, int phase) {
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(kGThreads, 1) persist_greedy_kernel(const Gree
       // request's window comes from its ready word (polled until it carries this launch's epoch), rows past it are
       // skipped without a copy
       if (lane == 0) {
-        const uint32_t epoch = s_epoch;
+        const uint32_t epoch = p_epoch;
         const long long per_b = (long long)k * nch, total = (long long)a.B * per_b;
         long long i = (long long)atomicAdd(work, 1ull), i1 = (long long)atomicAdd(work, 1ull);
         int bcur = -1, wb = 0;

@@ -533,11 +533,14 @@ __device__ void fused_select(const StreamArgs& a, uint8_t* smem) {
   const int NP = NT - 32;  // the selection's participants: warps 0 .. 16; warp 17 gathers the verdicts
   const FusedView v = fused_view(f, k, smem);
   __shared__ uint32_t s_epoch;
-  if (tid == 0) s_epoch = (uint32_t)__ldcg(f.ctl + 2) + 1u;  // this launch's epoch (the previous grid is complete)
+  // this launch's epoch (the previous grid is complete): loaded beside the scores, published after them (the barriers
+  // before phase 3 make it visible)
+  const uint32_t ep = tid == 0 ? (uint32_t)__ldcg(f.ctl + 2) : 0u;
   if (tid >= NP) {
     fused_verdicts<BF>(a, v, tid & 31);
   } else {
     fused_stage(f, k, v, tid, NP);
+    if (tid == 0) s_epoch = ep + 1u;
     fused_bar(NP);
     if (tid == 0) gstamp(a, 8);
     fused_keys(f, k, v, tid, NP, a.status);
