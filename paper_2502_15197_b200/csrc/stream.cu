@@ -143,7 +143,7 @@ __device__ __forceinline__ double consume_segment(const uint8_t* __restrict__ sp
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = 0.0;
   }
-  return seg_sum(fold8(w));
+  return fold8(w);  // the lane's sum; the caller runs the segment butterflies (interleaved over its segments)
 }
 
 // A lane's 8 row elements from global memory as fp32 probabilities (zeros past the row end)
@@ -887,6 +887,16 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
         Gs[x] = consume_segment<BF>(sp, sp + stage_row_bytes<BF>(), m.res != 0,
                                     (int64_t)m.c * kChunkElems + seg * kSegElems, seg * kSegElems, a.V, lane, m.lp,
                                     m.lq);
+      }
+      // the segments' balanced trees over the 32 lane sums (the contract's xor butterfly), level by level across the
+      // segments so the shuffle latencies overlap
+#pragma unroll
+      for (int mm = 1; mm < 32; mm <<= 1) {
+        double o[kSegsPerConsumer];
+#pragma unroll
+        for (int x = 0; x < kSegsPerConsumer; ++x) o[x] = __shfl_xor_sync(kFull, Gs[x], mm);
+#pragma unroll
+        for (int x = 0; x < kSegsPerConsumer; ++x) Gs[x] = Gs[x] + o[x];
       }
       __syncwarp();
       if (lane == 0) {
