@@ -199,7 +199,16 @@ __device__ int descend_global(const void* __restrict__ P, const void* __restrict
     double wl[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) wl[i] = RES ? w_res((double)pv[s][i], (double)qv[s][i]) : w_plain((double)pv[s][i]);
-    G[s] = seg_sum(fold8(wl));
+    G[s] = fold8(wl);
+  }
+  // the four segments' butterflies level by level (seg_sum's arithmetic; the shuffle latencies overlap)
+#pragma unroll
+  for (int mm = 1; mm < 32; mm <<= 1) {
+    double o[kWarpSegs];
+#pragma unroll
+    for (int s = 0; s < kWarpSegs; ++s) o[s] = __shfl_xor_sync(kFull, G[s], mm);
+#pragma unroll
+    for (int s = 0; s < kWarpSegs; ++s) G[s] = G[s] + o[s];
   }
   DESCENT_PROBE(5);
   const int s = seq_find(G, kWarpSegs, T);
