@@ -4,6 +4,7 @@
 // 16-byte loads (G CTAs x T threads), (4) the two at once (a fraction of the rows by DMA, the rest by the kernel).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o h2d_rows h2d_rows.cu
 #include <cuda_runtime.h>
+#include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -34,6 +35,58 @@ __global__ void gather_kernel(const int4* __restrict__ host, const long long* __
         if (i + u * blockDim.x < row_words) d[i + u * blockDim.x] = v[u];
     }
   }
+}
+
+// TMA variant: each CTA moves whole rows through a ring of shared-memory stages with bulk copies, host -> shared
+// (cp.async.bulk from the mapped host address) then shared -> device (cp.async.bulk.global.shared::cta)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int S, int CH>
+__global__ void __launch_bounds__(32) tma_gather_kernel(const char* __restrict__ host, const long long* src_row,
+                                                        char* dst, int nrows, long long row_bytes) {
+  extern __shared__ __align__(128) char stage[];
+  __shared__ __align__(8) unsigned long long full[S];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const long long nch = (row_bytes + CH - 1) / CH;
+  long long t = 0;
+  // items (row r of this CTA, chunk c): issue up to S loads ahead, then for each landed stage a bulk store
+  auto issue = [&](long long it) {
+    const int r = blockIdx.x + (int)(it / nch) * gridDim.x;
+    const long long c = it % nch;
+    const long long off = c * CH, n = row_bytes - off < CH ? row_bytes - off : CH;
+    const int s = (int)(it % S);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"((uint32_t)n));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(stage + (size_t)s * CH)),
+                 "l"(host + src_row[r] * row_bytes + off), "r"((uint32_t)n), "r"(smem_u32(&full[s]))
+                 : "memory");
+  };
+  const int myrows = blockIdx.x < nrows ? (nrows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long items = (long long)myrows * nch;
+  for (; t < items && t < S; ++t) issue(t);
+  (void)t;
+  for (long long it = 0; it < items; ++it) {
+    const int s = (int)(it % S);
+    const uint32_t par = (uint32_t)((it / S) & 1);
+    asm volatile("{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n@!p bra W;\n}" ::"r"(
+                     smem_u32(&full[s])),
+                 "r"(par)
+                 : "memory");
+    const int r = blockIdx.x + (int)(it / nch) * gridDim.x;
+    const long long c = it % nch;
+    const long long off = c * CH, n = row_bytes - off < CH ? row_bytes - off : CH;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + (long long)r * row_bytes + off),
+                 "r"(smem_u32(stage + (size_t)s * CH)), "r"((uint32_t)n)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // refill the PREVIOUS item's stage once its store has read it (the newest store may still be in flight)
+    if (it >= 1 && it - 1 + S < items) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      issue(it - 1 + S);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 int main(int argc, char** argv) {
@@ -110,6 +163,23 @@ int main(int argc, char** argv) {
         CK(cudaGetLastError());
         char name[64];
         snprintf(name, 64, "gather kernel %d x %d", G, T);
+        if (w) report(name, reps);
+      }
+    }
+  }
+  // (3b) TMA gather: one CTA (one thread) per SM-slot, S stages of CH bytes
+  {
+    constexpr int S = 6, CH = 32768;
+    CK(cudaFuncSetAttribute(tma_gather_kernel<S, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * CH));
+    for (int G : {148, 296, 592}) {
+      for (int w = 0; w < 2; ++w) {
+        CK(cudaEventRecord(e0, st[0]));
+        for (int r = 0; r < reps; ++r)
+          tma_gather_kernel<S, CH><<<G, 32, S * CH, st[0]>>>(hdev, drows, dst, nrows, row_bytes);
+        CK(cudaEventRecord(e1, st[0]));
+        CK(cudaGetLastError());
+        char name[64];
+        snprintf(name, 64, "TMA gather %d CTAs x %d x %d KB", G, S, CH / 1024);
         if (w) report(name, reps);
       }
     }
