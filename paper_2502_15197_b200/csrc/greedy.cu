@@ -21,7 +21,9 @@
 // unsigned order (NaN above +inf, -0.0 canonicalised to +0.0), low word = ~index (lower index wins a tie).
 // Then, in the same launch, one warp per request (strided over the CTAs) waits for the request's (w_b + 1) · nch
 // chunks, reads the w_b + 1 keys and writes accepted / out_tok; the last CTA out runs the compaction (offsets and
-// tokens, compact_kernel's contract) when asked to.
+// tokens, compact_kernel's contract) when asked to.  One-launch step (the selection as this kernel's prologue, small
+// batches): the windows' scan runs in the last CTA to publish its windows, during the stream; batches of at most
+// kFinRows requests are finished by CTA 0 alone — every descent, then the compaction from shared memory.
 #include <climits>
 
 #include "common.cuh"
