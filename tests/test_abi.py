@@ -136,3 +136,19 @@ def test_nccl_binding_resolves_without_gpu():
     assert b"communicator" in lib.tetris_last_error()
     assert lib.tetris_dist_select_f64(None, None, 0, 4, 8, 0, None, None, None, None, None, None, None, None, 0,
                                       None) == N.INVALID_ARGUMENT
+
+
+def test_plain_c_host_links_the_library(tmp_path):
+    """A C program compiled against include/tetris_b200.h and linked with libtetris_b200.so (no Python / torch in the
+    host) runs the CPU-side entry points: the ABI is consumable by a non-Python host as INTEGRATION.md says."""
+    import shutil
+
+    cc = shutil.which("gcc") or "/usr/bin/gcc"
+    lib_dir = N.LIB_PATH.parent
+    exe = tmp_path / "abi_host"
+    r = subprocess.run([cc, "-O1", "-o", str(exe), str(ROOT / "tests" / "c_host" / "abi_host.c"), "-I",
+                        str(ROOT / "include"), "-L", str(lib_dir), "-ltetris_b200", f"-Wl,-rpath,{lib_dir}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and out.stdout.startswith("ok"), (out.returncode, out.stdout, out.stderr)
