@@ -152,3 +152,21 @@ def test_plain_c_host_links_the_library(tmp_path):
     assert r.returncode == 0, r.stderr
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and out.stdout.startswith("ok"), (out.returncode, out.stdout, out.stderr)
+
+
+@pytest.mark.gpu
+def test_plain_c_host_runs_a_step_on_the_gpu(tmp_path):
+    """The same C host route on the GPU: cudaMalloc'd buffers, tetris_step_stochastic_f32 and tetris_step_greedy_f32
+    on one stream, the step's invariants checked in C (tests/c_host/step_host.c)."""
+    import shutil
+
+    cc = shutil.which("gcc") or "/usr/bin/gcc"
+    lib_dir = N.LIB_PATH.parent
+    exe = tmp_path / "step_host"
+    r = subprocess.run([cc, "-O1", "-o", str(exe), str(ROOT / "tests" / "c_host" / "step_host.c"), "-I",
+                        str(ROOT / "include"), "-I", "/usr/local/cuda/include", "-L", str(lib_dir), "-ltetris_b200",
+                        "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib_dir}",
+                        "-Wl,-rpath,/usr/local/cuda/lib64"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.startswith("ok"), (out.returncode, out.stdout, out.stderr)
