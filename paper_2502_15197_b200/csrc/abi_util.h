@@ -122,8 +122,9 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
   sizes[WS_COUNTERS] = kCounterSlots * 4;
   sizes[WS_GSEL] = kGselScratchBytes;  // shape-independent, right after the counters: a fixed offset in every layout
   if (op & TETRIS_OP_SELECT) {
-    const size_t keys = (size_t)B * k * 8, heap = (size_t)B * 16;  // radix keys / heap-replay items
-    sizes[WS_KEYS] = keys > heap ? keys : heap;
+    // radix keys; or the heap replay's items (16 B per row) followed by its cell keys
+    const size_t keys = (size_t)B * k * 8, heap = (size_t)B * 16;
+    sizes[WS_KEYS] = keys + heap;
   }
   if (op & TETRIS_OP_VERIFY) {
     // rows processed by one verify call: B requests (stochastic/greedy) or R sampled rows (sample_rows)

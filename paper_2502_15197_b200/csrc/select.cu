@@ -521,17 +521,18 @@ __global__ void __launch_bounds__(REG ? kRegMaxThreads : kSelMaxThreads, 1) sele
 // Mirrors CPython heapq (heapify/_siftup/_siftdown) as driven by select_tetris (selector.py:151-170) and counts every
 // _HeapItem.__lt__ (selector.py:128-130).  Single thread by construction: the count is a property of the sequential
 // schedule.
+// Items carry the selection's integer key instead of the double: desc_key(cum) orders like -cum (with -0.0 == +0.0,
+// as Python compares them) and the tie word row << 8 | depth like (row, depth), so one _HeapItem.__lt__ is a 96-bit
+// integer compare (no fp64 compare in the dependent chain).  Scores are validated (no NaN) before this runs.
 struct HeapItem {
-  double cum;
-  int32_t row, depth;
+  uint64_t key;
+  uint32_t tie;
+  uint32_t pad;
 };
 
 __device__ __forceinline__ bool item_lt(const HeapItem& x, const HeapItem& y, long long& cmp) {
   ++cmp;
-  const double nx = -x.cum, ny = -y.cum;  // key = (-cum, row, depth)
-  if (nx != ny) return nx < ny;
-  if (x.row != y.row) return x.row < y.row;
-  return x.depth < y.depth;
+  return x.key < y.key || (x.key == y.key && x.tie < y.tie);  // key = (-cum, row, depth)
 }
 
 __device__ void sift_down(HeapItem* h, int start, int pos, long long& cmp) {
@@ -564,28 +565,27 @@ __device__ void sift_up(HeapItem* h, int n, int pos, long long& cmp) {
   sift_down(h, start, pos, cmp);
 }
 
-// The replay is one dependent chain of heap accesses, so their latency is the cost: the heap (16 B per row) and, when
-// they fit too, the cum values live in shared memory (staged by the whole CTA first); otherwise in the workspace.
-__global__ void heap_stats_kernel(const double* __restrict__ cum_g, const int32_t* __restrict__ len, int B, int k,
-                                  long long C, long long* stats, HeapItem* heap_g, int heap_in_smem,
-                                  int cum_in_smem) {
+// The replay is one dependent chain of heap accesses, so their latency is the cost: the heap (16 B per row), the
+// cells' keys and the row lengths live in shared memory when they fit (staged by the whole CTA first), otherwise
+// the heap and the keys in the workspace.
+__global__ void heap_stats_kernel(const double* __restrict__ cum_g, const int32_t* __restrict__ len_g, int B, int k,
+                                  long long C, long long* stats, HeapItem* heap_g, uint64_t* keys_g,
+                                  int in_smem) {
   extern __shared__ __align__(16) uint8_t hs_smem[];
-  HeapItem* heap = heap_in_smem ? (HeapItem*)hs_smem : heap_g;
-  const double* cum = cum_g;
-  if (cum_in_smem) {
-    double* cs = (double*)(hs_smem + (size_t)B * sizeof(HeapItem));
-    for (long long i = threadIdx.x; i < (long long)B * k; i += blockDim.x) cs[i] = cum_g[i];
-    cum = cs;
-  }
+  HeapItem* heap = in_smem ? (HeapItem*)hs_smem : heap_g;
+  uint64_t* keys = in_smem ? (uint64_t*)(hs_smem + (size_t)B * sizeof(HeapItem)) : keys_g;
+  int* lens = in_smem ? (int*)(keys + (size_t)B * k) : nullptr;
+  for (long long i = threadIdx.x; i < (long long)B * k; i += blockDim.x) keys[i] = desc_key(cum_g[i]);
+  if (lens)
+    for (int r = threadIdx.x; r < B; r += blockDim.x) lens[r] = len_g ? len_g[r] : k;
   __syncthreads();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  auto L_of = [&](int r) { return lens ? lens[r] : (len_g ? len_g[r] : k); };
   long long cmp = 0, extracts = 0, inserts = 0, peak = 0;
   if (C > 0) {
     int n = 0;
-    for (int r = 0; r < B; ++r) {
-      const int L = len ? len[r] : k;
-      if (L > 0) heap[n++] = HeapItem{cum[(int64_t)r * k], r, 1};
-    }
+    for (int r = 0; r < B; ++r)
+      if (L_of(r) > 0) heap[n++] = HeapItem{keys[(int64_t)r * k], (uint32_t)r << 8 | 1u, 0u};
     for (int i = n / 2 - 1; i >= 0; --i) sift_up(heap, n, i, cmp);
     inserts = n;
     peak = n;
@@ -598,10 +598,9 @@ __global__ void heap_stats_kernel(const double* __restrict__ cum_g, const int32_
         sift_up(heap, n, 0, cmp);
       }
       ++extracts;
-      const int r = item.row, j = item.depth;
-      const int L = len ? len[r] : k;
-      if (j < L) {  // heappush
-        heap[n] = HeapItem{cum[(int64_t)r * k + j], r, j + 1};
+      const int r = (int)(item.tie >> 8), j = (int)(item.tie & 0xFFu);
+      if (j < L_of(r)) {  // heappush
+        heap[n] = HeapItem{keys[(int64_t)r * k + j], (uint32_t)r << 8 | (uint32_t)(j + 1), 0u};
         ++n;
         sift_down(heap, 0, n - 1, cmp);
         ++inserts;
@@ -789,14 +788,15 @@ extern "C" int tetris_heap_stats_f64(const double* cum, const int32_t* len, int3
   if (B > 0 && (!ws || ws_bytes < need))
     return abi::fail(TETRIS_INVALID_ARGUMENT, "workspace too small: %zu < %zu", ws_bytes, need);
   constexpr size_t kMaxSmem = 200 * 1024;
-  const size_t heap_b = (size_t)B * sizeof(HeapItem), cum_b = (size_t)B * k * sizeof(double);
-  const int heap_in = heap_b <= kMaxSmem, cum_in = heap_in && heap_b + cum_b <= kMaxSmem;
-  const size_t smem = (heap_in ? heap_b : 0) + (cum_in ? cum_b : 0);
-  cudaError_t e = abi::ensure_smem(heap_stats_kernel, smem);
+  const size_t smem_all = (size_t)B * sizeof(HeapItem) + (size_t)B * k * 8 + (size_t)B * 4;
+  const int in_smem = smem_all <= kMaxSmem;
+  cudaError_t e = abi::ensure_smem(heap_stats_kernel, in_smem ? smem_all : 0);
   if (e != cudaSuccess) return abi::cuda_fail(e);
-  heap_stats_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(
-      cum, len, B, k, (long long)C, (long long*)stats4,
-      (HeapItem*)abi::ws_region(ws, TETRIS_OP_SELECT, B, k, 0, abi::WS_KEYS), heap_in, cum_in);
+  // workspace fallback: the heap in WS_KEYS ([B] items, 16 B each), the cell keys behind it
+  uint8_t* base = (uint8_t*)abi::ws_region(ws, TETRIS_OP_SELECT, B, k, 0, abi::WS_KEYS);
+  heap_stats_kernel<<<1, 256, in_smem ? smem_all : 0, (cudaStream_t)stream>>>(
+      cum, len, B, k, (long long)C, (long long*)stats4, (HeapItem*)base,
+      (uint64_t*)(base + (size_t)B * sizeof(HeapItem)), in_smem);
   return abi::launch_check();
 }
 
