@@ -38,7 +38,6 @@ constexpr int kGStages = 6;
 constexpr int kGConsumers = 16;
 constexpr int kSegsPerWarp = kChunkElems / kSegElems / kGConsumers;  // staged segments per consumer warp
 constexpr int kGProducer = kGConsumers;
-constexpr int kGPublisher = kGConsumers + 1;
 constexpr int kGThreads = (kGConsumers + 2) * 32;
 constexpr int kFinRows = 36;  // one-launch batches up to this many requests: CTA 0 finishes them alone (2 per warp)
 constexpr int kGRing = 64;
