@@ -12,7 +12,9 @@ from paper_2502_15197_b200.synthetic import make_batch  # noqa: E402
 for (B, k, V, C, mode) in [(300, 6, 16384, 900, "stochastic"), (64, 4, 8200, 10, "stochastic"),
                            (200, 8, 8200, 700, "greedy"), (2048, 9, 1024, 9000, "greedy"),
                            (37, 0, 8192, 5, "stochastic"), (37, 0, 8192, 5, "greedy"),  # nothing drafted
-                           (90, 5, 1003, 200, "stochastic"), (90, 5, 1003, 200, "greedy")]:  # V % 8 != 0
+                           (90, 5, 1003, 200, "stochastic"), (90, 5, 1003, 200, "greedy"),  # V % 8 != 0
+                           (16, 5, 32000, 48, "greedy"),  # cfg1: one launch, CTA 0 finishes <= 36 requests alone
+                           (256, 8, 32000, 1200, "stochastic")]:  # cfg2 shape: the one-launch step at 2048 cells
     bt = make_batch(B, k, V, seed=1, mode=mode, ragged=True)
     step = ops.TetrisStep(B, k, V, C, mode=mode)
     for _ in range(2):
