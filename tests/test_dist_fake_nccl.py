@@ -1,4 +1,4 @@
-"""GPU: the native request-sharded entry points (csrc/dist.cu, tetris_dist_*) at world sizes 2 and 4 on ONE B200.
+"""GPU: the native request-sharded entry points (csrc/dist.cu, tetris_dist_*) at world sizes 2, 4 and 8 on ONE B200.
 
 NCCL cannot form a multi-rank communicator on one device, so the library is pointed ($TETRIS_NCCL_LIB) at an
 in-process stand-in (tests/fake_nccl/fake_nccl.cu) whose ncclAllGather is a rendezvous of the W rank threads plus
@@ -58,7 +58,9 @@ def _worker(shim: str) -> list:
                                              (4, 256, 8, 32000, 4000, "stochastic", False),
                                              (2, 1024, 16, 16384, 20000, "stochastic", False),
                                              (2, 128, 8, 8192, 1000, "stochastic", True),
-                                             (4, 16, 5, 32000, 200, "greedy", False)):
+                                             (4, 16, 5, 32000, 200, "greedy", False),
+                                             # SURVEY 8e's determinism check: W = 8 at B = 4096 in total
+                                             (8, 512, 16, 4096, 16384, "stochastic", False)):
             world = fk.fake_nccl_world_create(W)
             comms = [fk.fake_nccl_comm_create(world, r) for r in range(W)]
             if logits:
@@ -138,7 +140,7 @@ def _worker(shim: str) -> list:
         return [traceback.format_exc()]
 
 
-def test_native_sharded_steps_at_world_2_and_4(tmp_path):
+def test_native_sharded_steps_at_world_2_4_8(tmp_path):
     # a fresh interpreter (the NCCL library is resolved once per process), bounded by a timeout so that a
     # rendezvous that never completes fails the test instead of hanging the suite
     shim = _build_shim(tmp_path)
