@@ -37,6 +37,7 @@ struct SelectArgs {
   int32_t* offsets;    // [B+1]
   uint8_t* acc_bytes;  // pre-accept verdicts [ep_rows][k] (nullptr: gather in the epilogue)
   int accept_ctas;     // > 0: CTAs after cluster 0 compute acc_bytes concurrently with the selection
+  int accept_spread;   // select1: spread the accept CTAs over every SM (inputs in mapped host memory, see select1.cu)
   int* acc_counter;    // arrivals of those CTAs (zero between launches)
   long long* dbg;      // diagnostics: per-phase clock64() stamps of CTA 0 (nullptr: off)
   void* gscratch;      // workspace region WS_GSEL (grid selector), zero-initialised

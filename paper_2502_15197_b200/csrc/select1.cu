@@ -35,11 +35,13 @@ struct S1Shared {
 
 // The accept role (CTAs 1..): verify_token (accept_model.py:309-313) on every drafted position of the local rows.
 // Verdict byte: bit0 accept, bit1 draft token outside the vocabulary, bit2 uniform outside [0, 1).
+// CTA acta takes the contiguous positions [acta * per, (acta + 1) * per), per = ceil(n / nacta).
 __device__ void accept_role(const SelectArgs& a, int acta, int nacta) {
   const int k = a.k, nt = blockDim.x, tid = threadIdx.x;
-  const int64_t n = (int64_t)a.ep_rows * k, stride = (int64_t)nacta * nt;
+  const int64_t n = (int64_t)a.ep_rows * k, per = (n + nacta - 1) / nacta;
+  const int64_t e0 = (int64_t)acta * per, e1 = e0 + per < n ? e0 + per : n;
   const int32_t* llen = a.len ? a.len + a.ep_row0 : nullptr;
-  for (int64_t e = (int64_t)acta * nt + tid; e < n; e += stride) {
+  for (int64_t e = e0 + tid; e < e1; e += nt) {
     const int b = (int)(e / k), j = (int)(e - (int64_t)b * k);
     const int L = llen ? llen[b] : k;
     uint8_t v = 0;
@@ -464,7 +466,11 @@ int launch_select1(const SelectArgs& args_in, cudaStream_t st) {
   if (a.acc_bytes && a.accept_ctas > 0) {
     const int num_sms = abi::device_sm_count();
     const long long n = (long long)a.ep_rows * a.k;
-    long long want = (n + nt - 1) / nt;  // one drafted position (two gathers) per thread
+    // one drafted position (two gathers) per thread; or, when the inputs are mapped host memory (the staged step),
+    // every SM but CTA 0's: each scattered read there is a GPU TLB miss over a host pool of many GB, and the misses an
+    // SM can have in flight, not the link, bound the rate — 32768 reads take ~880 us from 8-16 SMs, ~132 us from 147
+    // (tools/micro/h2d_scalars.cu)
+    long long want = a.accept_spread ? (n + 63) / 64 : (n + nt - 1) / nt;
     if (want > num_sms - 1) want = num_sms - 1;
     if (want < 1) want = 1;
     naccept = (int)want;

@@ -492,7 +492,7 @@ static int select_accept_impl(const double* conf, const int32_t* len, int32_t B_
                               int32_t row0, int32_t B, const ProbIn& in, const int32_t* d, const double* u_acc,
                               int32_t u_packed, const int32_t* cap, int32_t V, int32_t* windows, int32_t* win_offsets,
                               int32_t* accepted, int32_t* offsets, int32_t* tokens, int64_t* stats4, uint32_t* status,
-                              void* ws, size_t ws_bytes, tetris_stream_t stream) {
+                              void* ws, size_t ws_bytes, tetris_stream_t stream, bool host_inputs = false) {
   int rc = check_shape(B, k, V);
   if (rc) return rc;
   if (C < 0) return abi::fail(TETRIS_INVALID_ARGUMENT, "capacity must be >= 0, got %lld", (long long)C);
@@ -539,6 +539,7 @@ static int select_accept_impl(const double* conf, const int32_t* len, int32_t B_
     sa.acc_bytes = (uint8_t*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ACCBYTES);
     sa.acc_counter = (int*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_COUNTERS) + abi::kSlotAccCounter;
     sa.accept_ctas = 1;
+    sa.accept_spread = host_inputs ? 1 : 0;
   }
   return launch_select(sa, (cudaStream_t)stream);
 }
@@ -936,7 +937,7 @@ static int staged_impl(const double* conf, const int32_t* len, int32_t B, int32_
                                          (const float*)lp_map, (const float*)lq_map}
                                 : ProbIn{(const float*)p_map, (const float*)q_map, nullptr, nullptr, nullptr, nullptr};
   if ((rc = select_accept_impl(conf, len, B, k, C, 0, B, mapped, d, u_acc, 0, cap, V, windows, win_offsets, accepted,
-                               offsets, tokens, stats4, status, ws, ws_bytes, stream)))
+                               offsets, tokens, stats4, status, ws, ws_bytes, stream, /*host_inputs=*/true)))
     return rc;
   // the rows the selection chose, host -> staging (request b: rows 2b, 2b+1), rowinfo rewritten as staging rows
   long long* rowinfo = (long long*)abi::ws_region(ws, TETRIS_OP_VERIFY, B, k, V, abi::WS_ROWINFO);
