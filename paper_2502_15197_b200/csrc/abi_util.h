@@ -129,7 +129,9 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
   if (op & TETRIS_OP_VERIFY) {
     // rows processed by one verify call: B requests (stochastic/greedy) or R sampled rows (sample_rows)
     sizes[WS_CHUNK_SUMS] = (size_t)B * nch * 8;
-    sizes[WS_WARP_SUMS] = (size_t)B * nch * TETRIS_CHUNK_WARPS * 8;
+    // warp sums; rows of <= kSegSumMaxChunks chunks: the 32 segment sums of every chunk instead (stream.cu)
+    const size_t per_chunk = nch <= 4 ? (size_t)TETRIS_CHUNK_WARPS * TETRIS_WARP_SEGS : (size_t)TETRIS_CHUNK_WARPS;
+    sizes[WS_WARP_SUMS] = (size_t)B * nch * per_chunk * 8;
     sizes[WS_ARG_VAL] = (size_t)B * (k + 1) * (nch > 1 ? nch : 2) * 4;  // also the greedy argmax keys (8 B per row)
     sizes[WS_ARG_IDX] = (size_t)B * (k + 1) * nch * 4;
     sizes[WS_SCRATCH] = align_up((size_t)B * 8) * 3 + align_up((size_t)B * 4);  // residual: rows, u, idx
@@ -137,7 +139,7 @@ inline size_t region_offset(int op, int B, int k, int V, Region which) {
     sizes[WS_ACCBYTES] = (size_t)B * k;  // pre-accept verdicts
     sizes[WS_ROWMAP] = 256 + (size_t)B * (k + 1) * 4;  // greedy: [0] selected-row count, then row -> (b, j)
     // speculative sampler: the phase-A chunk sums then warp sums (B <= kSpecSlots)
-    sizes[WS_SPEC_SUMS] = B <= (int)kSpecSlots ? (size_t)B * nch * 8 * (1 + TETRIS_CHUNK_WARPS) : 0;
+    sizes[WS_SPEC_SUMS] = B <= (int)kSpecSlots ? (size_t)B * nch * 8 * (1 + per_chunk) : 0;
     // logits form: the lse of each request's two rows beside the row info, and of each phase-A list entry's rows
     sizes[WS_ROWLSE] = (size_t)B * 8;
     sizes[WS_SPEC_LSE] = B <= (int)kSpecSlots ? (size_t)B * 8 : 0;

@@ -250,6 +250,56 @@ __device__ int descend_global(const void* __restrict__ P, const void* __restrict
   return (int)(e0 + s * kSegElems + g * kLaneElems + li);
 }
 
+// Rows of at most kSegSumMaxChunks chunks publish the 32 segment sums of every chunk in place of the 8 warp sums (the
+// consumers' values, folded by the publisher in the same order): the descent then knows the segment before it reads the
+// row and re-reads that one segment (8 elements per lane) instead of the warp run's four.
+constexpr int kSegSumMaxChunks = 4;
+constexpr int kChunkSegs = kChunkWarps * kWarpSegs;  // 32
+static_assert(kChunkSegs == 32, "one segment sum per lane");
+
+// descent below the segment level: G = the chosen warp run's four segment sums (as published)
+template <bool RES, bool BF>
+__device__ int descend_seg(const void* __restrict__ P, const void* __restrict__ Q, int64_t e0, int V, int lane,
+                           double T, float lp, float lq, const double (&G)[kWarpSegs]) {
+  const int s = seq_find(G, kWarpSegs, T);
+  if (s < 0) return -1;
+  float pv[8], qv[8];
+  row_lane<BF>(P, e0 + s * kSegElems + lane * kLaneElems, V, lp, pv);
+  if (RES) row_lane<BF>(Q, e0 + s * kSegElems + lane * kLaneElems, V, lq, qv);
+#ifdef TETRIS_DESCENT_PROBE
+  if (pv[0] == -1.f) T = 0.0;  // the loads are in
+#endif
+  DESCENT_PROBE(4);
+  DESCENT_PROBE(5);
+  double w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = RES ? w_res((double)pv[i], (double)qv[i]) : w_plain((double)pv[i]);
+  double lv[5];
+  lv[0] = fold8(w);
+  double x = lv[0];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    x = x + __shfl_xor_sync(kFull, x, 1 << t);
+    lv[t + 1] = x;
+  }
+  int g = 0;
+#pragma unroll
+  for (int t = 4; t >= 0; --t) {
+    const double L = __shfl_sync(kFull, lv[t], g);
+    const double Rr = __shfl_sync(kFull, lv[t], g + (1 << t));
+    if (!(L > T || Rr == 0.0)) {
+      T = T - L;
+      g += 1 << t;
+    }
+  }
+  DESCENT_PROBE(6);
+  double Tl = T;
+  const int li_own = seq_find(w, 8, Tl);
+  const int li = __shfl_sync(kFull, li_own, g);
+  if (li < 0) return -1;
+  return (int)(e0 + s * kSegElems + g * kLaneElems + li);
+}
+
 // Descent for request b after every chunk sum is published (one warp): the chunk and warp sums of all chunks are
 // fetched in one round trip (lane l holds sums l, l+32, ...), then the one warp run holding the sample is re-read.
 template <bool BF>
@@ -262,7 +312,8 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
   const float lp = BF ? a.lse_p[prow] : 0.f;
   const float lq = (BF && qrow >= 0) ? a.lse_q[qrow] : 0.f;
   const double* cs = chunk_sums + (int64_t)b * nch;
-  const double* ws = warp_sums + (int64_t)b * nch * kChunkWarps;
+  const bool segm = nch <= kSegSumMaxChunks;  // warp_sums holds segment sums (32 per chunk)
+  const double* ws = warp_sums + (int64_t)b * nch * (segm ? kChunkSegs : kChunkWarps);
   // nch <= 16: every sum the descent needs in ONE round trip — the chunk sums (lane c holds chunk c) and the
   // nch * 8 warp sums (lane l holds sums l, l + 32, l + 64, l + 96: chunk c's eight are register c / 4, lanes
   // 8 (c % 4) .. + 7).  Larger rows: chunk sums (two per lane) first, the chosen chunk's warp sums second.
@@ -270,9 +321,10 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
   double wv[4];
   double s_lo = lane < nch ? __ldcg(cs + lane) : 0.0;
   double s_hi = lane + 32 < nch ? __ldcg(cs + lane + 32) : 0.0;
-  if (one_trip) {
+  if (one_trip) {  // (segment sums: lane l holds segment l of chunk x in wv[x])
 #pragma unroll
-    for (int x = 0; x < 4; ++x) wv[x] = lane + 32 * x < nch * kChunkWarps ? __ldcg(ws + lane + 32 * x) : 0.0;
+    for (int x = 0; x < 4; ++x)
+      wv[x] = lane + 32 * x < nch * (segm ? kChunkSegs : kChunkWarps) ? __ldcg(ws + lane + 32 * x) : 0.0;
   }
   // accepted-prefix tokens of the compacted stream: every load of the descent's first round trip goes out together
   // (the sums above, the request's counts and uniform, its first 32 drafted tokens)
@@ -318,7 +370,17 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
     DESCENT_PROBE(2);
     // the 8 warp sums of the chosen chunk (from lane cc's registers, or lanes 0..7 load them, then broadcast)
     double Wc[kChunkWarps];
-    if (one_trip) {
+    double sg = 0.0;  // segment mode: lane l holds segment l of the chosen chunk
+    if (segm) {
+      const int c0 = cc < 0 ? 0 : cc;
+      sg = c0 == 0 ? wv[0] : c0 == 1 ? wv[1] : c0 == 2 ? wv[2] : wv[3];
+      // the warp sums, folded as the publisher folds them (four segments left to right), lanes 0..7
+      double xw = 0.0;
+#pragma unroll
+      for (int q = 0; q < kWarpSegs; ++q) xw = xw + __shfl_sync(kFull, sg, (lane & 7) * kWarpSegs + q);
+#pragma unroll
+      for (int w = 0; w < kChunkWarps; ++w) Wc[w] = __shfl_sync(kFull, xw, w);
+    } else if (one_trip) {
       const int c0 = cc < 0 ? 0 : cc, xr = c0 >> 2;
       const double src = xr == 0 ? wv[0] : xr == 1 ? wv[1] : xr == 2 ? wv[2] : wv[3];
 #pragma unroll
@@ -330,13 +392,20 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
     }
     const int ww = seq_find(Wc, kChunkWarps, T);
     DESCENT_PROBE(3);
+    double G[kWarpSegs];
+#pragma unroll
+    for (int q = 0; q < kWarpSegs; ++q) G[q] = __shfl_sync(kFull, sg, ((ww < 0 ? 0 : ww) * kWarpSegs + q) & 31);
     if (cc >= 0 && ww >= 0) {
       const int64_t e0 = (int64_t)cc * kChunkElems + ww * kWarpElems;
       const void* Pr = BF ? (const void*)(a.zp + prow * (int64_t)a.V) : (const void*)(a.p + prow * (int64_t)a.V);
       const void* Qr = !res ? nullptr
                        : BF ? (const void*)(a.zq + qrow * (int64_t)a.V) : (const void*)(a.q + qrow * (int64_t)a.V);
-      tok = res ? descend_global<true, BF>(Pr, Qr, e0, a.V, lane, T, lp, lq)
-                : descend_global<false, BF>(Pr, nullptr, e0, a.V, lane, T, lp, lq);
+      if (segm)
+        tok = res ? descend_seg<true, BF>(Pr, Qr, e0, a.V, lane, T, lp, lq, G)
+                  : descend_seg<false, BF>(Pr, nullptr, e0, a.V, lane, T, lp, lq, G);
+      else
+        tok = res ? descend_global<true, BF>(Pr, Qr, e0, a.V, lane, T, lp, lq)
+                  : descend_global<false, BF>(Pr, nullptr, e0, a.V, lane, T, lp, lq);
     }
   }
   DESCENT_PROBE(7);
@@ -942,6 +1011,7 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
 #pragma unroll
         for (int q = 0; q < kWarpSegs; ++q) x = x + sh.ring_g[slot][lane * kWarpSegs + q];
       }
+      const double gl = sh.ring_g[slot][lane];  // segment `lane` (published instead of the warp sums for short rows)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.ring_free[slot]);
       double S = 0.0;
@@ -950,7 +1020,10 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       const int64_t cs = (int64_t)m.b * nch + m.c;
       double* wsum = (SPEC && m.phase) ? a.warp_sums_spec : a.warp_sums;
       double* csum = (SPEC && m.phase) ? a.chunk_sums_spec : a.chunk_sums;
-      if (lane < kChunkWarps) __stcg(&wsum[cs * kChunkWarps + lane], x);
+      if (nch <= kSegSumMaxChunks)
+        __stcg(&wsum[cs * kChunkSegs + lane], gl);
+      else if (lane < kChunkWarps)
+        __stcg(&wsum[cs * kChunkWarps + lane], x);
       if (lane == 0) __stcg(&csum[cs], S);
       if (lane == npend) pend_b = (SPEC && m.phase) ? ~m.b : m.b;
       if (++npend == 32) flush();

@@ -28,16 +28,19 @@ __global__ void sums_kernel(StreamArgs a) {  // chunk / warp sums of every reque
     const float* P = a.p + (int64_t)a.prow[2 * b] * a.V;
     const float* Q = a.q + (int64_t)a.qrow[2 * b] * a.V;
     double x = 0.0;
+    const bool segm = a.nch <= kSegSumMaxChunks;  // short rows: the 32 segment sums instead of the warp sums
     for (int s = 0; s < kWarpSegs; ++s) {
       const int64_t e = e0 + s * kSegElems + lane * kLaneElems;
       double wl[8];
       for (int i = 0; i < 8; ++i) wl[i] = e + i < a.V ? w_res((double)P[e + i], (double)Q[e + i]) : 0.0;
-      x = x + seg_sum(fold8(wl));
+      const double g = seg_sum(fold8(wl));
+      if (segm && lane == 0) a.warp_sums[((int64_t)b * a.nch + c) * kChunkSegs + w * kWarpSegs + s] = g;
+      x = x + g;
     }
     __shared__ double xs[8];
     if (lane == 0) xs[w] = x;
     __syncthreads();
-    if (threadIdx.x < 8) a.warp_sums[((int64_t)b * a.nch + c) * kChunkWarps + threadIdx.x] = xs[threadIdx.x];
+    if (!segm && threadIdx.x < 8) a.warp_sums[((int64_t)b * a.nch + c) * kChunkWarps + threadIdx.x] = xs[threadIdx.x];
     if (threadIdx.x == 0) {
       double S = 0.0;
       for (int i = 0; i < 8; ++i) S = S + xs[i];
@@ -89,7 +92,7 @@ int main() {
   cudaMalloc(&du, 8 * R);
   cudaMemcpy(du, u.data(), 8 * R, cudaMemcpyHostToDevice);
   cudaMalloc(&cs, 8 * R * nch);
-  cudaMalloc(&ws, 8 * R * nch * 8);
+  cudaMalloc(&ws, (size_t)kChunkSegs * R * nch * 8);  // segment sums (short rows) or warp sums
   cudaMalloc(&mass, 8 * R);
   cudaMalloc(&tok, 4 * R);
   cudaMalloc(&cyc, 16 * R);
