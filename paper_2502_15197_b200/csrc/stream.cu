@@ -512,46 +512,43 @@ __device__ int stream_list(const StreamArgs& a, PersistShared& sh, uint8_t* stag
 // ---- the selection fused into the sampler's launch (FUSED variant, B_sel * k <= kFusedMaxCells) ------------------
 // fused_select.cuh's rank selection on all 576 threads, with this kernel's per-row epilogue: verify_token's first
 // rejection among the selected positions (accept_model.py:309-313, sim_engine.py:397-401) from verdicts gathered in
-// the selection's first round trip, the row to resample from, and — in the last CTA to publish — the compaction
-// offsets.  The producers wait for every CTA's rows (ctl[0] == G), the descents for the scans (ctl[1]).
-// The last CTA to count itself in (ctl[0]) writes win_offsets / PolicyStats (selector.py:150-170) and the compaction
-// offsets from every CTA's published rows, then raises ctl[1] (the descents wait for it).  Run by the 16 consumer
-// warps after the producer has started streaming, so it reads global memory only (the prologue's shared scratch is
-// the stage ring by then).
+// the selection's first round trip, the row to resample from, and the compaction offsets.  Every CTA counts itself in
+// (ctl[0]) once its rows are written; the producers poll per-request ready words, the descents wait for the scans
+// (ctl[1]).  The scans — win_offsets / PolicyStats (selector.py:150-170) and the compaction offsets over every CTA's
+// published rows — are run in the last CTA to count itself in: by its extra scanner warp while the other warps stream
+// (B_sel <= 32 * kFusedMaxRpt), else by its 16 consumer warps before they consume (global memory only: the prologue's
+// shared scratch is the stage ring by then).
 template <bool BF>
 __device__ void fused_scans(const StreamArgs& a, int pt, int nt) {
   const FusedSel& f = a.fs;
-  __shared__ int s_last;
   __shared__ long long s_tmp[33];
-  if (fused_publish(f, pt, nt, &s_last)) {
-    if (pt == 0) gstamp(a, 11);
-    int wr[kFusedMaxRpt], nr[kFusedMaxRpt];
-    fused_load_windows(f, pt, nt, wr);  // both scans' inputs in one round trip
-    const int R = a.R, rpl = (R + nt - 1) / nt, l0 = pt * rpl;
+  if (pt == 0) gstamp(a, 11);
+  int wr[kFusedMaxRpt], nr[kFusedMaxRpt];
+  fused_load_windows(f, pt, nt, wr);  // both scans' inputs in one round trip
+  const int R = a.R, rpl = (R + nt - 1) / nt, l0 = pt * rpl;
 #pragma unroll
-    for (int i = 0; i < kFusedMaxRpt; ++i) {
-      const int lr = l0 + i;
-      nr[i] = (i < rpl && lr < R) ? __ldcg(f.accepted + lr) + 1 : 0;
-      if (f.cap && i < rpl && lr < R) nr[i] = min(nr[i], max(__ldg(f.cap + lr), 0));
-    }
-    fused_win_scan(f, a.k, pt, nt, s_tmp, wr);
-    long long my = 0;
-#pragma unroll
-    for (int i = 0; i < kFusedMaxRpt; ++i) my += nr[i];
-    long long etot;
-    long long eex = fused_excl_scan<long long>(my, s_tmp, etot, pt, nt);
-#pragma unroll
-    for (int i = 0; i < kFusedMaxRpt; ++i) {
-      const int lr = l0 + i;
-      if (i < rpl && lr < R) {
-        f.offsets[lr] = (int32_t)eex;
-        eex += nr[i];
-      }
-    }
-    if (pt == 0) f.offsets[R] = (int32_t)etot;
-    fused_release_done(f, pt, nt);
-    if (pt == 0) gstamp(a, 12);
+  for (int i = 0; i < kFusedMaxRpt; ++i) {
+    const int lr = l0 + i;
+    nr[i] = (i < rpl && lr < R) ? __ldcg(f.accepted + lr) + 1 : 0;
+    if (f.cap && i < rpl && lr < R) nr[i] = min(nr[i], max(__ldg(f.cap + lr), 0));
   }
+  fused_win_scan(f, a.k, pt, nt, s_tmp, wr);
+  long long my = 0;
+#pragma unroll
+  for (int i = 0; i < kFusedMaxRpt; ++i) my += nr[i];
+  long long etot;
+  long long eex = fused_excl_scan<long long>(my, s_tmp, etot, pt, nt);
+#pragma unroll
+  for (int i = 0; i < kFusedMaxRpt; ++i) {
+    const int lr = l0 + i;
+    if (i < rpl && lr < R) {
+      f.offsets[lr] = (int32_t)eex;
+      eex += nr[i];
+    }
+  }
+  if (pt == 0) f.offsets[R] = (int32_t)etot;
+  fused_release_done(f, pt, nt);
+  if (pt == 0) gstamp(a, 12);
 }
 
 // The own cells' accept verdicts (verify_token, accept_model.py:309-313) by ONE warp — the publisher's, idle until
@@ -674,7 +671,8 @@ __device__ void fused_select(const StreamArgs& a, uint8_t* smem) {
 }
 
 template <bool SPEC, bool BF, bool FUSED = false>
-__global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_stream_kernel(const StreamArgs a) {
+__global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 1)
+    persist_stream_kernel(const StreamArgs a) {
   constexpr int kStages = Elem<BF>::kStages;
   extern __shared__ __align__(128) uint8_t stage_mem[];
   __shared__ PersistShared sh;
@@ -942,7 +940,10 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
     __syncwarp();
   } else if (warp < kConsumerWarps) {
     // ---------------------------------------------------------------- consumers
-    if (FUSED) fused_scans<BF>(a, tid, kConsumerWarps * 32);
+    if (FUSED && a.fs.B_sel > 32 * kFusedMaxRpt) {  // large selections: the consumers count in and scan
+      __shared__ int s_last;
+      if (fused_publish(a.fs, tid, kConsumerWarps * 32, &s_last)) fused_scans<BF>(a, tid, kConsumerWarps * 32);
+    }
     for (int t = 0;; ++t) {
       const int s = t % kStages;
       mbar_wait(&sh.full[s], (uint32_t)((t / kStages) & 1));
@@ -1070,6 +1071,20 @@ __global__ void __launch_bounds__(kPersistThreads + (SPEC ? 32 : 0), 1) persist_
       mbar_arrive(&sx.listB_ready);  // release (CTA scope): the list is visible to the producer's wait
     }
     __syncwarp();
+  } else if (FUSED) {
+    // ---------------------------------------------------------------- scanner (one-launch step)
+    // Counts the CTA in (its rows were written before the prologue's last __syncthreads); in the last CTA to count in
+    // it runs the scans while the other warps stream — no consumer waits for them (small selections; larger ones are
+    // scanned by the consumers, above).
+    if (a.fs.B_sel <= 32 * kFusedMaxRpt) {
+      int last = 0;
+      if (lane == 0) last = atomic_add_acq_rel_gpu(a.fs.ctl, 1) == (int)gridDim.x - 1;
+      last = __shfl_sync(kFull, last, 0);
+      if (last) {
+        __threadfence();
+        fused_scans<BF>(a, lane, 32);
+      }
+    }
   }
   if (a.req_cnt != nullptr) {
     // Descent, one warp per request (requests strided over the CTAs so the re-reads spread over all SMs), as soon
@@ -1270,7 +1285,7 @@ int launch_persist_stream(const StreamArgs& a_in, cudaStream_t st) {
   const long long items = (long long)a.R * a.nch;
   // fused: every SM (the selection's rank work is spread over the CTAs, and more CTAs shorten it)
   const int grid = fused ? g_num_sms : (int)(items < g_num_sms ? items : g_num_sms);
-  const int threads = kPersistThreads + (spec ? 32 : 0);
+  const int threads = kPersistThreads + ((spec || fused) ? 32 : 0);  // + the planner / scanner warp
   if (a.req_cnt != nullptr) {
     // one launch: streaming + per-request completion counters + descent
     cudaLaunchConfig_t cfg = {};
