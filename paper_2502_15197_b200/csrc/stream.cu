@@ -602,7 +602,7 @@ __device__ void fused_verdicts(const StreamArgs& a, const FusedView& v, int lane
 }
 
 template <bool BF>
-__device__ void fused_select(const StreamArgs& a, uint8_t* smem) {
+__device__ uint32_t fused_select(const StreamArgs& a, uint8_t* smem) {
   const FusedSel& f = a.fs;
   const int tid = threadIdx.x, NT = blockDim.x, G = gridDim.x, g = blockIdx.x, k = a.k;
   const int NP = NT - 32;  // the selection's participants: warps 0 .. 16; warp 17 gathers the verdicts
@@ -668,6 +668,7 @@ __device__ void fused_select(const StreamArgs& a, uint8_t* smem) {
   // the stage ring is written by the TMA engine (async proxy) after these generic shared-memory accesses
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  return epoch;  // this launch's epoch, for the producer's ready-word polls (no reload of ctl[2])
 }
 
 template <bool SPEC, bool BF, bool FUSED = false>
@@ -757,6 +758,7 @@ __global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 
     if (tid == 0) gstamp(a, 1);
   }
   long long f_i0 = 0, f_i1 = 0;
+  uint32_t f_epoch = 0;
   if (FUSED) {
     // the producer's first two claims go out before the selection, so their round trip overlaps it (the counter was
     // reset by the previous launch, complete after griddepcontrol.wait)
@@ -764,7 +766,7 @@ __global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 
       f_i0 = (long long)atomicAdd(work, 1ull);
       f_i1 = (long long)atomicAdd(work, 1ull);
     }
-    fused_select<BF>(a, stage_mem);
+    f_epoch = fused_select<BF>(a, stage_mem);
   }
 
   if (warp == kProducerWarp) {
@@ -775,7 +777,7 @@ __global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 
         // word (polled until it carries this launch's epoch — no wait for the other CTAs' selection work), the next
         // item's word read while the current copy waits for its stage
         const uint64_t pol = l2_evict_normal_policy();
-        const uint32_t epoch = (uint32_t)__ldcg(a.fs.ctl + 2) + 1u;
+        const uint32_t epoch = f_epoch;
         long long i = f_i0, i1 = f_i1;
         unsigned long long w = i < total ? fused_wait_ready(a.fs.ready + i / nch, epoch) : 0ull;
         gstamp(a, 7);
