@@ -997,6 +997,12 @@ __global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 
     // relaxed increment per chunk (lane i for the i-th pending chunk).  Phase-A chunks go to their own sums and
     // counters.
     int pend_b = 0, npend = 0;
+#ifndef TETRIS_FLUSH_SMALL
+#define TETRIS_FLUSH_SMALL 2  // A/B (tools/gpurun_calls/r2ar.sh): 1 / 2 / 4 / 32 -> cfg2 23.86 / 22.53 / 22.72 / 22.76 us
+#endif
+    // small streams (a few items per CTA): publish sooner, so a request's descent need not wait for the end of every
+    // stream that carried one of its chunks
+    const int flush_every = total <= 2048 ? TETRIS_FLUSH_SMALL : 32;
     auto flush = [&]() {
       if (npend == 0 || a.req_cnt == nullptr) return;
       __syncwarp();
@@ -1029,7 +1035,7 @@ __global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 
         __stcg(&wsum[cs * kChunkWarps + lane], x);
       if (lane == 0) __stcg(&csum[cs], S);
       if (lane == npend) pend_b = (SPEC && m.phase) ? ~m.b : m.b;
-      if (++npend == 32) flush();
+      if (++npend == flush_every) flush();
     }
     flush();
     if (lane == 0) gstamp(a, 5);
