@@ -53,3 +53,7 @@ for i, d in enumerate(dbgs):
               rel(col(1).median()), rel(col(3).max()), rel(col(4).median()), rel(col(4).max())))
     if len(col(6)):
         print("        last CTA elected %.2f, its scans + compaction done %.2f" % (rel(col(6).max()), rel(col(7).max())))
+    print("        per slot (min / median / max over CTAs):",
+          " ".join("s%d %.2f/%.2f/%.2f" % (j, rel(col(j).min()), rel(col(j).median()), rel(col(j).max()))
+                   for j in range(8) if len(col(j))))
+    print("        CTA 0:", " ".join("s%d %.2f" % (j, rel(float(st[0, j]))) for j in range(8) if int(st[0, j]) > 0))
