@@ -345,7 +345,9 @@ __device__ void finalize_request(const StreamArgs& a, int b, bool res, int lane,
   double mass = 0.0;
   for (int c = 0; c < nch; ++c) mass = mass + __shfl_sync(kFull, c < 32 ? s_lo : s_hi, c & 31);
   int tok = -1;
+#ifndef TETRIS_VERDICT_STAMP
   if (lane == 0 && b == (int)blockIdx.x) gstamp(a, 15);  // diagnostics: the first round trip is in
+#endif
   if (mass > 0.0) {
     double T = u * mass;
     // chunk level (left to right), then warp level of the chosen chunk
@@ -613,6 +615,9 @@ __device__ uint32_t fused_select(const StreamArgs& a, uint8_t* smem) {
   const uint32_t ep = tid == 0 ? (uint32_t)__ldcg(f.ctl + 2) : 0u;
   if (tid >= NP) {
     fused_verdicts<BF>(a, v, tid & 31);
+#ifdef TETRIS_VERDICT_STAMP  // diagnostics only: slot 15 = the verdict warp done (instead of the descent's sums)
+    if ((tid & 31) == 0) gstamp(a, 15);
+#endif
   } else {
     fused_stage(f, k, v, tid, NP);
     if (tid == 0) s_epoch = ep + 1u;
