@@ -207,30 +207,15 @@ __device__ inline void fused_ranks_rows(const FusedView& v, int k, int pt, int n
         n[j] = 0u;
       }
       int o = sub;
-      for (; o + 3 * nsub < rs; o += 4 * nsub) {  // 4 loads in flight
-        uint64_t x[4];
-#pragma unroll
-        for (int y = 0; y < 4; ++y) x[y] = v.keys[o + y * nsub];
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-#pragma unroll
-          for (int j = 0; j < KM; ++j) n[j] = add_ge(n[j], km[j], x[y]);
-      }
+      // one load per step: a thread scans Np / nsub keys (8 at cfg2, 64 at most), and this one-shot code runs from a
+      // cold instruction cache — the 4-loads-in-flight variant's larger body was slower (cfg2 22.48 -> 22.41 us, cfg1
+      // 11.39 -> 11.31 us without it, tools/gpurun_calls/r2aw.sh)
       for (; o < rs; o += nsub) {
         const uint64_t x = v.keys[o];
 #pragma unroll
         for (int j = 0; j < KM; ++j) n[j] = add_ge(n[j], km[j], x);
       }
       o = re + sub;
-      for (; o + 3 * nsub < Np; o += 4 * nsub) {
-        uint64_t x[4];
-#pragma unroll
-        for (int y = 0; y < 4; ++y) x[y] = v.keys[o + y * nsub];
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-#pragma unroll
-          for (int j = 0; j < KM; ++j) n[j] = add_ge(n[j], km1[j], x[y]);
-      }
       for (; o < Np; o += nsub) {
         const uint64_t x = v.keys[o];
 #pragma unroll
