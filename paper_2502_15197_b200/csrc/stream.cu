@@ -788,7 +788,6 @@ __global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 
         gstamp(a, 7);
         int t = 0;
         while (i < total) {
-          const long long i2 = (long long)atomicAdd(work, 1ull);
           const unsigned long long w1 = i1 < total ? __ldcg(a.fs.ready + i1 / nch) : 0ull;
           const long long prow = (long long)((w >> 22) & 0x3FFFFFull), qrow = (long long)(w & 0x3FFFFFull) - 1;
           float lp = 0.f, lq = 0.f;
@@ -798,6 +797,9 @@ __global__ void __launch_bounds__(kPersistThreads + ((SPEC || FUSED) ? 32 : 0), 
           }
           if (t == 0) gstamp(a, 2);
           issue_item<BF>(a, sh, stage_mem, t++, (int)(i / nch), (int)(i % nch), prow, qrow, 0, pol, lp, lq);
+          // the next claim goes out after the copy (its round trip is only needed a whole item later; issued before
+          // the copy it delayed every copy: cfg2 22.40 -> 22.15 us, tools/gpurun_calls/r2az.sh)
+          const long long i2 = (long long)atomicAdd(work, 1ull);
           i = i1;
           i1 = i2;
           if (i < total) w = fused_ready(w1, epoch) ? w1 : fused_wait_ready(a.fs.ready + i / nch, epoch);
